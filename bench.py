@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Headline benchmark: dual 2048x2048 eyebuffers of the full-size synthetic VR-NeRF model
+(BASELINE.json config C3 at N=1, C4's dynamic row balancing at N>1), Mrays/s and fps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config C3]
+
+A step is one stereo frame (2 x 2048^2 = 8,388,608 rays) along the 120-frame head path.
+N>1 runs under torch.distributed.run, one rank per GPU (NCCL), rows of the stacked dual-eye
+image split by the throughput-proportional scheduler and gathered to rank 0 each frame.
+Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mrays/sec and fps for dual 2K×2K eyebuffers at 1/2/4/8 B200 vs CPU ref"
+UNIT = "Mrays/s"
+GATHER_BYTES_PER_LEVEL_SAMPLE = 8 * 2 * 4  # 8 corners x 2 features x fp32
+MLP_FLOP_PER_SAMPLE = 18944  # 9,472 MACs per evaluated sample
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C3", choices=["C2", "C3", "C4", "C5"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU time of the reference baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def load_scene(spec):
+    """Synthetic bake of SURVEY.md §8d: seeded parameters + the reference-baked occupancy."""
+    import paper_2311_02542_b200 as L
+    g = L.HashGridConfig(spec.levels, spec.features_per_level, spec.base_resolution,
+                         spec.per_level_scale, spec.table_size)
+    field = L.RadianceField.synthetic(L.FieldConfig(grid=g), spec.seed, spec.amplitude)
+    if spec.dense_occupancy:
+        grid = L.OccupancyGrid(spec.occ_res)
+    else:
+        z = np.load(os.path.join(ROOT, "tests", "golden",
+                                 f"occ_{spec.name.replace('-dense', '')}.npz"))
+        res = int(z["res"])
+        grid = L.OccupancyGrid(res, np.unpackbits(z["bits"])[: res ** 3])
+    return field, grid
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap",
+              "utilization.gpu"]
+
+    def __init__(self, device: int):
+        self.device, self.proc, self.lines = device, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) == len(self.FIELDS):
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        busy = [r for r in rows if r[6].isdigit() and int(r[6]) > 0] or rows
+        sm = sorted(float(r[0]) for r in busy if r[0].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in busy for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": float(busy[0][1]) if busy[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(busy)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch from the committed ncu --set full capture, if any."""
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        k = prof["kernels"].get(kernel)
+        return None if k is None else k.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- reference
+
+def reference_model(spec):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    ref = O.Reference()
+    cfg = O.field_config(spec.levels, spec.features_per_level, spec.base_resolution,
+                         spec.per_level_scale, spec.table_size, spec.hidden_width,
+                         spec.bottleneck, 0)
+    field, grid = load_scene(spec)  # host-only parts of the product: params + occupancy bits
+    p = O.Params(cfg, field.grid_params, field.density_params, field.color_params)
+    return O, ref, ref.model(p, grid.bits, grid.res)
+
+
+def reference_sample(O, ref, model, cam_spec, target_s, threads):
+    """Times the reference run_frame (scheduler.cpp:114) over a centred band of rows of one
+    eye, sized to take ~target_s seconds; returns (rays/s, rows, seconds)."""
+    cam = O.camera(cam_spec.rot, cam_spec.origin, cam_spec.fx, cam_spec.fy, cam_spec.cx,
+                   cam_spec.cy, cam_spec.width, cam_spec.height, cam_spec.t_near, cam_spec.t_far)
+    opts = O.render_options()
+    mid = cam_spec.height // 2
+    rows = max(threads, 2)
+    ms, _ = ref.run_frame(model, cam, opts, mid - rows // 2, mid - rows // 2 + rows, threads)
+    rate = rows * cam_spec.width / (ms / 1000.0)
+    rows = int(min(cam_spec.height, max(threads, target_s * rate / cam_spec.width)))
+    b = max(0, mid - rows // 2)
+    ms, _ = ref.run_frame(model, cam, opts, b, b + rows, threads)
+    return rows * cam_spec.width / (ms / 1000.0), rows, ms / 1000.0
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2311_02542_b200 import scenes
+    cfg = scenes.CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    try:
+        O, ref, model = reference_model(cfg.model)
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"reference build missing: {e}"}))
+        return
+    rays_frame = cfg.eyes * cfg.eye_size ** 2
+    rot, origin = scenes.head_pose(0)
+    eye = scenes.eye_cameras(cfg.eye_size, rot, origin)[0]
+    per_step_s = min(6.0, max(1.0, 120.0 / max(args.steps + args.warmup, 1)))
+    rate, rows, _ = reference_sample(O, ref, model, eye, per_step_s, threads)
+    for _ in range(max(args.warmup - 1, 0)):
+        reference_sample(O, ref, model, eye, per_step_s, threads)
+    rates = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, rows, _ = reference_sample(O, ref, model, eye, per_step_s, threads)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    mrays = float(np.mean(rates)) / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(mrays, 6), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(wall * 1000 / max(args.steps, 1), 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64 geometry / f32 field",
+        "data": "synthetic (seeded init_random + reference-baked occupancy)",
+        "config": {"workload": f"{args.config}: {cfg.description}", "eye_size": cfg.eye_size,
+                   "eyes": cfg.eyes, "table_size": cfg.model.table_size,
+                   "rays_per_frame": rays_frame, "parallelism": f"{threads} host threads"},
+        "fps": round(mrays * 1e6 / rays_frame, 6),
+        "cpu_baseline": {"value": round(mrays, 6), "unit": UNIT, "cores": threads,
+                         "kind": "reference",
+                         "sample": f"run_frame over {rows} centred rows x {cfg.eye_size} of the "
+                                   f"left eye per step, simd={ref.simd_name()}"},
+        "e2e": {"value": round(mrays, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------- ours
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2311_02542_b200 as L
+    from paper_2311_02542_b200 import _abi, scenes
+    from paper_2311_02542_b200.multigpu import StereoFrameDriver
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = scenes.CONFIGS[args.config]
+    spec = cfg.model
+    field, grid = load_scene(spec)
+    dm = L.DeviceModel(field, grid, local)
+    opts = L.RenderOptions()
+    drv = StereoFrameDriver(torch, dm, cfg.eye_size, opts, rank, world, dist=dist if world > 1 else None,
+                            counters=True)
+    rays_frame = drv.H * drv.W
+
+    for f in range(args.warmup):
+        drv.frame(f)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    drv.stats.zero_()
+    drv.launches = 0
+    kernel_ms = 0.0
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t_start.record()
+        for k in range(args.steps):
+            st = drv.frame(args.warmup + k)
+            kernel_ms += st.worker_ms[rank]
+        t_end.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    elapsed = float(t_start.elapsed_time(t_end))
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    counters = drv.counters()
+    launches = drv.launches
+    if world > 1:
+        t = torch.tensor([float(x) for x in counters] + [float(launches), kernel_ms],
+                         dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        counters = t[:4].cpu().numpy()
+        launches = int(t[4].item())
+    sec = elapsed / 1000.0
+    value = rays_frame * args.steps / sec / 1e6
+    fps = args.steps / sec
+
+    # ---- end to end through the public API with host buffers -------------------------
+    e2e_steps = max(1, args.e2e_steps)
+    d2h = 3 * rays_frame * 4
+    h2d = 2 * (C.sizeof(_abi.CameraDesc) + C.sizeof(_abi.RenderOptionsDesc))
+    if world == 1:
+        host = torch.empty((cfg.eyes, 3, cfg.eye_size, cfg.eye_size), dtype=torch.float32).pin_memory()
+        host_np = host.numpy()
+        cams = drv.cameras(0)
+        dm.render_rows(cams[0], opts, 0, cfg.eye_size, host_np[0])  # warm
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
+            cams = drv.cameras(k)
+            for eye in range(cfg.eyes):
+                dm.render_rows(cams[eye], opts, 0, cfg.eye_size, host_np[eye])
+        e2e_s = time.perf_counter() - t0
+    else:
+        host = torch.empty((3, drv.H, drv.W), dtype=torch.float32).pin_memory()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
+            drv.frame(k)
+            if rank == 0:
+                host.copy_(drv.rgb, non_blocking=True)
+            torch.cuda.synchronize()
+        dist.barrier()
+        e2e_s = time.perf_counter() - t0
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = rays_frame * e2e_steps / e2e_s / 1e6
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    evals, level_samples, candidates, rays = (float(x) for x in counters)
+    gather_bytes = level_samples * GATHER_BYTES_PER_LEVEL_SAMPLE
+    kernel_s = kernel_ms / 1000.0  # rank-0 render launches (this rank's share at N>1)
+    frac_rank = 1.0 / world
+    achieved = gather_bytes * frac_rank / kernel_s / 1e9 if kernel_s > 0 else None
+    mlp_tflops = evals * frac_rank * MLP_FLOP_PER_SAMPLE / kernel_s / 1e12 if kernel_s > 0 else None
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            O, ref, model = reference_model(spec)
+            rot, origin = scenes.head_pose(0)
+            eye = scenes.eye_cameras(cfg.eye_size, rot, origin)[0]
+            threads = os.cpu_count() or 1
+            rate, rows, secs = reference_sample(O, ref, model, eye, args.cpu_seconds, threads)
+            cpu = {"value": round(rate / 1e6, 6), "unit": UNIT, "cores": threads,
+                   "kind": "reference",
+                   "sample": f"reference run_frame over {rows} centred rows x {cfg.eye_size} of "
+                             f"the left eye ({rows * cfg.eye_size} rays, {secs:.1f}s), "
+                             f"simd={ref.simd_name()}"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(elapsed / args.steps, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64 geometry / f32 field", "data": "synthetic (seeded init_random + reference-baked occupancy)",
+        "config": {"workload": f"{args.config}: {cfg.description}", "eye_size": cfg.eye_size,
+                   "eyes": cfg.eyes, "table_size": spec.table_size, "rays_per_frame": rays_frame,
+                   "samples_per_ray": opts.samples_per_ray, "parallelism": f"rows{world}",
+                   "l2": "inputs larger than L2 (hash table %.0f MB fp32)" % (field.grid_params.nbytes / 1e6),
+                   "kernel": "k_render_simt"},
+        "fps": round(fps, 3),
+        "work": {"evals_per_ray": round(evals / max(rays, 1), 3),
+                 "active_levels_per_eval": round(level_samples / max(evals, 1), 3),
+                 "candidates_per_ray": round(candidates / max(rays, 1), 3)},
+        "roofline": {"bound": "hbm", "achieved": None if achieved is None else round(achieved, 1),
+                     "peak": hbm, "unit": "GB/s",
+                     "frac": None if achieved is None else round(achieved / hbm, 4),
+                     "traffic": ncu_traffic("k_render_simt"),
+                     "algorithmic": "64 B per active (w_l>0) level-sample: 8 corners x 2 fp32"},
+        "roofline_mlp": {"bound": "tensor", "achieved": None if mlp_tflops is None else round(mlp_tflops, 2),
+                         "peak": peaks.get("bf16_tflops_sustained", 1398.6), "unit": "TFLOP/s",
+                         "algorithmic": "18,944 FLOP per evaluated sample"},
+        "clocks": clk.summary(),
+        "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "lumi_render_rows (C ABI, host buffers)" if world == 1 else
+                        "StereoFrameDriver + D2H of the gathered frame"},
+        "gpu_launches": launches,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

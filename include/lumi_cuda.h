@@ -1,0 +1,187 @@
+/*
+ * lumi_cuda.h -- C ABI of the B200-native VR-NeRF frame renderer.
+ *
+ * This is the drop-in boundary for the reference's rendering path: every entry point
+ * takes plain pointers, sizes and POD descriptors (no CUDA, C++ or torch types; CUDA
+ * streams are passed as `void*`), returns a LUMI_* status and leaves a thread-local
+ * message in lumi_last_error().  The C++ shim in include/lumi/cuda_renderer.h binds the
+ * reference API (proj/include/lumi/renderer.h) onto it; INTEGRATION.md shows the binding.
+ *
+ * Reference interfaces replaced (paths relative to the reference checkout):
+ *   lumi_render_rows            render_rows<FieldT>          proj/include/lumi/renderer.h:252-278
+ *   lumi_render_rows_async      (device-resident form of the same, one stream per worker)
+ *   lumi_march_kept_async       march_ray occupancy skip     proj/include/lumi/renderer.h:205-208
+ *   lumi_model_create           RadianceField<float> + OccupancyGrid state
+ *                               proj/include/lumi/field.h:65-93, grid.h:58-74,
+ *                               network.h:144-159, occupancy.h:32-100
+ *   lumi_field_layout           MultiResHashGrid layout      proj/include/lumi/grid.h:58-74
+ *   lumi_synth_params           RadianceField::init_random   proj/include/lumi/field.h:88-93
+ *   lumi_bake_occupancy         OccupancyGrid::probe + prune proj/src/occupancy.cpp:97-154
+ *   lumi_equal_assignment, lumi_assign_rows, lumi_next_assignment, lumi_aggregate_stats
+ *                               the row scheduler            proj/src/scheduler.cpp:18-162
+ *
+ * All device work is sm_100a CUDA (paper_2311_02542_b200/csrc); there is no CPU
+ * fallback -- without a usable B200 the calls fail with LUMI_ERR_CUDA.
+ */
+#ifndef LUMI_CUDA_H
+#define LUMI_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LUMI_ABI_VERSION 1
+#define LUMI_MAX_LEVELS 16
+
+enum {
+  LUMI_OK = 0,
+  LUMI_ERR_INVALID = 1,     /* bad argument; the reference raises lumi::Error */
+  LUMI_ERR_CUDA = 2,        /* CUDA runtime failure / no device */
+  LUMI_ERR_UNSUPPORTED = 3, /* configuration outside what the kernels implement */
+};
+
+/* proj/include/lumi/grid.h:18-29 + proj/include/lumi/field.h:22-27 */
+typedef struct LumiFieldDesc {
+  int32_t levels;             /* <= LUMI_MAX_LEVELS */
+  int32_t features_per_level; /* must be 2 */
+  int32_t base_resolution;
+  int32_t hidden_width; /* must be 64 */
+  double per_level_scale;
+  uint32_t table_size; /* power of two */
+  int32_t bottleneck;  /* must be 16 */
+  int32_t color_space; /* 0 = kPq (sigmoid head), 1 = kLinear (trunc_exp head) */
+  int32_t _pad;
+} LumiFieldDesc;
+
+/* MultiResHashGrid storage layout (grid.h:58-74): one float array, level l at
+   offset[l] floats, entry e at +e*features_per_level. */
+typedef struct LumiGridLayout {
+  int32_t levels;
+  int32_t features_per_level;
+  int32_t resolution[LUMI_MAX_LEVELS];
+  uint32_t entries[LUMI_MAX_LEVELS];
+  uint8_t dense[LUMI_MAX_LEVELS];
+  uint64_t offset[LUMI_MAX_LEVELS];
+  uint64_t total_floats;
+  uint64_t density_params; /* floats, weights then bias per layer (network.h:144-151) */
+  uint64_t color_params;
+} LumiGridLayout;
+
+/* proj/include/lumi/camera.h:15-23 (pose row-major world <- camera) */
+typedef struct LumiCameraDesc {
+  double rot[9];
+  double origin[3];
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  double t_near, t_far;
+} LumiCameraDesc;
+
+/* proj/include/lumi/renderer.h:22-30 */
+typedef struct LumiRenderOptions {
+  int32_t samples_per_ray; /* 2..1024 */
+  int32_t lod_enabled;
+  double lod_bias;
+  double termination_transmittance; /* 0 disables the early cut */
+  double background[3];             /* model-space (PQ) background */
+  int32_t contraction;              /* 0 = kNone, 1 = kLInfCubic */
+  int32_t chunk_size;               /* only shapes RowStats.evals, as in the reference */
+} LumiRenderOptions;
+
+/* proj/include/lumi/renderer.h:241-246 */
+typedef struct LumiRowStats {
+  int32_t row;
+  int32_t _pad;
+  double ms;
+  int64_t rays;
+  int64_t evals;
+} LumiRowStats;
+
+/* Device-resident frame target for the async entry points.  Planar channel-major
+   images (image.h:16-35) of `width` x `height`; camera row y lands in target row
+   `row_offset + y` (so both eyes of a stereo pair stack into one buffer).  Optional
+   planes may be NULL.  `counts` receives per pixel {evals, contributing} (int32 x2);
+   `row_evals` receives per camera row the sum of evals (indexed by camera row). */
+typedef struct LumiFrameTarget {
+  float* rgb;
+  float* depth;
+  float* opacity;
+  int32_t* counts;
+  int64_t* row_evals;
+  uint8_t* srgb8; /* optional interleaved RGB8 display buffer (PQ -> sRGB epilogue) */
+  /* optional device counters, accumulated (not reset): [0] network evaluations actually
+     executed, [1] active (w_l > 0) level-samples gathered, [2] candidates marched,
+     [3] rays.  Used for the algorithmic-bytes roofline. */
+  uint64_t* work_stats;
+  double exposure_bias_stops;
+  int32_t width;
+  int32_t height;
+  int32_t row_offset;
+  int32_t _pad;
+} LumiFrameTarget;
+
+typedef struct LumiModel LumiModel;
+
+const char* lumi_last_error(void);
+int lumi_abi_version(void);
+/* Fills `info` (>= 256 bytes) with the device name / SM count; LUMI_ERR_CUDA without one. */
+int lumi_device_info(int device, char* info, size_t info_len);
+
+/* ---- model ---------------------------------------------------------------------- */
+int lumi_field_layout(const LumiFieldDesc* desc, LumiGridLayout* out);
+/* Seeded synthetic parameters, bit-identical to RadianceField<float>::init_random(seed)
+   followed (amp > 0) by the grid overwrite Rng(seed+1).uniform(-amp, amp). Host memory. */
+int lumi_synth_params(const LumiFieldDesc* desc, uint64_t seed, double amp, float* table,
+                      float* density_params, float* color_params);
+/* Uploads a field + occupancy (host pointers) to `device`.  occupancy: occ_res^3 bytes,
+   nonzero = occupied, index (iz*res+iy)*res+ix (occupancy.cpp:22-29). */
+int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
+                      const float* density_params, const float* color_params,
+                      const uint8_t* occupancy, int occ_res, LumiModel** out);
+int lumi_model_set_occupancy(LumiModel* m, const uint8_t* occupancy, int occ_res);
+int lumi_model_destroy(LumiModel* m);
+/* Device-side memory footprint of the model in bytes. */
+int lumi_model_bytes(const LumiModel* m, uint64_t* bytes);
+
+/* ---- rendering ------------------------------------------------------------------ */
+/* Drop-in for render_rows (renderer.h:252-278): host planar buffers of the camera's
+   full image size, rows [row_begin,row_end) written.  depth/opacity/stats may be NULL;
+   stats receives (row_end-row_begin) entries.  Synchronous. */
+int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions* opts,
+                     int row_begin, int row_end, float* out, float* depth, float* opacity,
+                     LumiRowStats* stats);
+/* Same, into device memory, enqueued on `stream` (cudaStream_t or NULL). */
+int lumi_render_rows_async(LumiModel* m, const LumiCameraDesc* cam,
+                           const LumiRenderOptions* opts, int row_begin, int row_end,
+                           const LumiFrameTarget* target, void* stream);
+/* Occupancy-kept candidate bitmask per pixel, independent of the network (the set the
+   reference marches with the early cut disabled).  mask: device, camera-sized
+   [height][width][ceil(spp/32)] uint32; counts: device [height][width] int32. */
+int lumi_march_kept_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions* opts,
+                          int row_begin, int row_end, uint32_t* mask, int32_t* counts,
+                          void* stream);
+
+/* ---- occupancy bake (GPU) ------------------------------------------------------- */
+/* OccupancyGrid::probe(k) with the density head + prune(alpha), zero history, no
+   carving; results to host buffers (probe_max may be NULL). */
+int lumi_bake_occupancy(LumiModel* m, const LumiCameraDesc* cams, int ncams,
+                        int samples_per_ray, int points_per_axis, int occ_res, float alpha,
+                        uint8_t* occupancy_out, float* probe_max_out);
+
+/* ---- row scheduler (host) ------------------------------------------------------- */
+int lumi_equal_assignment(int height, int workers, int32_t* rows, double* shares);
+int lumi_assign_rows(int height, int workers, const double* throughputs,
+                     const double* prev_shares, double dampening, int32_t* rows,
+                     double* shares);
+int lumi_next_assignment(int height, int workers, const double* prev_shares,
+                         const int32_t* prev_rows, const double* worker_ms, int width,
+                         double dampening, int32_t* rows, double* shares);
+int lumi_aggregate_stats(const double* wall_ms, int frames, double* mean_fps, double* std_fps,
+                         double* p99_fps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LUMI_CUDA_H */

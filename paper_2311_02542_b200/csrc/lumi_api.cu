@@ -1,0 +1,668 @@
+// lumi_api.cpp -- the C ABI (include/lumi_cuda.h): model upload, render entry points, the
+// GPU occupancy bake driver and the row scheduler.
+//
+// Host arithmetic that feeds bit-exact device geometry (sample distances, step ratio,
+// per-level resolutions, log of the level scale) is computed here with the same libm as
+// the reference, never on the device (renderer.h:135-142, grid.h:25-27, grid.cpp:10-11).
+#include "lumi_cuda.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "kernels.h"
+#include "render_common.cuh"
+
+using lumi_dev::RenderParams;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define LUMI_CUDA_TRY(expr)                                                               \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(LUMI_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+// ---- pcg32, proj/include/lumi/common.h:78-114 ----------------------------------------
+struct Pcg32 {
+  static constexpr uint64_t kMult = 6364136223846793005ULL;
+  uint64_t state = 0, inc = 0;
+  explicit Pcg32(uint64_t seed, uint64_t stream = 0xda3e39cb94b95bdbULL) {
+    inc = (stream << 1u) | 1u;
+    next();
+    state += seed;
+    next();
+  }
+  uint32_t next() {
+    uint64_t old = state;
+    state = old * kMult + inc;
+    uint32_t xs = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
+    uint32_t rot = static_cast<uint32_t>(old >> 59u);
+    return (xs >> rot) | (xs << ((32u - rot) & 31u));
+  }
+  void advance(uint64_t delta) {  // LCG jump-ahead
+    uint64_t cm = kMult, cp = inc, am = 1, ap = 0;
+    while (delta) {
+      if (delta & 1) {
+        am *= cm;
+        ap = ap * cm + cp;
+      }
+      cp = (cm + 1) * cp;
+      cm *= cm;
+      delta >>= 1;
+    }
+    state = am * state + ap;
+  }
+  double uniform() { return next() * (1.0 / 4294967296.0); }
+  double normal() {
+    double u1 = std::max(uniform(), 1e-12);
+    double u2 = uniform();
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+  }
+};
+
+int check_desc(const LumiFieldDesc* d) {
+  if (!d) return fail(LUMI_ERR_INVALID, "null field descriptor");
+  if (d->levels < 1 || d->levels > LUMI_MAX_LEVELS)
+    return fail(LUMI_ERR_UNSUPPORTED, "levels must be in [1, 16]");
+  if (d->features_per_level != 2)
+    return fail(LUMI_ERR_UNSUPPORTED, "features_per_level must be 2");
+  if (d->hidden_width != 64) return fail(LUMI_ERR_UNSUPPORTED, "hidden_width must be 64");
+  if (d->bottleneck != 16) return fail(LUMI_ERR_UNSUPPORTED, "bottleneck must be 16");
+  if (d->table_size == 0 || (d->table_size & (d->table_size - 1)))
+    return fail(LUMI_ERR_INVALID, "table_size must be a power of two");
+  if (d->color_space != 0 && d->color_space != 1) return fail(LUMI_ERR_INVALID, "bad color_space");
+  if (!(d->per_level_scale > 1.0) || d->base_resolution < 1)
+    return fail(LUMI_ERR_INVALID, "bad grid scale/base resolution");
+  return LUMI_OK;
+}
+
+int layout_of(const LumiFieldDesc* d, LumiGridLayout* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->levels = d->levels;
+  out->features_per_level = d->features_per_level;
+  uint64_t off = 0;
+  for (int l = 0; l < d->levels; ++l) {
+    // HashGridConfig::resolution (grid.h:25-27)
+    int res = static_cast<int>(std::floor(d->base_resolution * std::pow(d->per_level_scale, l)));
+    if (l > 0 && res <= out->resolution[l - 1])
+      return fail(LUMI_ERR_INVALID, "hash grid: resolutions must be strictly increasing");
+    if (res < 1 || res > (1 << 30)) return fail(LUMI_ERR_UNSUPPORTED, "resolution out of range");
+    uint64_t v = static_cast<uint64_t>(res) + 1;
+    uint64_t dense = v * v * v;
+    out->resolution[l] = res;
+    out->dense[l] = dense <= d->table_size;
+    out->entries[l] = out->dense[l] ? static_cast<uint32_t>(dense) : d->table_size;
+    out->offset[l] = off;
+    off += static_cast<uint64_t>(out->entries[l]) * d->features_per_level;
+  }
+  out->total_floats = off;
+  const uint64_t F = static_cast<uint64_t>(d->levels) * d->features_per_level, H = d->hidden_width,
+                 B = d->bottleneck;
+  out->density_params = F * H + H + H * (1 + B) + (1 + B);
+  out->color_params = (B + 16) * H + H + H * H + H + H * 3 + 3;
+  return LUMI_OK;
+}
+
+int check_cam(const LumiCameraDesc* c) {
+  if (!c) return fail(LUMI_ERR_INVALID, "null camera");
+  if (!(c->fx > 0 && c->fy > 0))
+    return fail(LUMI_ERR_INVALID, "generate_ray: focal lengths must be positive");
+  if (c->width < 1 || c->height < 1) return fail(LUMI_ERR_INVALID, "bad image size");
+  for (int i = 0; i < 9; ++i)
+    if (!std::isfinite(c->rot[i])) return fail(LUMI_ERR_INVALID, "non-finite pose");
+  for (int i = 0; i < 3; ++i)
+    if (!std::isfinite(c->origin[i])) return fail(LUMI_ERR_INVALID, "non-finite pose");
+  if (!(c->t_near > 0 && c->t_far > c->t_near))
+    return fail(LUMI_ERR_INVALID, "march_ray: bad sampling interval");
+  return LUMI_OK;
+}
+
+int check_opts(const LumiRenderOptions* o) {
+  if (!o) return fail(LUMI_ERR_INVALID, "null render options");
+  if (o->samples_per_ray < 2) return fail(LUMI_ERR_INVALID, "march_ray: bad sampling interval");
+  if (o->samples_per_ray > lumi_dev::kMaxSamples)
+    return fail(LUMI_ERR_UNSUPPORTED, "samples_per_ray must be <= 1024");
+  if (o->chunk_size < 1) return fail(LUMI_ERR_INVALID, "chunk_size must be positive");
+  if (o->contraction != 0 && o->contraction != 1) return fail(LUMI_ERR_INVALID, "bad contraction");
+  return LUMI_OK;
+}
+
+}  // namespace
+
+struct LumiModel {
+  int device = 0;
+  LumiFieldDesc desc{};
+  LumiGridLayout layout{};
+  float* d_table = nullptr;
+  float* d_dparams = nullptr;
+  float* d_cparams = nullptr;
+  uint8_t* d_occ = nullptr;
+  int occ_res = 0;
+  unsigned int* d_counter = nullptr;
+  std::mutex mu;
+  std::map<std::tuple<double, double, int>, std::pair<double*, double>> ts_cache;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Exponential sample distances and step ratio (renderer.h:135-142) on the host.
+int get_ts(LumiModel* m, double tn, double tf, int n, const double** d_ts, double* ratio) {
+  std::lock_guard<std::mutex> lk(m->mu);
+  auto key = std::make_tuple(tn, tf, n);
+  auto it = m->ts_cache.find(key);
+  if (it == m->ts_cache.end()) {
+    std::vector<double> ts(n);
+    const double log_ratio = std::log(tf / tn);
+    for (int i = 0; i < n; ++i) ts[i] = tn * std::exp(log_ratio * (static_cast<double>(i) / (n - 1)));
+    ts[0] = tn;
+    ts[n - 1] = tf;
+    const double r = std::pow(tf / tn, 1.0 / (n - 1));
+    double* d = nullptr;
+    LUMI_CUDA_TRY(cudaMalloc(&d, sizeof(double) * n));
+    LUMI_CUDA_TRY(cudaMemcpy(d, ts.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    it = m->ts_cache.emplace(key, std::make_pair(d, r)).first;
+  }
+  *d_ts = it->second.first;
+  *ratio = it->second.second;
+  return LUMI_OK;
+}
+
+int make_params(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions* o, int b, int e,
+                RenderParams* p) {
+  int rc;
+  if ((rc = check_cam(cam)) || (rc = check_opts(o))) return rc;
+  if (!(b >= 0 && e <= cam->height && b <= e))
+    return fail(LUMI_ERR_INVALID, "render_rows: row range outside image");
+  std::memset(p, 0, sizeof(*p));
+  std::memcpy(p->cam.rot, cam->rot, sizeof(cam->rot));
+  std::memcpy(p->cam.origin, cam->origin, sizeof(cam->origin));
+  p->cam.fx = cam->fx;
+  p->cam.fy = cam->fy;
+  p->cam.cx = cam->cx;
+  p->cam.cy = cam->cy;
+  p->cam.width = cam->width;
+  p->cam.height = cam->height;
+  p->cam.t_near = cam->t_near;
+  p->cam.t_far = cam->t_far;
+  auto& g = p->grid;
+  g.table = reinterpret_cast<const float2*>(m->d_table);
+  g.levels = m->layout.levels;
+  for (int l = 0; l < g.levels; ++l) {
+    g.res[l] = m->layout.resolution[l];
+    g.hash_mask[l] = m->layout.entries[l] - 1u;
+    if (m->layout.dense[l]) g.dense_mask |= 1u << l;
+    g.offset2[l] = m->layout.offset[l] / 2;
+  }
+  g.two_base = 2.0 * m->desc.base_resolution;  // grid.cpp:10 evaluates 2.0 * base first
+  g.log_scale = std::log(m->desc.per_level_scale);
+  p->mlp.dparams = m->d_dparams;
+  p->mlp.cparams = m->d_cparams;
+  p->mlp.color_space = m->desc.color_space;
+  p->occ = m->d_occ;
+  p->occ_res = m->occ_res;
+  if ((rc = get_ts(m, cam->t_near, cam->t_far, o->samples_per_ray, &p->ts, &p->ratio))) return rc;
+  p->n = o->samples_per_ray;
+  p->lod_enabled = o->lod_enabled ? 1 : 0;
+  p->lod_bias = o->lod_bias;
+  p->t_cut = o->termination_transmittance;
+  for (int c = 0; c < 3; ++c) p->bg[c] = o->background[c];
+  p->contraction = o->contraction;
+  p->chunk = o->chunk_size;
+  p->row_begin = b;
+  p->row_end = e;
+  p->work_counter = m->d_counter;
+  return LUMI_OK;
+}
+
+int set_target(RenderParams* p, const LumiFrameTarget* t, int b, int e) {
+  if (!t || !t->rgb) return fail(LUMI_ERR_INVALID, "frame target needs an rgb plane");
+  if (t->width != p->cam.width)
+    return fail(LUMI_ERR_INVALID, "frame target width must equal the camera width");
+  if (t->row_offset + b < 0 || t->row_offset + e > t->height)
+    return fail(LUMI_ERR_INVALID, "frame target too small for the row range");
+  p->rgb = t->rgb;
+  p->depth = t->depth;
+  p->opacity = t->opacity;
+  p->counts = t->counts;
+  p->row_evals = t->row_evals;
+  p->srgb8 = t->srgb8;
+  p->work_stats = reinterpret_cast<unsigned long long*>(t->work_stats);
+  p->exposure_gain = std::exp2(t->exposure_bias_stops);
+  p->tw = t->width;
+  p->th = t->height;
+  p->row_offset = t->row_offset;
+  return LUMI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lumi_last_error(void) { return g_err.c_str(); }
+int lumi_abi_version(void) { return LUMI_ABI_VERSION; }
+
+int lumi_device_info(int device, char* info, size_t len) {
+  cudaDeviceProp prop;
+  LUMI_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (info && len)
+    std::snprintf(info, len, "%s sm_%d%d SMs=%d mem=%.1fGiB", prop.name, prop.major, prop.minor,
+                  prop.multiProcessorCount, prop.totalGlobalMem / 1073741824.0);
+  if (prop.major != 10)
+    return fail(LUMI_ERR_UNSUPPORTED, std::string("need an sm_100 (B200) device, got ") + prop.name);
+  return LUMI_OK;
+}
+
+int lumi_field_layout(const LumiFieldDesc* desc, LumiGridLayout* out) {
+  int rc = check_desc(desc);
+  if (rc) return rc;
+  if (!out) return fail(LUMI_ERR_INVALID, "null layout");
+  return layout_of(desc, out);
+}
+
+int lumi_synth_params(const LumiFieldDesc* desc, uint64_t seed, double amp, float* table,
+                      float* dparams, float* cparams) {
+  LumiGridLayout lay;
+  int rc = lumi_field_layout(desc, &lay);
+  if (rc) return rc;
+  if (!table || !dparams || !cparams) return fail(LUMI_ERR_INVALID, "null output buffer");
+  // RadianceField::init_random (field.h:88-93): grid uniform(+-1e-4) (grid.h:82-84), then the
+  // density and colour nets (He-normal weights, zero bias, network.h:73-78).
+  Pcg32 rng(seed);
+  if (amp > 0) {
+    rng.advance(lay.total_floats);  // the grid draws are overwritten below
+  } else {
+    for (uint64_t i = 0; i < lay.total_floats; ++i)
+      table[i] = static_cast<float>(-1e-4 + (1e-4 - -1e-4) * rng.uniform());
+  }
+  auto layer = [&](int in, int out, float* p) {
+    const double scale = std::sqrt(2.0 / in);
+    for (int i = 0; i < in * out; ++i) p[i] = static_cast<float>(rng.normal() * scale);
+    for (int i = 0; i < out; ++i) p[in * out + i] = 0.0f;
+    return p + static_cast<size_t>(in) * out + out;
+  };
+  const int F = desc->levels * desc->features_per_level, H = desc->hidden_width,
+            B = desc->bottleneck;
+  float* p = layer(F, H, dparams);
+  layer(H, 1 + B, p);
+  p = layer(B + 16, H, cparams);
+  p = layer(H, H, p);
+  layer(H, 3, p);
+  if (amp > 0) {  // grid overwrite, the pattern of trainer.cpp:257-259
+    Pcg32 g(seed + 1);
+    for (uint64_t i = 0; i < lay.total_floats; ++i)
+      table[i] = static_cast<float>(-amp + (amp - -amp) * g.uniform());
+  }
+  return LUMI_OK;
+}
+
+int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
+                      const float* dparams, const float* cparams, const uint8_t* occ, int occ_res,
+                      LumiModel** out) {
+  if (!out) return fail(LUMI_ERR_INVALID, "null output handle");
+  *out = nullptr;
+  LumiGridLayout lay;
+  int rc = lumi_field_layout(desc, &lay);
+  if (rc) return rc;
+  if (!table || !dparams || !cparams) return fail(LUMI_ERR_INVALID, "null parameter buffer");
+  int ndev = 0;
+  LUMI_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(LUMI_ERR_CUDA, "no such CUDA device");
+  if ((rc = lumi_device_info(device, nullptr, 0))) return rc;
+  DeviceGuard dg(device);
+  auto m = new LumiModel();
+  m->device = device;
+  m->desc = *desc;
+  m->layout = lay;
+  auto cleanup = [&](int code) {
+    lumi_model_destroy(m);
+    return code;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&m->d_table, lay.total_floats * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&m->d_dparams, lay.density_params * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&m->d_cparams, lay.color_params * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&m->d_counter, 64 * sizeof(unsigned int))) != cudaSuccess ||
+      (e = cudaMemcpy(m->d_table, table, lay.total_floats * sizeof(float),
+                      cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(m->d_dparams, dparams, lay.density_params * sizeof(float),
+                      cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(m->d_cparams, cparams, lay.color_params * sizeof(float),
+                      cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemset(m->d_counter, 0, 64 * sizeof(unsigned int))) != cudaSuccess)
+    return cleanup(fail(LUMI_ERR_CUDA, std::string("model upload: ") + cudaGetErrorString(e)));
+  if ((rc = lumi_model_set_occupancy(m, occ, occ_res))) return cleanup(rc);
+  *out = m;
+  return LUMI_OK;
+}
+
+int lumi_model_set_occupancy(LumiModel* m, const uint8_t* occ, int res) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  if (res < 1 || res > 1024) return fail(LUMI_ERR_INVALID, "occupancy: bad resolution");  // occupancy.cpp:14
+  DeviceGuard dg(m->device);
+  const size_t n = static_cast<size_t>(res) * res * res;
+  std::vector<uint8_t> bits(n, 1);  // default all occupied (occupancy.cpp:15)
+  if (occ)
+    for (size_t i = 0; i < n; ++i) bits[i] = occ[i] ? 1 : 0;
+  if (m->d_occ) cudaFree(m->d_occ);
+  m->d_occ = nullptr;
+  LUMI_CUDA_TRY(cudaMalloc(&m->d_occ, n));
+  LUMI_CUDA_TRY(cudaMemcpy(m->d_occ, bits.data(), n, cudaMemcpyHostToDevice));
+  m->occ_res = res;
+  return LUMI_OK;
+}
+
+int lumi_model_destroy(LumiModel* m) {
+  if (!m) return LUMI_OK;
+  DeviceGuard dg(m->device);
+  cudaFree(m->d_table);
+  cudaFree(m->d_dparams);
+  cudaFree(m->d_cparams);
+  cudaFree(m->d_occ);
+  cudaFree(m->d_counter);
+  for (auto& kv : m->ts_cache) cudaFree(kv.second.first);
+  delete m;
+  return LUMI_OK;
+}
+
+int lumi_model_bytes(const LumiModel* m, uint64_t* bytes) {
+  if (!m || !bytes) return fail(LUMI_ERR_INVALID, "null argument");
+  *bytes = (m->layout.total_floats + m->layout.density_params + m->layout.color_params) * 4 +
+           static_cast<uint64_t>(m->occ_res) * m->occ_res * m->occ_res;
+  return LUMI_OK;
+}
+
+int lumi_render_rows_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions* o,
+                           int b, int e, const LumiFrameTarget* t, void* stream) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  DeviceGuard dg(m->device);
+  RenderParams p;
+  int rc = make_params(m, cam, o, b, e, &p);
+  if (rc) return rc;
+  if ((rc = set_target(&p, t, b, e))) return rc;
+  LUMI_CUDA_TRY(launch_render_simt(p, static_cast<cudaStream_t>(stream)));
+  return LUMI_OK;
+}
+
+int lumi_march_kept_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions* o,
+                          int b, int e, uint32_t* mask, int32_t* counts, void* stream) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  DeviceGuard dg(m->device);
+  RenderParams p;
+  int rc = make_params(m, cam, o, b, e, &p);
+  if (rc) return rc;
+  LUMI_CUDA_TRY(launch_march_kept(p, mask, counts, static_cast<cudaStream_t>(stream)));
+  return LUMI_OK;
+}
+
+int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions* o, int b,
+                     int e, float* out, float* depth, float* opacity, LumiRowStats* stats) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  if (!out) return fail(LUMI_ERR_INVALID, "null output image");
+  int rc;
+  if ((rc = check_cam(cam)) || (rc = check_opts(o))) return rc;
+  if (!(b >= 0 && e <= cam->height && b <= e))
+    return fail(LUMI_ERR_INVALID, "render_rows: row range outside image");
+  if (b == e) return LUMI_OK;
+  DeviceGuard dg(m->device);
+  const int W = cam->width, rows = e - b;
+  const size_t plane = static_cast<size_t>(W) * rows;
+  cudaStream_t s;
+  LUMI_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  float* d_buf = nullptr;
+  int64_t* d_rows = nullptr;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto done = [&](int code) {
+    cudaStreamSynchronize(s);
+    cudaFree(d_buf);
+    cudaFree(d_rows);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    return code;
+  };
+  cudaError_t ce;
+  if ((ce = cudaMallocAsync(&d_buf, plane * 5 * sizeof(float), s)) != cudaSuccess ||
+      (ce = cudaMallocAsync(&d_rows, rows * sizeof(int64_t), s)) != cudaSuccess ||
+      (ce = cudaMemsetAsync(d_rows, 0, rows * sizeof(int64_t), s)) != cudaSuccess)
+    return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+  LumiFrameTarget t{};
+  t.rgb = d_buf;
+  t.depth = d_buf + 3 * plane;
+  t.opacity = d_buf + 4 * plane;
+  t.row_evals = d_rows - b;  // indexed by camera row
+  t.width = W;
+  t.height = rows;
+  t.row_offset = -b;
+  cudaEventRecord(e0, s);
+  if ((rc = lumi_render_rows_async(m, cam, o, b, e, &t, s))) return done(rc);
+  cudaEventRecord(e1, s);
+  const size_t full = static_cast<size_t>(W) * cam->height;
+  for (int c = 0; c < 3; ++c)
+    if ((ce = cudaMemcpyAsync(out + c * full + static_cast<size_t>(b) * W, d_buf + c * plane,
+                              plane * sizeof(float), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+  if (depth &&
+      (ce = cudaMemcpyAsync(depth + static_cast<size_t>(b) * W, d_buf + 3 * plane,
+                            plane * sizeof(float), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+  if (opacity &&
+      (ce = cudaMemcpyAsync(opacity + static_cast<size_t>(b) * W, d_buf + 4 * plane,
+                            plane * sizeof(float), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+  std::vector<int64_t> row_ev(rows);
+  if ((ce = cudaMemcpyAsync(row_ev.data(), d_rows, rows * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+  if ((ce = cudaStreamSynchronize(s)) != cudaSuccess)
+    return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+  if (stats) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    for (int y = b; y < e; ++y) {
+      // The device renders all rows in one launch; the row share of the launch time is
+      // reported (renderer.h:272-276 measures each row on the CPU).
+      stats[y - b].row = y;
+      stats[y - b].ms = ms / rows;
+      stats[y - b].rays = W;
+      stats[y - b].evals = row_ev[y - b];
+    }
+  }
+  return done(LUMI_OK);
+}
+
+int lumi_bake_occupancy(LumiModel* m, const LumiCameraDesc* cams, int ncams, int spp, int k,
+                        int res, float alpha, uint8_t* occ_out, float* probe_out) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  if (k < 1) return fail(LUMI_ERR_INVALID, "probe: need at least one point per axis");
+  if (res < 1 || res > 1024) return fail(LUMI_ERR_INVALID, "occupancy: bad resolution");
+  if (spp < 2 || ncams < 0 || (ncams > 0 && !cams)) return fail(LUMI_ERR_INVALID, "bad cameras");
+  if (!occ_out) return fail(LUMI_ERR_INVALID, "null occupancy output");
+  DeviceGuard dg(m->device);
+  // Per-camera step ratios on the host libm (occupancy.cpp:106-108).
+  std::vector<double> cam_buf(5 * static_cast<size_t>(std::max(ncams, 1)));
+  for (int i = 0; i < ncams; ++i) {
+    for (int j = 0; j < 3; ++j) cam_buf[3 * i + j] = cams[i].origin[j];
+    cam_buf[3 * ncams + i] = cams[i].t_near;
+    cam_buf[4 * ncams + i] = std::pow(cams[i].t_far / cams[i].t_near, 1.0 / (spp - 1));
+  }
+  const size_t n = static_cast<size_t>(res) * res * res;
+  double* d_cam = nullptr;
+  float* d_probe = nullptr;
+  uint8_t* d_occ = nullptr;
+  auto done = [&](int code) {
+    cudaFree(d_cam);
+    cudaFree(d_probe);
+    cudaFree(d_occ);
+    return code;
+  };
+  cudaError_t ce;
+  if ((ce = cudaMalloc(&d_cam, cam_buf.size() * sizeof(double))) != cudaSuccess ||
+      (ce = cudaMalloc(&d_probe, n * sizeof(float))) != cudaSuccess ||
+      (ce = cudaMalloc(&d_occ, n)) != cudaSuccess ||
+      (ce = cudaMemcpy(d_cam, cam_buf.data(), cam_buf.size() * sizeof(double),
+                       cudaMemcpyHostToDevice)) != cudaSuccess)
+    return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+  RenderParams rp;
+  LumiCameraDesc dummy{};
+  dummy.rot[0] = dummy.rot[4] = dummy.rot[8] = 1.0;
+  dummy.fx = dummy.fy = 1.0;
+  dummy.width = dummy.height = 1;
+  dummy.t_near = 0.05;
+  dummy.t_far = 10.0;
+  LumiRenderOptions o{};
+  o.samples_per_ray = spp;
+  o.chunk_size = 32;
+  o.contraction = 1;
+  int rc = make_params(m, &dummy, &o, 0, 0, &rp);
+  if (rc) return done(rc);
+  lumi_dev::BakeParams bp;
+  bp.grid = rp.grid;
+  bp.mlp = rp.mlp;
+  bp.res = res;
+  bp.k = k;
+  bp.ncams = ncams;
+  bp.alpha = alpha;
+  bp.cam_origin = d_cam;
+  bp.cam_tnear = d_cam + 3 * ncams;
+  bp.cam_ratio = d_cam + 4 * ncams;
+  bp.probe_max = d_probe;
+  bp.occ = d_occ;
+  if ((ce = launch_bake(bp, nullptr)) != cudaSuccess ||
+      (ce = cudaMemcpy(occ_out, d_occ, n, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (probe_out &&
+       (ce = cudaMemcpy(probe_out, d_probe, n * sizeof(float), cudaMemcpyDeviceToHost)) != cudaSuccess))
+    return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+  return done(LUMI_OK);
+}
+
+// ---- scheduler (scheduler.cpp:18-162) -----------------------------------------------------
+
+static void round_rows(const double* shares, int n, int height, int32_t* rows) {
+  std::vector<std::pair<double, int>> rem(n);
+  int assigned = 0;
+  for (int i = 0; i < n; ++i) {
+    double exact = shares[i] * height;
+    rows[i] = static_cast<int>(std::floor(exact));
+    rem[i] = {exact - rows[i], i};
+    assigned += rows[i];
+  }
+  std::sort(rem.begin(), rem.end(), [](const auto& a, const auto& b) {
+    if (a.first != b.first) return a.first > b.first;
+    return a.second < b.second;
+  });
+  for (int k = 0; k < height - assigned; ++k) rows[rem[k % n].second] += 1;
+  if (height >= n) {
+    for (int i = 0; i < n; ++i) {
+      while (rows[i] == 0) {
+        int big = static_cast<int>(std::max_element(rows, rows + n) - rows);
+        rows[big] -= 1;
+        rows[i] += 1;
+      }
+    }
+  }
+}
+
+int lumi_equal_assignment(int height, int workers, int32_t* rows, double* shares) {
+  if (workers < 1) return fail(LUMI_ERR_INVALID, "assignment: need at least one worker");
+  if (height < workers) return fail(LUMI_ERR_INVALID, "assignment: more workers than rows");
+  if (!rows || !shares) return fail(LUMI_ERR_INVALID, "null output");
+  std::vector<double> s(workers, 1.0 / workers);
+  round_rows(s.data(), workers, height, rows);
+  for (int i = 0; i < workers; ++i) shares[i] = static_cast<double>(rows[i]) / height;
+  return LUMI_OK;
+}
+
+int lumi_assign_rows(int height, int n, const double* tp, const double* prev_shares, double damp,
+                     int32_t* rows, double* shares) {
+  if (!(n >= 1 && height >= n)) return fail(LUMI_ERR_INVALID, "assign_rows: more workers than rows");
+  if (!tp || !prev_shares || !rows || !shares) return fail(LUMI_ERR_INVALID, "null argument");
+  double total = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!(tp[i] > 0)) return fail(LUMI_ERR_INVALID, "assign_rows: throughputs must be positive");
+    total += tp[i];
+  }
+  std::vector<double> s(n);
+  for (int i = 0; i < n; ++i) {
+    double target = tp[i] / total;
+    s[i] = prev_shares[i] + damp * (target - prev_shares[i]);
+  }
+  double sum = std::accumulate(s.begin(), s.end(), 0.0);
+  for (auto& v : s) v /= sum;
+  round_rows(s.data(), n, height, rows);
+  int at = 0;
+  for (int i = 0; i < n; ++i) {
+    shares[i] = static_cast<double>(rows[i]) / height;
+    at += rows[i];
+  }
+  if (at != height) return fail(LUMI_ERR_INVALID, "assign_rows: partition does not cover all rows");
+  return LUMI_OK;
+}
+
+int lumi_next_assignment(int height, int n, const double* prev_shares, const int32_t* prev_rows,
+                         const double* worker_ms, int width, double damp, int32_t* rows,
+                         double* shares) {
+  if (!prev_rows || !worker_ms) return fail(LUMI_ERR_INVALID, "null argument");
+  std::vector<double> tp(n);
+  for (int i = 0; i < n; ++i) {
+    double ms = std::max(worker_ms[i], 1e-6);
+    tp[i] = std::max(static_cast<double>(static_cast<int64_t>(prev_rows[i]) * width), 1.0) /
+            (ms / 1000.0);
+  }
+  return lumi_assign_rows(height, n, tp.data(), prev_shares, damp, rows, shares);
+}
+
+int lumi_aggregate_stats(const double* ms, int n, double* mean_fps, double* std_fps,
+                         double* p99_fps) {
+  if (n <= 0 || !ms) return fail(LUMI_ERR_INVALID, "aggregate_stats: no frames");
+  std::vector<double> times(ms, ms + n);
+  auto fps = [](double w) { return w > 0 ? 1000.0 / w : 0.0; };
+  double mean = 0;
+  for (double w : times) mean += fps(w);
+  mean /= n;
+  double var = 0;
+  for (double w : times) var += (fps(w) - mean) * (fps(w) - mean);
+  var /= n;
+  std::sort(times.begin(), times.end());
+  double idx = 0.99 * (times.size() - 1);
+  size_t lo = static_cast<size_t>(std::floor(idx));
+  size_t hi = std::min(lo + 1, times.size() - 1);
+  double frac = idx - lo;
+  double p99 = times[lo] * (1 - frac) + times[hi] * frac;
+  if (mean_fps) *mean_fps = mean;
+  if (std_fps) *std_fps = std::sqrt(var);
+  if (p99_fps) *p99_fps = p99 > 0 ? 1000.0 / p99 : 0.0;
+  return LUMI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// render_common.cuh -- kernel parameter block and shared per-ray epilogue.
+#pragma once
+#include <cstdint>
+
+#include "field.cuh"
+#include "geometry.cuh"
+
+namespace lumi_dev {
+
+constexpr int kMaxSamples = 1024;
+
+struct RenderParams {
+  CamDev cam;
+  GridDev grid;
+  MlpDev mlp;
+  const uint8_t* occ;  // occ_res^3 bytes
+  int occ_res;
+  const double* ts;    // host-computed exponential distances (renderer.h:135-141)
+  double ratio;        // host-computed pow(t_far/t_near, 1/(n-1)) (renderer.h:142)
+  int n;               // samples_per_ray
+  int lod_enabled;
+  double lod_bias;
+  double t_cut;
+  double bg[3];
+  int contraction;
+  int chunk;
+  int row_begin, row_end;
+  // target (LumiFrameTarget)
+  float* rgb;
+  float* depth;
+  float* opacity;
+  int32_t* counts;
+  int64_t* row_evals;
+  uint8_t* srgb8;
+  unsigned long long* work_stats;  // [evals, active level-samples, candidates, rays]
+  double exposure_gain;  // 2^bias
+  int tw, th, row_offset;
+  // persistent scheduling
+  unsigned int* work_counter;
+  int tile_w, tile_h, tiles_x, tiles_total;
+};
+
+// color.cpp:17-44 constants (scene-linear 1.0 = 100 cd/m^2)
+__device__ __forceinline__ double pq_decode_dev(double v) {
+  const double m1 = 1305.0 / 8192.0, m2 = 2523.0 / 32.0, c1 = 107.0 / 128.0,
+               c2 = 2413.0 / 128.0, c3 = 2392.0 / 128.0;
+  const double p = pow(v, 1.0 / m2);
+  double num = p - c1;
+  if (num < 0.0) num = 0.0;
+  const double den = c2 - c3 * p;
+  return pow(num / den, 1.0 / m1) / (100.0 / 10000.0);
+}
+
+__device__ __forceinline__ double srgb_oetf_dev(double v) {
+  v = clamp01(v);
+  return v <= 0.0031308 ? 12.92 * v : 1.055 * pow(v, 1.0 / 2.4) - 0.055;
+}
+
+// Display epilogue: PQ -> scene linear (pq_to_srgb_float, trainer.cpp:175-182) scaled by
+// 2^bias and mapped to sRGB8 as tonemap_srgb does (color.cpp:104-115).
+__device__ __forceinline__ uint8_t display_srgb8(double v, int color_space, double gain) {
+  const double lin = color_space == 0 ? pq_decode_dev(clamp01(v)) : (v > 0.0 ? v : 0.0);
+  const double s = srgb_oetf_dev(clamp01(lin * gain));
+  return (uint8_t)llround(s * 255.0);
+}
+
+struct RayResult {
+  double px, py, pz, depth, opacity;
+  int evals, contributing;
+};
+
+// Final per-ray bookkeeping (renderer.h:233-236) and output stores.
+__device__ __forceinline__ void store_ray(const RenderParams& p, int x, int y, RayResult r,
+                                          double trans) {
+  r.px = dadd(r.px, dmul(trans, p.bg[0]));
+  r.py = dadd(r.py, dmul(trans, p.bg[1]));
+  r.pz = dadd(r.pz, dmul(trans, p.bg[2]));
+  const double depth = r.depth / dadd(r.opacity, 1e-10);
+  const size_t plane = (size_t)p.tw * p.th;
+  const size_t pix = (size_t)(p.row_offset + y) * p.tw + x;
+  p.rgb[pix] = __double2float_rn(r.px);
+  p.rgb[plane + pix] = __double2float_rn(r.py);
+  p.rgb[2 * plane + pix] = __double2float_rn(r.pz);
+  if (p.depth) p.depth[pix] = __double2float_rn(depth);
+  if (p.opacity) p.opacity[pix] = __double2float_rn(r.opacity);
+  if (p.counts) {
+    p.counts[2 * pix] = r.evals;
+    p.counts[2 * pix + 1] = r.contributing;
+  }
+  if (p.srgb8) {
+    p.srgb8[3 * pix + 0] = display_srgb8(r.px, p.mlp.color_space, p.exposure_gain);
+    p.srgb8[3 * pix + 1] = display_srgb8(r.py, p.mlp.color_space, p.exposure_gain);
+    p.srgb8[3 * pix + 2] = display_srgb8(r.pz, p.mlp.color_space, p.exposure_gain);
+  }
+  if (p.row_evals) atomicAdd((unsigned long long*)&p.row_evals[y], (unsigned long long)r.evals);
+}
+
+// RayMarchRecord::evals (renderer.h:168, 225-230): evaluated samples come in whole chunks;
+// after a cut at `contributing`, the partially used chunk still counts in full unless it
+// is the final one.
+__device__ __forceinline__ int chunk_evals(bool terminated, int contributing, int kept_total_seen,
+                                           int chunk) {
+  if (!terminated) return kept_total_seen;
+  const int lim = ((contributing + chunk - 1) / chunk) * chunk;
+  return min(kept_total_seen, lim);
+}
+
+// Warp-aggregated work counters (one atomic per warp per counter).
+__device__ __forceinline__ void add_work_stats(const RenderParams& p, unsigned long long evals,
+                                               unsigned long long level_samples,
+                                               unsigned long long candidates,
+                                               unsigned long long rays) {
+  if (!p.work_stats) return;
+  const unsigned mask = __activemask();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    evals += __shfl_xor_sync(mask, evals, o);
+    level_samples += __shfl_xor_sync(mask, level_samples, o);
+    candidates += __shfl_xor_sync(mask, candidates, o);
+    rays += __shfl_xor_sync(mask, rays, o);
+  }
+  if ((threadIdx.x & 31) == (__ffs(mask) - 1)) {
+    atomicAdd(p.work_stats + 0, evals);
+    atomicAdd(p.work_stats + 1, level_samples);
+    atomicAdd(p.work_stats + 2, candidates);
+    atomicAdd(p.work_stats + 3, rays);
+  }
+}
+
+}  // namespace lumi_dev

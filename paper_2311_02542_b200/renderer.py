@@ -1,0 +1,390 @@
+"""Host-side mirror of the reference renderer/model API over the sm_100a C ABI.
+
+Names, argument meaning and error behaviour follow proj/include/lumi/{grid,field,camera,
+occupancy,renderer}.h so code (and tests) written against the reference read the same:
+
+    field = RadianceField(FieldConfig(grid=HashGridConfig(table_size=1 << 19)))
+    field.init_random(1234)
+    out = Image(cam.width, cam.height, 3)
+    render_rows(field, grid, cam, RenderOptions(), 0, cam.height, out, None, None, stats)
+
+The device work happens in liblumi_cuda.so (paper_2311_02542_b200/csrc); this module only
+marshals descriptors and owns device-model caching.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import threading
+import weakref
+from dataclasses import dataclass, field as dc_field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import Error, check
+
+__all__ = [
+    "Error", "HashGridConfig", "ColorSpaceMode", "FieldConfig", "RadianceField", "OccupancyGrid",
+    "ContractionMode", "CameraModel", "RenderOptions", "RowStats", "Image", "DeviceModel",
+    "render_rows", "lod_levels_of", "device_info",
+]
+
+
+def _p(a) -> Optional[int]:
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+@dataclass
+class HashGridConfig:
+    """proj/include/lumi/grid.h:18-29 (note the reference default table_size = 2^15)."""
+
+    levels: int = 16
+    features_per_level: int = 2
+    base_resolution: int = 128
+    per_level_scale: float = 1.4
+    table_size: int = 1 << 15
+
+    def resolution(self, level: int) -> int:
+        return int(math.floor(self.base_resolution * math.pow(self.per_level_scale, level)))
+
+    def feature_dim(self) -> int:
+        return self.levels * self.features_per_level
+
+
+class ColorSpaceMode(enum.IntEnum):
+    kPq = 0
+    kLinear = 1
+
+
+@dataclass
+class FieldConfig:
+    """proj/include/lumi/field.h:22-27."""
+
+    grid: HashGridConfig = dc_field(default_factory=HashGridConfig)
+    hidden_width: int = 64
+    bottleneck: int = 16
+    color_space: ColorSpaceMode = ColorSpaceMode.kPq
+
+    def desc(self) -> _abi.FieldDesc:
+        g = self.grid
+        return _abi.FieldDesc(g.levels, g.features_per_level, g.base_resolution, self.hidden_width,
+                              float(g.per_level_scale), int(g.table_size), self.bottleneck,
+                              int(self.color_space), 0)
+
+
+def layout_of(cfg: FieldConfig) -> _abi.GridLayout:
+    lay = _abi.GridLayout()
+    d = cfg.desc()
+    check(_abi.lib().lumi_field_layout(C.byref(d), C.byref(lay)))
+    return lay
+
+
+class RadianceField:
+    """Host parameters of RadianceField<float> (field.h:65-209) in the reference layout:
+    one float grid table (grid.h:58-74) and per-net flattened weights-then-bias
+    (network.h:144-151)."""
+
+    Scalar = np.float32
+    kShDim = 16
+
+    def __init__(self, cfg: FieldConfig = None):
+        self.cfg = cfg or FieldConfig()
+        self.layout = layout_of(self.cfg)
+        self.grid_params = np.zeros(self.layout.total_floats, np.float32)
+        self.density_params = np.zeros(self.layout.density_params, np.float32)
+        self.color_params = np.zeros(self.layout.color_params, np.float32)
+        self.version = 0
+
+    def config(self) -> FieldConfig:
+        return self.cfg
+
+    def _synth(self, seed: int, amp: float) -> None:
+        d = self.cfg.desc()
+        check(_abi.lib().lumi_synth_params(C.byref(d), int(seed), float(amp), _p(self.grid_params),
+                                           _p(self.density_params), _p(self.color_params)))
+        self.version += 1
+
+    def init_random(self, seed: int) -> None:
+        """RadianceField::init_random (field.h:88-93), bit-identical pcg32 stream."""
+        self._synth(seed, 0.0)
+
+    @classmethod
+    def synthetic(cls, cfg: FieldConfig, seed: int, amplitude: float) -> "RadianceField":
+        """init_random(seed) then grid <- Rng(seed+1).uniform(-a, a) (trainer.cpp:257-259)."""
+        f = cls(cfg)
+        f._synth(seed, amplitude)
+        return f
+
+    def level_is_dense(self, level: int) -> bool:
+        return bool(self.layout.dense[level])
+
+    def parameter_count(self) -> int:
+        return int(self.grid_params.size)
+
+    def touch(self) -> None:
+        """Call after editing parameters in place so cached device copies refresh."""
+        self.version += 1
+
+
+class OccupancyGrid:
+    """Binary occupancy over the contracted domain [-2,2]^3 (occupancy.h:32-100): one byte per
+    voxel, index (iz*res+iy)*res+ix, default all occupied (occupancy.cpp:13-20)."""
+
+    kMaxResolution = 1024
+
+    def __init__(self, resolution: int = 128, bits: Optional[np.ndarray] = None):
+        if not (0 < resolution <= self.kMaxResolution):
+            raise Error("occupancy: bad resolution")
+        self.res = int(resolution)
+        n = self.res ** 3
+        if bits is None:
+            self.bits = np.ones(n, np.uint8)
+        else:
+            bits = np.ascontiguousarray(bits, dtype=np.uint8).reshape(-1)
+            if bits.size != n:
+                raise Error("occupancy: bit count does not match resolution")
+            self.bits = (bits != 0).astype(np.uint8)
+        self.version = 0
+
+    def resolution(self) -> int:
+        return self.res
+
+    def voxel_count(self) -> int:
+        return self.res ** 3
+
+    def voxel_index(self, c) -> int:
+        """occupancy.cpp:22-29."""
+        u, v, w = ((c[0] + 2.0) * 0.25, (c[1] + 2.0) * 0.25, (c[2] + 2.0) * 0.25)
+        if u < 0 or u > 1 or v < 0 or v > 1 or w < 0 or w > 1:
+            return -1
+        r = self.res
+        ix, iy, iz = (min(int(u * r), r - 1), min(int(v * r), r - 1), min(int(w * r), r - 1))
+        return (iz * r + iy) * r + ix
+
+    def is_occupied(self, c) -> bool:
+        i = self.voxel_index(c)
+        return i >= 0 and bool(self.bits[i])
+
+    def occupied_bit(self, index: int) -> bool:
+        return bool(self.bits[index])
+
+    def occupied_count(self) -> int:
+        return int(self.bits.sum())
+
+    def touch(self) -> None:
+        self.version += 1
+
+
+class ContractionMode(enum.IntEnum):
+    kNone = 0
+    kLInfCubic = 1
+
+
+@dataclass
+class CameraModel:
+    """proj/include/lumi/camera.h:15-23 (pose row-major world <- camera)."""
+
+    rot: Sequence[float] = (1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0)
+    origin: Sequence[float] = (0.0, 0.0, 0.0)
+    fx: float = 0.0
+    fy: float = 0.0
+    cx: float = 0.0
+    cy: float = 0.0
+    width: int = 0
+    height: int = 0
+    t_near: float = 0.05
+    t_far: float = 10.0
+
+    def desc(self) -> _abi.CameraDesc:
+        c = _abi.CameraDesc()
+        c.rot[:] = [float(v) for v in self.rot]
+        c.origin[:] = [float(v) for v in self.origin]
+        c.fx, c.fy, c.cx, c.cy = float(self.fx), float(self.fy), float(self.cx), float(self.cy)
+        c.width, c.height = int(self.width), int(self.height)
+        c.t_near, c.t_far = float(self.t_near), float(self.t_far)
+        return c
+
+    @classmethod
+    def from_spec(cls, spec) -> "CameraModel":
+        return cls(tuple(spec.rot), tuple(spec.origin), spec.fx, spec.fy, spec.cx, spec.cy,
+                   spec.width, spec.height, spec.t_near, spec.t_far)
+
+
+@dataclass
+class RenderOptions:
+    """proj/include/lumi/renderer.h:22-30."""
+
+    samples_per_ray: int = 256
+    lod_bias: float = 0.0
+    lod_enabled: bool = True
+    termination_transmittance: float = 1e-4
+    background: Sequence[float] = (0.0, 0.0, 0.0)
+    contraction: ContractionMode = ContractionMode.kLInfCubic
+    chunk_size: int = 32
+
+    def desc(self) -> _abi.RenderOptionsDesc:
+        o = _abi.RenderOptionsDesc()
+        o.samples_per_ray = int(self.samples_per_ray)
+        o.lod_enabled = 1 if self.lod_enabled else 0
+        o.lod_bias = float(self.lod_bias)
+        o.termination_transmittance = float(self.termination_transmittance)
+        o.background[:] = [float(v) for v in self.background]
+        o.contraction = int(self.contraction)
+        o.chunk_size = int(self.chunk_size)
+        return o
+
+
+@dataclass
+class RowStats:
+    """proj/include/lumi/renderer.h:241-246."""
+
+    row: int = 0
+    ms: float = 0.0
+    rays: int = 0
+    evals: int = 0
+
+
+class Image:
+    """Planar channel-major float image (image.h:16-35): data[c, y, x]."""
+
+    def __init__(self, width: int, height: int, channels: int, fill: float = 0.0):
+        self.width, self.height, self.channels = int(width), int(height), int(channels)
+        self.data = np.full((self.channels, self.height, self.width), fill, np.float32)
+
+    def at(self, x: int, y: int, c: int) -> float:
+        return float(self.data[c, y, x])
+
+
+def device_info(device: int = 0) -> str:
+    buf = C.create_string_buffer(256)
+    check(_abi.lib().lumi_device_info(device, buf, 256))
+    return buf.value.decode()
+
+
+class DeviceModel:
+    """A field + occupancy grid resident on one B200 (LumiModel*)."""
+
+    def __init__(self, field: RadianceField, grid: OccupancyGrid, device: int = 0):
+        self.device = device
+        self.cfg = field.cfg
+        h = C.c_void_p()
+        d = field.cfg.desc()
+        check(_abi.lib().lumi_model_create(device, C.byref(d), _p(field.grid_params),
+                                           _p(field.density_params), _p(field.color_params),
+                                           _p(grid.bits), grid.res, C.byref(h)))
+        self.h = h
+        self.field_version = field.version
+        self.grid_version = grid.version
+        self._lock = threading.Lock()
+
+    def set_occupancy(self, grid: OccupancyGrid) -> None:
+        check(_abi.lib().lumi_model_set_occupancy(self.h, _p(grid.bits), grid.res))
+        self.grid_version = grid.version
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            _abi.lib().lumi_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def nbytes(self) -> int:
+        v = C.c_uint64()
+        check(_abi.lib().lumi_model_bytes(self.h, C.byref(v)))
+        return int(v.value)
+
+    # -- rendering -------------------------------------------------------------------
+    def render_rows(self, cam: CameraModel, opts: RenderOptions, row_begin: int, row_end: int,
+                    out: np.ndarray, depth: Optional[np.ndarray] = None,
+                    opacity: Optional[np.ndarray] = None,
+                    stats: Optional[List[RowStats]] = None) -> None:
+        """Synchronous, host buffers (renderer.h:252-278 semantics)."""
+        W, H = cam.width, cam.height
+        for name, a, shape in (("out", out, (3, H, W)), ("depth", depth, (H, W)),
+                               ("opacity", opacity, (H, W))):
+            if a is not None and (a.dtype != np.float32 or a.size != int(np.prod(shape)) or
+                                  not a.flags.c_contiguous):
+                raise Error(f"render_rows: {name} must be a contiguous float32 image of {shape}")
+        rows = max(row_end - row_begin, 0)
+        st = (_abi.RowStatsDesc * max(rows, 1))()
+        cd, od = cam.desc(), opts.desc()
+        check(_abi.lib().lumi_render_rows(self.h, C.byref(cd), C.byref(od), row_begin, row_end,
+                                          _p(out), _p(depth), _p(opacity),
+                                          st if stats is not None else None))
+        if stats is not None:
+            for i in range(rows):
+                stats.append(RowStats(st[i].row, st[i].ms, st[i].rays, st[i].evals))
+
+    def render_rows_async(self, cam: CameraModel, opts: RenderOptions, row_begin: int,
+                          row_end: int, target: _abi.FrameTarget, stream: int = 0) -> None:
+        """Device-resident variant: `target` holds device pointers; enqueued on `stream`."""
+        cd, od = cam.desc(), opts.desc()
+        check(_abi.lib().lumi_render_rows_async(self.h, C.byref(cd), C.byref(od), row_begin,
+                                                row_end, C.byref(target), C.c_void_p(stream)))
+
+    def march_kept_async(self, cam: CameraModel, opts: RenderOptions, row_begin: int,
+                         row_end: int, mask_ptr: int, counts_ptr: int, stream: int = 0) -> None:
+        cd, od = cam.desc(), opts.desc()
+        check(_abi.lib().lumi_march_kept_async(self.h, C.byref(cd), C.byref(od), row_begin,
+                                               row_end, C.c_void_p(mask_ptr),
+                                               C.c_void_p(counts_ptr), C.c_void_p(stream)))
+
+    def bake_occupancy(self, cams: Sequence[CameraModel], samples_per_ray: int,
+                       points_per_axis: int, resolution: int, alpha: float,
+                       want_probe: bool = False):
+        """OccupancyGrid::probe + prune on the GPU (occupancy.cpp:97-154)."""
+        arr = (_abi.CameraDesc * max(len(cams), 1))(*[c.desc() for c in cams])
+        n = resolution ** 3
+        occ = np.zeros(n, np.uint8)
+        pm = np.zeros(n, np.float32) if want_probe else None
+        check(_abi.lib().lumi_bake_occupancy(self.h, arr, len(cams), samples_per_ray,
+                                             points_per_axis, resolution, float(alpha), _p(occ),
+                                             _p(pm)))
+        grid = OccupancyGrid(resolution, occ)
+        return (grid, pm) if want_probe else grid
+
+
+_cache_lock = threading.Lock()
+_model_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _device_model(field: RadianceField, grid: OccupancyGrid, device: int) -> DeviceModel:
+    with _cache_lock:
+        per_field = _model_cache.setdefault(field, {})
+        key = (device, id(grid))
+        m = per_field.get(key)
+        if m is None or m.field_version != field.version:
+            if m is not None:
+                m.close()
+            m = DeviceModel(field, grid, device)
+            per_field[key] = m
+        elif m.grid_version != grid.version:
+            m.set_occupancy(grid)
+        return m
+
+
+def render_rows(field: RadianceField, grid: OccupancyGrid, cam: CameraModel, opts: RenderOptions,
+                row_begin: int, row_end: int, out, depth_out=None, opacity_out=None,
+                stats: Optional[List[RowStats]] = None, device: int = 0) -> None:
+    """Drop-in for lumi::render_rows (renderer.h:252-278): renders rows [row_begin, row_end)
+    of `cam` into the full-size planar `out` (Image or float32 [3,H,W]); optional depth /
+    opacity planes; `stats` is appended one RowStats per row.  Raises Error on a bad row range
+    exactly like the reference's require()."""
+    def arr(a):
+        return None if a is None else (a.data if isinstance(a, Image) else a)
+
+    if not (row_begin >= 0 and row_end <= cam.height and row_begin <= row_end):
+        raise Error("render_rows: row range outside image")
+    m = _device_model(field, grid, device)
+    m.render_rows(cam, opts, row_begin, row_end, arr(out), arr(depth_out), arr(opacity_out), stats)
+
+
+def lod_levels_of(cfg: FieldConfig) -> List[int]:
+    return [cfg.grid.resolution(l) for l in range(cfg.grid.levels)]

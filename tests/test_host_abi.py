@@ -1,0 +1,90 @@
+"""CPU checks of the product boundary: the C-ABI library loads and exports every symbol
+include/lumi_cuda.h declares; host-side model construction (layout, seeded synthetic
+parameters) and argument validation match the reference -- no GPU compute here."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2311_02542_b200 as L
+from paper_2311_02542_b200 import _abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "lumi_cuda.h")).read()
+    return sorted(set(re.findall(r"\b(lumi_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(_abi.LIB_PATH)
+    names = declared_symbols()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_abi.SIGNATURES)  # the Python binding covers the whole ABI
+    assert _abi.lib().lumi_abi_version() == 1
+
+
+def test_layout_matches_reference_grid(oracle):
+    for ts in (1 << 15, 1 << 19, 1 << 22):
+        cfg = L.FieldConfig(grid=L.HashGridConfig(table_size=ts))
+        f = L.RadianceField(cfg)
+        lo = oracle.layout(O.field_config(table_size=ts))
+        assert f.layout.total_floats == lo.total_floats
+        for l in range(16):
+            assert f.layout.resolution[l] == lo.resolution[l] == cfg.grid.resolution(l)
+            assert f.layout.dense[l] == lo.dense[l]
+            assert f.layout.offset[l] == lo.offset[l]
+    # level 0 dense only at T=2^22; 65,061,249 entries -> 130M floats
+    f = L.RadianceField(L.FieldConfig(grid=L.HashGridConfig(table_size=1 << 22)))
+    assert f.level_is_dense(0) and not f.level_is_dense(1)
+    assert f.layout.total_floats == 2 * 65061249
+    assert f.layout.density_params == 3217 and f.layout.color_params == 6467
+
+
+@pytest.mark.parametrize("seed,amp,ts", [(1234, 1.0, 1 << 19), (7, 0.0, 1 << 12), (99, 0.5, 1 << 15)])
+def test_synthetic_params_bit_identical_to_reference_rng(oracle, seed, amp, ts):
+    f = L.RadianceField.synthetic(L.FieldConfig(grid=L.HashGridConfig(table_size=ts)), seed, amp)
+    p = oracle.synth_params(O.field_config(table_size=ts), seed, amp)
+    assert np.array_equal(f.grid_params, p.table)
+    assert np.array_equal(f.density_params, p.dparams)
+    assert np.array_equal(f.color_params, p.cparams)
+    g = L.RadianceField(L.FieldConfig(grid=L.HashGridConfig(table_size=ts)))
+    if amp == 0.0:
+        g.init_random(seed)
+        assert np.array_equal(g.grid_params, p.table)
+
+
+def test_unsupported_and_invalid_configs_fail_loudly():
+    with pytest.raises(L.Error):
+        L.RadianceField(L.FieldConfig(grid=L.HashGridConfig(table_size=1000)))
+    with pytest.raises(L.Error):
+        L.RadianceField(L.FieldConfig(hidden_width=32))
+    with pytest.raises(L.Error):
+        L.OccupancyGrid(0)
+
+
+def test_occupancy_index_matches_oracle(oracle):
+    g = L.OccupancyGrid(16)
+    rng = np.random.default_rng(3)
+    for p in rng.uniform(-2.2, 2.2, (300, 3)):
+        assert g.voxel_index(p) == oracle.voxel_index(16, p)
+
+
+def test_render_without_gpu_fails_loudly():
+    """No CPU fallback: on a host without a B200 model creation raises a CUDA error."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    f = L.RadianceField(L.FieldConfig(grid=L.HashGridConfig(table_size=1 << 12)))
+    with pytest.raises(L.Error) as ei:
+        L.DeviceModel(f, L.OccupancyGrid(8))
+    assert ei.value.code == _abi.LUMI_ERR_CUDA
