@@ -340,7 +340,7 @@ def run_ours(args):
                    "eyes": cfg.eyes, "table_size": spec.table_size, "rays_per_frame": rays_frame,
                    "samples_per_ray": opts.samples_per_ray, "parallelism": f"rows{world}",
                    "l2": "inputs larger than L2 (hash table %.0f MB fp32)" % (field.grid_params.nbytes / 1e6),
-                   "kernel": "k_render_simt"},
+                   "kernel": dm.kernel},
         "fps": round(fps, 3),
         "work": {"evals_per_ray": round(evals / max(rays, 1), 3),
                  "active_levels_per_eval": round(level_samples / max(evals, 1), 3),
@@ -348,7 +348,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": None if achieved is None else round(achieved, 1),
                      "peak": hbm, "unit": "GB/s",
                      "frac": None if achieved is None else round(achieved / hbm, 4),
-                     "traffic": ncu_traffic("k_render_simt"),
+                     "traffic": ncu_traffic("k_render_" + dm.kernel),
                      "algorithmic": "64 B per active (w_l>0) level-sample: 8 corners x 2 fp32"},
         "roofline_mlp": {"bound": "tensor", "achieved": None if mlp_tflops is None else round(mlp_tflops, 2),
                          "peak": peaks.get("bf16_tflops_sustained", 1398.6), "unit": "TFLOP/s",

@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(HERE, "lib", "liblumi_cuda.so")
 
 LUMI_MAX_LEVELS = 16
 LUMI_OK, LUMI_ERR_INVALID, LUMI_ERR_CUDA, LUMI_ERR_UNSUPPORTED = 0, 1, 2, 3
+LUMI_KERNEL_TC, LUMI_KERNEL_SIMT = 0, 1
 
 
 class Error(RuntimeError):
@@ -75,6 +76,7 @@ SIGNATURES = {
     "lumi_synth_params": ([_vp, _u64, _d, _vp, _vp, _vp], C.c_int),
     "lumi_model_create": ([_i, _vp, _vp, _vp, _vp, _vp, _i, _vp], C.c_int),
     "lumi_model_set_occupancy": ([_vp, _vp, _i], C.c_int),
+    "lumi_model_set_kernel": ([_vp, _i], C.c_int),
     "lumi_model_destroy": ([_vp], C.c_int),
     "lumi_model_bytes": ([_vp, _vp], C.c_int),
     "lumi_render_rows": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp], C.c_int),

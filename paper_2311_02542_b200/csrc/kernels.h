@@ -25,4 +25,6 @@ struct BakeParams {
 cudaError_t launch_render_simt(const lumi_dev::RenderParams& p, cudaStream_t s);
 cudaError_t launch_march_kept(const lumi_dev::RenderParams& p, uint32_t* mask, int32_t* counts,
                               cudaStream_t s);
+cudaError_t launch_render_tc(lumi_dev::RenderParams p, cudaStream_t s, int num_sms);
+size_t render_tc_smem_bytes();
 cudaError_t launch_bake(const lumi_dev::BakeParams& p, cudaStream_t s);

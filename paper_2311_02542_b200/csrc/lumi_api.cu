@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <numeric>
@@ -147,6 +148,8 @@ int check_opts(const LumiRenderOptions* o) {
 
 }  // namespace
 
+constexpr unsigned kCounterSlots = 64;
+
 struct LumiModel {
   int device = 0;
   LumiFieldDesc desc{};
@@ -156,7 +159,10 @@ struct LumiModel {
   float* d_cparams = nullptr;
   uint8_t* d_occ = nullptr;
   int occ_res = 0;
-  unsigned int* d_counter = nullptr;
+  unsigned int* d_counter = nullptr;  // kCounterSlots per-launch tile counters
+  std::atomic<unsigned> counter_slot{0};
+  int kernel = LUMI_KERNEL_TC;
+  int num_sms = 148;
   std::mutex mu;
   std::map<std::tuple<double, double, int>, std::pair<double*, double>> ts_cache;
 };
@@ -239,7 +245,7 @@ int make_params(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions
   p->chunk = o->chunk_size;
   p->row_begin = b;
   p->row_end = e;
-  p->work_counter = m->d_counter;
+  p->work_counter = m->d_counter + (m->counter_slot.fetch_add(1) % kCounterSlots) * 32;
   return LUMI_OK;
 }
 
@@ -350,14 +356,15 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
   if ((e = cudaMalloc(&m->d_table, lay.total_floats * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&m->d_dparams, lay.density_params * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&m->d_cparams, lay.color_params * sizeof(float))) != cudaSuccess ||
-      (e = cudaMalloc(&m->d_counter, 64 * sizeof(unsigned int))) != cudaSuccess ||
+      (e = cudaMalloc(&m->d_counter, kCounterSlots * 32 * sizeof(unsigned int))) != cudaSuccess ||
       (e = cudaMemcpy(m->d_table, table, lay.total_floats * sizeof(float),
                       cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(m->d_dparams, dparams, lay.density_params * sizeof(float),
                       cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(m->d_cparams, cparams, lay.color_params * sizeof(float),
                       cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMemset(m->d_counter, 0, 64 * sizeof(unsigned int))) != cudaSuccess)
+      (e = cudaMemset(m->d_counter, 0, kCounterSlots * 32 * sizeof(unsigned int))) != cudaSuccess ||
+      (e = cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess)
     return cleanup(fail(LUMI_ERR_CUDA, std::string("model upload: ") + cudaGetErrorString(e)));
   if ((rc = lumi_model_set_occupancy(m, occ, occ_res))) return cleanup(rc);
   *out = m;
@@ -393,6 +400,14 @@ int lumi_model_destroy(LumiModel* m) {
   return LUMI_OK;
 }
 
+int lumi_model_set_kernel(LumiModel* m, int kernel) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  if (kernel != LUMI_KERNEL_TC && kernel != LUMI_KERNEL_SIMT)
+    return fail(LUMI_ERR_INVALID, "unknown kernel variant");
+  m->kernel = kernel;
+  return LUMI_OK;
+}
+
 int lumi_model_bytes(const LumiModel* m, uint64_t* bytes) {
   if (!m || !bytes) return fail(LUMI_ERR_INVALID, "null argument");
   *bytes = (m->layout.total_floats + m->layout.density_params + m->layout.color_params) * 4 +
@@ -408,7 +423,10 @@ int lumi_render_rows_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRe
   int rc = make_params(m, cam, o, b, e, &p);
   if (rc) return rc;
   if ((rc = set_target(&p, t, b, e))) return rc;
-  LUMI_CUDA_TRY(launch_render_simt(p, static_cast<cudaStream_t>(stream)));
+  if (m->kernel == LUMI_KERNEL_SIMT)
+    LUMI_CUDA_TRY(launch_render_simt(p, static_cast<cudaStream_t>(stream)));
+  else
+    LUMI_CUDA_TRY(launch_render_tc(p, static_cast<cudaStream_t>(stream), m->num_sms));
   return LUMI_OK;
 }
 

@@ -1,0 +1,426 @@
+// render_tc.cu -- the B200 frame renderer: a persistent kernel in which every CTA owns 128
+// live rays (one per thread), marches each to its next occupancy-kept sample, gathers the
+// mip hash-grid features for that sample, runs the five 64-wide MLP layers of the whole
+// 128-sample batch on the 5th-generation tensor cores (tcgen05.mma, fp16 operands staged in
+// shared memory, fp32 accumulators in TMEM) and composites front to back in registers.
+//
+// Thread t  <->  ray slot t  <->  batch row t  <->  TMEM lane t.  Rays that terminate or run
+// out of samples are replaced from a tile queue (16x8-pixel tiles handed out by a global
+// atomic), so the batch stays full and spatially coherent (neighbouring rays at similar
+// depths gather neighbouring hash-grid cells).
+//
+// Reference semantics: renderer.h:126-237 (march / flush / composite), field.h:106-137
+// (forward_chunk), grid.h:90-167 (encode).  Geometry and the occupancy test are bit-exact
+// (geometry.cuh); features are bit-exact (field.cuh); the MLP runs in fp16 x fp16 -> fp32 on
+// tensor cores (oracle-measured error 1.6e-4 max |dPQ| at C1 vs the 1e-3 bar).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "render_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace lumi_dev {
+namespace tc {
+
+constexpr int kThreads = 128;  // UMMA M
+constexpr int kTileW = 16, kTileH = 8;
+constexpr uint32_t kTmemCols = 64;
+
+struct __align__(1024) Smem {
+  uint8_t A[128 * 64 * 2];   // activations, K-major core-matrix tile (K <= 64)
+  uint8_t W1[64 * 32 * 2];   // density L1  N=64 K=32
+  uint8_t W2[32 * 64 * 2];   // density L2  N=32 (17 used) K=64
+  uint8_t C1[64 * 32 * 2];   // colour L1   N=64 K=32
+  uint8_t C2[64 * 64 * 2];   // colour L2   N=64 K=64
+  uint8_t C3[16 * 64 * 2];   // colour L3   N=16 (3 used) K=64
+  float b1[64], b2[32], cb1[64], cb2[64], cb3[16];
+  double ts[kMaxSamples];
+  uint64_t mbar;
+  uint32_t tmem_base;
+  int q_next, q_end, q_done;
+};
+
+// byte offset of (row, 8-element K chunk) in a K-major SWIZZLE_NONE tile with kchunks chunks
+__device__ __forceinline__ uint32_t core_off(int row, int chunk, int kchunks) {
+  return (uint32_t)((row >> 3) * (kchunks * 128) + chunk * 128 + (row & 7) * 16);
+}
+
+__device__ __forceinline__ uint4 pack8(const float* v) {
+  __half2 h0 = __floats2half2_rn(v[0], v[1]), h1 = __floats2half2_rn(v[2], v[3]),
+          h2 = __floats2half2_rn(v[4], v[5]), h3 = __floats2half2_rn(v[6], v[7]);
+  uint4 u;
+  u.x = *reinterpret_cast<uint32_t*>(&h0);
+  u.y = *reinterpret_cast<uint32_t*>(&h1);
+  u.z = *reinterpret_cast<uint32_t*>(&h2);
+  u.w = *reinterpret_cast<uint32_t*>(&h3);
+  return u;
+}
+
+__device__ __forceinline__ void st_shared16(uint8_t* base, uint32_t off, uint4 v) {
+  *reinterpret_cast<uint4*>(base + off) = v;
+}
+
+// weights [n_real x K] fp32 row-major (network.h:64) -> fp16 tile with n_pad rows
+__device__ void load_weight_tile(uint8_t* dst, const float* __restrict__ W, int n_real, int n_pad,
+                                 int K) {
+  const int kch = K / 8;
+  for (int it = threadIdx.x; it < n_pad * kch; it += blockDim.x) {
+    const int n = it / kch, j = it % kch;
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = n < n_real ? __ldg(W + (size_t)n * K + 8 * j + q) : 0.f;
+    st_shared16(dst, core_off(n, j, kch), pack8(v));
+  }
+}
+
+template <int N, int K>
+__device__ __forceinline__ void issue_layer(const Smem& s, const uint8_t* B, uint32_t d_tmem) {
+  constexpr uint32_t idesc = ptx::idesc_f16_f32<128, N>();
+  const uint32_t a = ptx::smem_addr(s.A), b = ptx::smem_addr(B);
+#pragma unroll
+  for (int kk = 0; kk < K / 16; ++kk) {
+    const uint64_t ad = ptx::make_smem_desc(a + kk * 256, 128, (K / 8) * 128);
+    const uint64_t bd = ptx::make_smem_desc(b + kk * 256, 128, (K / 8) * 128);
+    ptx::mma_f16(d_tmem, ad, bd, idesc, kk > 0 ? 1u : 0u);
+  }
+}
+
+struct Ray {
+  int id, x, y;
+  d3 d, nd;
+  int i, kept, contributing, cut_limit;
+  bool term;
+  double trans, px, py, pz, depth, opac;
+};
+
+struct Sample {
+  d3 c;
+  double t, delta;
+  LodW lw;
+};
+
+struct Counters {
+  unsigned long long evals, level_samples, marched, rays;
+};
+
+__device__ __forceinline__ bool occupied(const RenderParams& p, d3 c) {
+  const int64_t vi = voxel_index(c, p.occ_res);
+  return vi >= 0 && __ldg(p.occ + vi) != 0;
+}
+
+__device__ __forceinline__ bool take_ray(const RenderParams& p, Smem& s, Ray& r) {
+  for (;;) {
+    const int idx = atomicAdd(&s.q_next, 1);
+    if (idx >= s.q_end) return false;
+    const int tile = idx / (kTileW * kTileH), w = idx % (kTileW * kTileH);
+    const int x = (tile % p.tiles_x) * kTileW + (w % kTileW);
+    const int y = p.row_begin + (tile / p.tiles_x) * kTileH + w / kTileW;
+    if (x >= p.cam.width || y >= p.row_end) continue;  // partial edge tile
+    r.id = idx;
+    r.x = x;
+    r.y = y;
+    r.d = ray_dir(p.cam, (double)x + 0.5, (double)y + 0.5);
+    r.nd = ray_dir(p.cam, (double)x + 1.5, (double)y + 0.5);
+    r.i = 0;
+    r.kept = r.contributing = 0;
+    r.cut_limit = 0x7fffffff;
+    r.term = false;
+    r.trans = 1.0;
+    r.px = r.py = r.pz = r.depth = r.opac = 0.0;
+    return true;
+  }
+}
+
+// March to the next occupancy-kept candidate (renderer.h:205-224).  Returns false when the
+// ray is finished (candidates exhausted, or the post-cut chunk tail has been counted).
+__device__ __forceinline__ bool advance(const RenderParams& p, const double* ts, Ray& r,
+                                        Sample& smp, Counters& cnt) {
+  if (r.term && r.kept >= r.cut_limit) return false;
+  const d3 o{p.cam.origin[0], p.cam.origin[1], p.cam.origin[2]};
+  while (r.i < p.n) {
+    const int i = r.i++;
+    ++cnt.marched;
+    const double t = ts[i];
+    const d3 c = contract(ray_at(o, r.d, t), p.contraction);
+    if (!occupied(p, c)) continue;
+    ++r.kept;
+    if (r.term) {
+      if (r.kept >= r.cut_limit) return false;
+      continue;
+    }
+    smp.c = c;
+    smp.t = t;
+    smp.delta = (i + 1 < p.n) ? dsub(ts[i + 1], t) : dmul(t, dsub(p.ratio, 1.0));
+    if (p.lod_enabled) {
+      const double rc = contracted_footprint(o, r.d, r.nd, t, p.contraction);
+      smp.lw = lod_weights(lod_level(dmax(rc, 1e-12), p.grid.two_base, p.grid.log_scale,
+                                     p.grid.levels),
+                           p.lod_bias, p.grid.levels);
+    } else {
+      smp.lw = LodW{p.grid.levels, 0.f, false};
+    }
+    cnt.level_samples += active_levels(smp.lw, p.grid.levels);
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void finish(const RenderParams& p, Ray& r, Counters& cnt) {
+  RayResult res{r.px, r.py, r.pz, r.depth, r.opac,
+                chunk_evals(r.term, r.contributing, r.kept, p.chunk), r.contributing};
+  store_ray(p, r.x, r.y, res, r.trans);
+  ++cnt.rays;
+  r.id = -1;
+}
+
+__device__ void refill(const RenderParams& p, Smem& s, int total) {
+  if (s.q_next < s.q_end || s.q_done) return;
+  const int base = (int)atomicAdd(p.work_counter, (unsigned)(kTileW * kTileH));
+  if (base >= total) {
+    s.q_done = 1;
+    s.q_next = s.q_end = 0;
+  } else {
+    s.q_next = base;
+    s.q_end = min(base + kTileW * kTileH, total);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 3) k_render_tc(RenderParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  // ---- one-time setup: weights -> fp16 core-matrix tiles, biases, distances, TMEM --------
+  const float* dp = p.mlp.dparams;
+  const float* cp = p.mlp.cparams;
+  load_weight_tile(s.W1, dp, 64, 64, 32);
+  load_weight_tile(s.W2, dp + 64 * 32 + 64, 1 + kBottleneck, 32, 64);
+  load_weight_tile(s.C1, cp, 64, 64, 32);
+  load_weight_tile(s.C2, cp + 64 * 32 + 64, 64, 64, 64);
+  load_weight_tile(s.C3, cp + 64 * 32 + 64 + 64 * 64 + 64, 3, 16, 64);
+  for (int i = tid; i < 64; i += kThreads) {
+    s.b1[i] = dp[64 * 32 + i];
+    s.cb1[i] = cp[64 * 32 + i];
+    s.cb2[i] = cp[64 * 32 + 64 + 64 * 64 + i];
+  }
+  for (int i = tid; i < 32; i += kThreads) s.b2[i] = i < 17 ? dp[64 * 32 + 64 + 17 * 64 + i] : 0.f;
+  for (int i = tid; i < 16; i += kThreads)
+    s.cb3[i] = i < 3 ? cp[64 * 32 + 64 + 64 * 64 + 64 + 3 * 64 + i] : 0.f;
+  for (int i = tid; i < p.n; i += kThreads) s.ts[i] = p.ts[i];
+  const int tiles_y = (p.row_end - p.row_begin + kTileH - 1) / kTileH;
+  const int total = p.tiles_x * tiles_y * kTileW * kTileH;
+  if (tid == 0) {
+    ptx::mbar_init(&s.mbar, 1);
+    ptx::fence_mbar_init();
+    s.q_next = s.q_end = 0;
+    s.q_done = 0;
+    refill(p, s, total);
+  }
+  if (warp == 0) ptx::tmem_alloc<kTmemCols>(&s.tmem_base);
+  ptx::fence_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+  const uint32_t t_lane = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's 32 TMEM lanes
+
+  Counters cnt{0, 0, 0, 0};
+  Ray r;
+  r.id = -1;
+  uint32_t phase = 0;
+  const bool issuer = (tid == 0);
+
+  for (;;) {
+    // ---- A: every thread brings one kept sample (refilling finished rays) ------------------
+    Sample smp;
+    bool have = false;
+    for (;;) {
+      if (r.id < 0 && !take_ray(p, s, r)) break;
+      if (advance(p, s.ts, r, smp, cnt)) {
+        have = true;
+        break;
+      }
+      finish(p, r, cnt);
+    }
+    // ---- B: hash-grid gather -> fp16 row of A (K = 32) --------------------------------------
+    if (have) {
+      float feat[kFeat];
+      encode(p.grid, smp.c, smp.lw, feat);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) st_shared16(s.A, core_off(tid, j, 4), pack8(feat + 8 * j));
+    }
+    ptx::fence_async_smem();
+    if (!__syncthreads_or(have)) {
+      if (tid == 0) refill(p, s, total);
+      __syncthreads();
+      if (s.q_done && s.q_next >= s.q_end) break;
+      continue;
+    }
+
+    float v[64];
+    // ---- density L1: [128x32] x [32x64] -> relu -------------------------------------------
+    if (issuer) {
+      ptx::tc_fence_after();
+      issue_layer<64, 32>(s, s.W1, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ptx::tmem_ld16(t_lane + 16 * q, v + 16 * q);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 64; ++j) v[j] = fmaxf(v[j] + s.b1[j], 0.f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) st_shared16(s.A, core_off(tid, j, 8), pack8(v + 8 * j));
+    ptx::fence_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+
+    // ---- density L2: [128x64] x [64x32(17)] -> sigma, bottleneck ++ SH ---------------------
+    if (issuer) {
+      ptx::tc_fence_after();
+      issue_layer<32, 64>(s, s.W2, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+    ptx::tmem_ld16(t_lane, v);
+    ptx::tmem_ld16(t_lane + 16, v + 16);
+    ptx::tmem_ld_wait();
+    const float sigma = trunc_exp(v[0] + s.b2[0]);
+    {
+      float cin[32];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) cin[j] = v[1 + j] + s.b2[1 + j];
+      sh_encode(r.d, cin + 16);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) st_shared16(s.A, core_off(tid, j, 4), pack8(cin + 8 * j));
+    }
+    ptx::fence_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+
+    // ---- colour L1: [128x32] x [32x64] -> relu -------------------------------------------
+    if (issuer) {
+      ptx::tc_fence_after();
+      issue_layer<64, 32>(s, s.C1, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ptx::tmem_ld16(t_lane + 16 * q, v + 16 * q);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 64; ++j) v[j] = fmaxf(v[j] + s.cb1[j], 0.f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) st_shared16(s.A, core_off(tid, j, 8), pack8(v + 8 * j));
+    ptx::fence_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+
+    // ---- colour L2: [128x64] x [64x64] -> relu -------------------------------------------
+    if (issuer) {
+      ptx::tc_fence_after();
+      issue_layer<64, 64>(s, s.C2, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ptx::tmem_ld16(t_lane + 16 * q, v + 16 * q);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 64; ++j) v[j] = fmaxf(v[j] + s.cb2[j], 0.f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) st_shared16(s.A, core_off(tid, j, 8), pack8(v + 8 * j));
+    ptx::fence_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+
+    // ---- colour L3: [128x64] x [64x16(3)] -> sigmoid (PQ head) ---------------------------
+    if (issuer) {
+      ptx::tc_fence_after();
+      issue_layer<16, 64>(s, s.C3, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+    ptx::tmem_ld16(t_lane, v);
+    ptx::tmem_ld_wait();
+    ptx::tc_fence_before();
+
+    // ---- C: front-to-back compositing (renderer.h:170-190), double ----------------------
+    if (have) {
+      float rgb[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float raw = v[k] + s.cb3[k];
+        rgb[k] = p.mlp.color_space == 0 ? sigmoid(raw) : trunc_exp(raw);
+      }
+      const double a = dsub(1.0, exp(dmul(-(double)sigma, smp.delta)));
+      const double w = dmul(r.trans, a);
+      r.px = dadd(r.px, dmul(w, (double)rgb[0]));
+      r.py = dadd(r.py, dmul(w, (double)rgb[1]));
+      r.pz = dadd(r.pz, dmul(w, (double)rgb[2]));
+      r.depth = dadd(r.depth, dmul(w, smp.t));
+      r.opac = dadd(r.opac, w);
+      r.trans = dmul(r.trans, dsub(1.0, a));
+      ++r.contributing;
+      ++cnt.evals;
+      if (p.t_cut > 0 && r.trans < p.t_cut) {
+        r.term = true;
+        r.cut_limit = ((r.contributing + p.chunk - 1) / p.chunk) * p.chunk;
+      }
+    }
+    if (tid == 0) refill(p, s, total);
+    __syncthreads();
+  }
+
+  // ---- teardown --------------------------------------------------------------------------
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 0) ptx::tmem_dealloc<kTmemCols>(tmem);
+  add_work_stats(p, cnt.evals, cnt.level_samples, cnt.marched, cnt.rays);
+}
+
+}  // namespace tc
+}  // namespace lumi_dev
+
+using namespace lumi_dev;
+
+size_t render_tc_smem_bytes() { return sizeof(tc::Smem) + 1024; }
+
+cudaError_t launch_render_tc(RenderParams p, cudaStream_t s, int num_sms) {
+  const long long rays = (long long)(p.row_end - p.row_begin) * p.cam.width;
+  if (rays <= 0) return cudaSuccess;
+  static int blocks_per_sm = -1;
+  const size_t smem = render_tc_smem_bytes();
+  if (blocks_per_sm < 0) {
+    cudaError_t e = cudaFuncSetAttribute(tc::k_render_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, tc::k_render_tc, tc::kThreads,
+                                                      smem);
+    if (e != cudaSuccess) return e;
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  p.tile_w = tc::kTileW;
+  p.tile_h = tc::kTileH;
+  p.tiles_x = (p.cam.width + tc::kTileW - 1) / tc::kTileW;
+  const long long tiles =
+      (long long)p.tiles_x * ((p.row_end - p.row_begin + tc::kTileH - 1) / tc::kTileH);
+  const long long grid = std::min<long long>((long long)blocks_per_sm * num_sms, tiles);
+  cudaError_t e = cudaMemsetAsync(p.work_counter, 0, sizeof(unsigned int), s);
+  if (e != cudaSuccess) return e;
+  tc::k_render_tc<<<(unsigned)grid, tc::kThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}

@@ -278,7 +278,14 @@ class DeviceModel:
         self.h = h
         self.field_version = field.version
         self.grid_version = grid.version
+        self.kernel = "tc"
         self._lock = threading.Lock()
+
+    def set_kernel(self, kernel: str) -> None:
+        """'tc' (persistent tcgen05 kernel, default) or 'simt' (fp32 CUDA-core cross-check)."""
+        k = {"tc": _abi.LUMI_KERNEL_TC, "simt": _abi.LUMI_KERNEL_SIMT}[kernel]
+        check(_abi.lib().lumi_model_set_kernel(self.h, k))
+        self.kernel = kernel
 
     def set_occupancy(self, grid: OccupancyGrid) -> None:
         check(_abi.lib().lumi_model_set_occupancy(self.h, _p(grid.bits), grid.res))
