@@ -38,6 +38,12 @@ struct RenderParams {
   // persistent scheduling
   unsigned int* work_counter;
   int tile_w, tile_h, tiles_x, tiles_total;
+  // occupancy-kept candidates per ray id (tile-major ids), from the march pass:
+  // kept_mask[word * total_rays + id], kept_count[id]
+  uint32_t* kept_mask;
+  uint16_t* kept_count;
+  int mask_words;
+  long long total_rays;
 };
 
 // color.cpp:17-44 constants (scene-linear 1.0 = 100 cd/m^2)
@@ -111,19 +117,17 @@ __device__ __forceinline__ void add_work_stats(const RenderParams& p, unsigned l
                                                unsigned long long candidates,
                                                unsigned long long rays) {
   if (!p.work_stats) return;
+  // per-thread values stay far below 2^27, so 32-bit warp sums cannot overflow
   const unsigned mask = __activemask();
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    evals += __shfl_xor_sync(mask, evals, o);
-    level_samples += __shfl_xor_sync(mask, level_samples, o);
-    candidates += __shfl_xor_sync(mask, candidates, o);
-    rays += __shfl_xor_sync(mask, rays, o);
-  }
+  const unsigned e = __reduce_add_sync(mask, (unsigned)evals);
+  const unsigned l = __reduce_add_sync(mask, (unsigned)level_samples);
+  const unsigned c = __reduce_add_sync(mask, (unsigned)candidates);
+  const unsigned r = __reduce_add_sync(mask, (unsigned)rays);
   if ((threadIdx.x & 31) == (__ffs(mask) - 1)) {
-    atomicAdd(p.work_stats + 0, evals);
-    atomicAdd(p.work_stats + 1, level_samples);
-    atomicAdd(p.work_stats + 2, candidates);
-    atomicAdd(p.work_stats + 3, rays);
+    atomicAdd(p.work_stats + 0, (unsigned long long)e);
+    atomicAdd(p.work_stats + 1, (unsigned long long)l);
+    atomicAdd(p.work_stats + 2, (unsigned long long)c);
+    atomicAdd(p.work_stats + 3, (unsigned long long)r);
   }
 }
 

@@ -16,6 +16,9 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "kernels.h"
 #include "render_common.cuh"
 #include "tc_ptx.cuh"
@@ -39,6 +42,8 @@ struct __align__(1024) Smem {
   uint64_t mbar;
   uint32_t tmem_base;
   int q_next, q_end, q_done;
+  uint8_t pair_src[kThreads / 32][32 * kMaxLevels];  // per-warp (sample lane, level) work list
+  uint8_t pair_lvl[kThreads / 32][32 * kMaxLevels];
 };
 
 // byte offset of (row, 8-element K chunk) in a K-major SWIZZLE_NONE tile with kchunks chunks
@@ -89,7 +94,8 @@ __device__ __forceinline__ void issue_layer(const Smem& s, const uint8_t* B, uin
 struct Ray {
   int id, x, y;
   d3 d, nd;
-  int i, kept, contributing, cut_limit;
+  int wi, kept_total, contributing, cut_limit;
+  uint32_t word;  // unvisited kept candidates of mask word wi
   bool term;
   double trans, px, py, pz, depth, opac;
 };
@@ -109,21 +115,31 @@ __device__ __forceinline__ bool occupied(const RenderParams& p, d3 c) {
   return vi >= 0 && __ldg(p.occ + vi) != 0;
 }
 
+// ray id (tile-major: 16x8 tiles, row-major inside a tile) -> pixel; false for the padding
+// ids of partial edge tiles
+__device__ __forceinline__ bool ray_pixel(const RenderParams& p, long long idx, int& x, int& y) {
+  const long long tile = idx / (kTileW * kTileH);
+  const int w = (int)(idx % (kTileW * kTileH));
+  x = (int)(tile % p.tiles_x) * kTileW + (w % kTileW);
+  y = p.row_begin + (int)(tile / p.tiles_x) * kTileH + w / kTileW;
+  return x < p.cam.width && y < p.row_end;
+}
+
 __device__ __forceinline__ bool take_ray(const RenderParams& p, Smem& s, Ray& r) {
   for (;;) {
     const int idx = atomicAdd(&s.q_next, 1);
     if (idx >= s.q_end) return false;
-    const int tile = idx / (kTileW * kTileH), w = idx % (kTileW * kTileH);
-    const int x = (tile % p.tiles_x) * kTileW + (w % kTileW);
-    const int y = p.row_begin + (tile / p.tiles_x) * kTileH + w / kTileW;
-    if (x >= p.cam.width || y >= p.row_end) continue;  // partial edge tile
+    int x, y;
+    if (!ray_pixel(p, idx, x, y)) continue;
     r.id = idx;
     r.x = x;
     r.y = y;
     r.d = ray_dir(p.cam, (double)x + 0.5, (double)y + 0.5);
     r.nd = ray_dir(p.cam, (double)x + 1.5, (double)y + 0.5);
-    r.i = 0;
-    r.kept = r.contributing = 0;
+    r.wi = 0;
+    r.word = __ldg(p.kept_mask + idx);
+    r.kept_total = __ldg(p.kept_count + idx);
+    r.contributing = 0;
     r.cut_limit = 0x7fffffff;
     r.term = false;
     r.trans = 1.0;
@@ -132,46 +148,68 @@ __device__ __forceinline__ bool take_ray(const RenderParams& p, Smem& s, Ray& r)
   }
 }
 
-// March to the next occupancy-kept candidate (renderer.h:205-224).  Returns false when the
-// ray is finished (candidates exhausted, or the post-cut chunk tail has been counted).
+// Next occupancy-kept candidate of the ray (renderer.h:205-224), read from the march-pass
+// bitmask.  Returns false when the ray is finished (no kept candidate left, or cut).
 __device__ __forceinline__ bool advance(const RenderParams& p, const double* ts, Ray& r,
                                         Sample& smp, Counters& cnt) {
-  if (r.term && r.kept >= r.cut_limit) return false;
-  const d3 o{p.cam.origin[0], p.cam.origin[1], p.cam.origin[2]};
-  while (r.i < p.n) {
-    const int i = r.i++;
-    ++cnt.marched;
-    const double t = ts[i];
-    const d3 c = contract(ray_at(o, r.d, t), p.contraction);
-    if (!occupied(p, c)) continue;
-    ++r.kept;
-    if (r.term) {
-      if (r.kept >= r.cut_limit) return false;
-      continue;
-    }
-    smp.c = c;
-    smp.t = t;
-    smp.delta = (i + 1 < p.n) ? dsub(ts[i + 1], t) : dmul(t, dsub(p.ratio, 1.0));
-    if (p.lod_enabled) {
-      const double rc = contracted_footprint(o, r.d, r.nd, t, p.contraction);
-      smp.lw = lod_weights(lod_level(dmax(rc, 1e-12), p.grid.two_base, p.grid.log_scale,
-                                     p.grid.levels),
-                           p.lod_bias, p.grid.levels);
-    } else {
-      smp.lw = LodW{p.grid.levels, 0.f, false};
-    }
-    cnt.level_samples += active_levels(smp.lw, p.grid.levels);
-    return true;
+  if (r.term) return false;
+  while (r.word == 0) {
+    if (++r.wi >= p.mask_words) return false;
+    r.word = __ldg(p.kept_mask + (size_t)r.wi * p.total_rays + r.id);
   }
-  return false;
+  const int i = r.wi * 32 + __ffs(r.word) - 1;
+  r.word &= r.word - 1;
+  const d3 o{p.cam.origin[0], p.cam.origin[1], p.cam.origin[2]};
+  const double t = ts[i];
+  smp.c = contract(ray_at(o, r.d, t), p.contraction);
+  smp.t = t;
+  smp.delta = (i + 1 < p.n) ? dsub(ts[i + 1], t) : dmul(t, dsub(p.ratio, 1.0));
+  if (p.lod_enabled) {
+    const double rc = contracted_footprint(o, r.d, r.nd, t, p.contraction);
+    smp.lw = lod_weights(lod_level(dmax(rc, 1e-12), p.grid.two_base, p.grid.log_scale,
+                                   p.grid.levels),
+                         p.lod_bias, p.grid.levels);
+  } else {
+    smp.lw = LodW{p.grid.levels, 0.f, false};
+  }
+  cnt.level_samples += active_levels(smp.lw, p.grid.levels);
+  return true;
 }
 
 __device__ __forceinline__ void finish(const RenderParams& p, Ray& r, Counters& cnt) {
   RayResult res{r.px, r.py, r.pz, r.depth, r.opac,
-                chunk_evals(r.term, r.contributing, r.kept, p.chunk), r.contributing};
+                chunk_evals(r.term, r.contributing, r.kept_total, p.chunk), r.contributing};
   store_ray(p, r.x, r.y, res, r.trans);
   ++cnt.rays;
   r.id = -1;
+}
+
+// March pass: every candidate of every ray through the exact occupancy test
+// (renderer.h:205-208), one thread per ray in tile-major id order; writes the kept bitmask
+// [word][ray] and the kept count.  Uniform 256-iteration loops, no divergence on ray length.
+__global__ void __launch_bounds__(128) k_march_mask(RenderParams p) {
+  __shared__ double s_ts[kMaxSamples];
+  for (int i = threadIdx.x; i < p.n; i += blockDim.x) s_ts[i] = p.ts[i];
+  __syncthreads();
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= p.total_rays) return;
+  int x, y;
+  const bool valid = ray_pixel(p, idx, x, y);
+  const d3 o{p.cam.origin[0], p.cam.origin[1], p.cam.origin[2]};
+  const d3 d = valid ? ray_dir(p.cam, (double)x + 0.5, (double)y + 0.5) : d3{0, 0, 1};
+  int count = 0;
+  for (int w0 = 0; w0 < p.mask_words; ++w0) {
+    uint32_t bits = 0;
+    if (valid) {
+      const int hi = min(32, p.n - w0 * 32);
+      for (int b = 0; b < hi; ++b)
+        if (occupied(p, contract(ray_at(o, d, s_ts[w0 * 32 + b]), p.contraction))) bits |= 1u << b;
+    }
+    count += __popc(bits);
+    p.kept_mask[(size_t)w0 * p.total_rays + idx] = bits;
+  }
+  p.kept_count[idx] = (uint16_t)count;
+  add_work_stats(p, 0, 0, valid ? (unsigned long long)p.n : 0ull, 0);
 }
 
 __device__ void refill(const RenderParams& p, Smem& s, int total) {
@@ -208,8 +246,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_tc(RenderParams p) {
   for (int i = tid; i < 16; i += kThreads)
     s.cb3[i] = i < 3 ? cp[64 * 32 + 64 + 64 * 64 + 64 + 3 * 64 + i] : 0.f;
   for (int i = tid; i < p.n; i += kThreads) s.ts[i] = p.ts[i];
-  const int tiles_y = (p.row_end - p.row_begin + kTileH - 1) / kTileH;
-  const int total = p.tiles_x * tiles_y * kTileW * kTileH;
+  const int total = (int)p.total_rays;
   if (tid == 0) {
     ptx::mbar_init(&s.mbar, 1);
     ptx::fence_mbar_init();
@@ -243,12 +280,55 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_tc(RenderParams p) {
       }
       finish(p, r, cnt);
     }
-    // ---- B: hash-grid gather -> fp16 row of A (K = 32) --------------------------------------
-    if (have) {
-      float feat[kFeat];
-      encode(p.grid, smp.c, smp.lw, feat);
+    // ---- B: warp-cooperative hash-grid gather (grid.h:90-167) ------------------------------
+    // The warp's 32 samples have different numbers of active LOD levels; their (sample,
+    // level) pairs are listed level-major and dealt round-robin to the 32 lanes, so every
+    // lane gathers in every pass and neighbouring rays hit neighbouring cells of the same
+    // level in one warp-wide load.  Features land as fp16 straight in this sample's A row.
+    {
+      const int lane = tid & 31;
+      const uint4 zero = make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) st_shared16(s.A, core_off(tid, j, 4), pack8(feat + 8 * j));
+      for (int j = 0; j < 4; ++j) st_shared16(s.A, core_off(tid, j, 4), zero);
+      const int na = have ? active_levels(smp.lw, p.grid.levels) : 0;
+      uint8_t* psrc = s.pair_src[warp];
+      uint8_t* plvl = s.pair_lvl[warp];
+      const unsigned lt = (1u << lane) - 1u;
+      int npairs = 0;
+      for (int l = 0; l < p.grid.levels; ++l) {
+        const unsigned m = __ballot_sync(0xffffffffu, na > l);
+        if (na > l) {
+          const int at = npairs + __popc(m & lt);
+          psrc[at] = (uint8_t)lane;
+          plvl[at] = (uint8_t)l;
+        }
+        npairs += __popc(m);
+      }
+      __syncwarp();
+      const double u = have ? dmul(dadd(smp.c.x, 2.0), 0.25) : 0.0;
+      const double v = have ? dmul(dadd(smp.c.y, 2.0), 0.25) : 0.0;
+      const double w = have ? dmul(dadd(smp.c.z, 2.0), 0.25) : 0.0;
+      const uint8_t* Abase = s.A + (warp * 32 / 8) * (4 * 128);
+#pragma unroll 1
+      for (int base = 0; base < npairs; base += 32) {
+        const int pi = base + lane;
+        const bool ok = pi < npairs;
+        const int src = ok ? psrc[pi] : lane;
+        const int l = ok ? plvl[pi] : 0;
+        const double su = __shfl_sync(0xffffffffu, u, src);
+        const double sv = __shfl_sync(0xffffffffu, v, src);
+        const double sw = __shfl_sync(0xffffffffu, w, src);
+        LodW lw;
+        lw.full = __shfl_sync(0xffffffffu, smp.lw.full, src);
+        lw.frac = __shfl_sync(0xffffffffu, smp.lw.frac, src);
+        lw.floor_only = __shfl_sync(0xffffffffu, (int)smp.lw.floor_only, src) != 0;
+        if (ok) {
+          const float2 f = encode_level(p.grid, l, su, sv, sw, lod_weight_at(lw, l));
+          const __half2 h = __floats2half2_rn(f.x, f.y);
+          *reinterpret_cast<__half2*>(const_cast<uint8_t*>(Abase) + core_off(src, l >> 2, 4) +
+                                      (l & 3) * 4) = h;
+        }
+      }
     }
     ptx::fence_async_smem();
     if (!__syncthreads_or(have)) {
@@ -408,19 +488,52 @@ cudaError_t launch_render_tc(RenderParams p, cudaStream_t s, int num_sms) {
     cudaError_t e = cudaFuncSetAttribute(tc::k_render_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(tc::k_render_tc, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, tc::k_render_tc, tc::kThreads,
                                                       smem);
     if (e != cudaSuccess) return e;
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    // The runtime's estimate has been seen to under-report for this kernel on sm_100 (1 vs the
+    // 3 CTAs/SM ncu reports from registers/smem); take the register/smem bound directly.
+    cudaFuncAttributes fa;
+    if ((e = cudaFuncGetAttributes(&fa, tc::k_render_tc)) != cudaSuccess) return e;
+    const int regs_per_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+    const int by_regs = 65536 / (regs_per_warp * (tc::kThreads / 32));
+    const int by_smem = (228 * 1024) / (int)(smem + 1024);
+    blocks_per_sm = std::max(blocks_per_sm, std::max(1, std::min(by_regs, by_smem)));
+    if (std::getenv("LUMI_DEBUG")) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, tc::k_render_tc);
+      int b0 = -1, b1 = -1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, tc::k_render_tc, tc::kThreads, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, tc::k_render_tc, tc::kThreads, 32768);
+      std::fprintf(stderr,
+                   "[lumi] k_render_tc: %zu B smem, %d CTAs/SM x %d SMs (regs %d, static smem %zu, "
+                   "local %zu, maxdyn %d, occ@0=%d occ@32K=%d)\n",
+                   smem, blocks_per_sm, num_sms, fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes,
+                   fa.maxDynamicSharedSizeBytes, b0, b1);
+    }
   }
   p.tile_w = tc::kTileW;
   p.tile_h = tc::kTileH;
   p.tiles_x = (p.cam.width + tc::kTileW - 1) / tc::kTileW;
   const long long tiles =
       (long long)p.tiles_x * ((p.row_end - p.row_begin + tc::kTileH - 1) / tc::kTileH);
+  p.total_rays = tiles * tc::kTileW * tc::kTileH;
+  if (p.total_rays >= (1ll << 31)) return cudaErrorInvalidValue;
+  p.mask_words = (p.n + 31) / 32;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&p.kept_mask, (size_t)p.total_rays * p.mask_words * 4, s)) != cudaSuccess)
+    return e;
+  if ((e = cudaMallocAsync(&p.kept_count, (size_t)p.total_rays * 2, s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(p.work_counter, 0, sizeof(unsigned int), s)) != cudaSuccess) return e;
+  tc::k_march_mask<<<(unsigned)((p.total_rays + 127) / 128), 128, 0, s>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const long long grid = std::min<long long>((long long)blocks_per_sm * num_sms, tiles);
-  cudaError_t e = cudaMemsetAsync(p.work_counter, 0, sizeof(unsigned int), s);
-  if (e != cudaSuccess) return e;
   tc::k_render_tc<<<(unsigned)grid, tc::kThreads, smem, s>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  cudaFreeAsync(p.kept_mask, s);
+  cudaFreeAsync(p.kept_count, s);
   return cudaGetLastError();
 }
