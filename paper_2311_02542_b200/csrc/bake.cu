@@ -67,3 +67,17 @@ cudaError_t launch_bake(const lumi_dev::BakeParams& p, cudaStream_t s) {
   lumi_dev::k_bake<<<(unsigned)((total + 127) / 128), 128, 0, s>>>(p);
   return cudaGetLastError();
 }
+
+namespace lumi_dev {
+// fp32 table -> fp16 pairs (round to nearest even), grid-stride.
+__global__ void k_to_half(const float* __restrict__ src, __half* __restrict__ dst, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = __float2half_rn(src[i]);
+}
+}  // namespace lumi_dev
+
+cudaError_t launch_to_half(const float* src, void* dst, uint64_t n, cudaStream_t s) {
+  lumi_dev::k_to_half<<<148 * 8, 256, 0, s>>>(src, static_cast<__half*>(dst), n);
+  return cudaGetLastError();
+}

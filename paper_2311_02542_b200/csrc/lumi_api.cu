@@ -154,7 +154,8 @@ struct LumiModel {
   int device = 0;
   LumiFieldDesc desc{};
   LumiGridLayout layout{};
-  float* d_table = nullptr;
+  float* d_table = nullptr;   // reference fp32 layout (SIMT cross-check kernel)
+  void* d_table16 = nullptr;  // half2 copy (tensor-core renderer)
   float* d_dparams = nullptr;
   float* d_cparams = nullptr;
   uint8_t* d_occ = nullptr;
@@ -221,6 +222,7 @@ int make_params(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions
   p->cam.t_far = cam->t_far;
   auto& g = p->grid;
   g.table = reinterpret_cast<const float2*>(m->d_table);
+  g.table16 = reinterpret_cast<const __half2*>(m->d_table16);
   g.levels = m->layout.levels;
   for (int l = 0; l < g.levels; ++l) {
     g.res[l] = m->layout.resolution[l];
@@ -364,7 +366,10 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
       (e = cudaMemcpy(m->d_cparams, cparams, lay.color_params * sizeof(float),
                       cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemset(m->d_counter, 0, kCounterSlots * 32 * sizeof(unsigned int))) != cudaSuccess ||
-      (e = cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess)
+      (e = cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess ||
+      (e = cudaMalloc(&m->d_table16, lay.total_floats * 2)) != cudaSuccess ||
+      (e = launch_to_half(m->d_table, m->d_table16, lay.total_floats, nullptr)) != cudaSuccess ||
+      (e = cudaDeviceSynchronize()) != cudaSuccess)
     return cleanup(fail(LUMI_ERR_CUDA, std::string("model upload: ") + cudaGetErrorString(e)));
   if ((rc = lumi_model_set_occupancy(m, occ, occ_res))) return cleanup(rc);
   *out = m;
@@ -391,6 +396,7 @@ int lumi_model_destroy(LumiModel* m) {
   if (!m) return LUMI_OK;
   DeviceGuard dg(m->device);
   cudaFree(m->d_table);
+  cudaFree(m->d_table16);
   cudaFree(m->d_dparams);
   cudaFree(m->d_cparams);
   cudaFree(m->d_occ);

@@ -91,6 +91,24 @@ __device__ __forceinline__ void issue_layer(const Smem& s, const uint8_t* B, uin
   }
 }
 
+// Hidden-layer epilogue: TMEM row (64 fp32 accumulators of this thread's sample) + bias,
+// ReLU, fp16 -> this thread's row of the next layer's A tile (K = 64).  Two halves of 32
+// columns keep the live register count down.
+__device__ __forceinline__ void relu64_to_A(uint32_t t_lane, const float* bias, uint8_t* A,
+                                            int row) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float v[32];
+    ptx::tmem_ld16(t_lane + 32 * h, v);
+    ptx::tmem_ld16(t_lane + 32 * h + 16, v + 16);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + bias[32 * h + j], 0.f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) st_shared16(A, core_off(row, 4 * h + j, 8), pack8(v + 8 * j));
+  }
+}
+
 struct Ray {
   int id, x, y;
   d3 d, nd;
@@ -107,7 +125,7 @@ struct Sample {
 };
 
 struct Counters {
-  unsigned long long evals, level_samples, marched, rays;
+  unsigned evals, level_samples, marched, rays;
 };
 
 __device__ __forceinline__ bool occupied(const RenderParams& p, d3 c) {
@@ -224,7 +242,7 @@ __device__ void refill(const RenderParams& p, Smem& s, int total) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 3) k_render_tc(RenderParams p) {
+__global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -310,24 +328,37 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_tc(RenderParams p) {
       const double w = have ? dmul(dadd(smp.c.z, 2.0), 0.25) : 0.0;
       const uint8_t* Abase = s.A + (warp * 32 / 8) * (4 * 128);
 #pragma unroll 1
-      for (int base = 0; base < npairs; base += 32) {
-        const int pi = base + lane;
-        const bool ok = pi < npairs;
-        const int src = ok ? psrc[pi] : lane;
-        const int l = ok ? plvl[pi] : 0;
-        const double su = __shfl_sync(0xffffffffu, u, src);
-        const double sv = __shfl_sync(0xffffffffu, v, src);
-        const double sw = __shfl_sync(0xffffffffu, w, src);
-        LodW lw;
-        lw.full = __shfl_sync(0xffffffffu, smp.lw.full, src);
-        lw.frac = __shfl_sync(0xffffffffu, smp.lw.frac, src);
-        lw.floor_only = __shfl_sync(0xffffffffu, (int)smp.lw.floor_only, src) != 0;
-        if (ok) {
-          const float2 f = encode_level(p.grid, l, su, sv, sw, lod_weight_at(lw, l));
-          const __half2 h = __floats2half2_rn(f.x, f.y);
-          *reinterpret_cast<__half2*>(const_cast<uint8_t*>(Abase) + core_off(src, l >> 2, 4) +
-                                      (l & 3) * 4) = h;
+      // two (sample, level) pairs per lane per pass: 16 independent gathers in flight
+      for (int base = 0; base < npairs; base += 64) {
+        int src[2], lv[2];
+        bool ok[2];
+        double su[2], sv[2], sw[2];
+        float wl[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int pi = base + 32 * q + lane;
+          ok[q] = pi < npairs;
+          src[q] = ok[q] ? psrc[pi] : lane;
+          lv[q] = ok[q] ? plvl[pi] : 0;
+          su[q] = __shfl_sync(0xffffffffu, u, src[q]);
+          sv[q] = __shfl_sync(0xffffffffu, v, src[q]);
+          sw[q] = __shfl_sync(0xffffffffu, w, src[q]);
+          LodW lw;
+          lw.full = __shfl_sync(0xffffffffu, smp.lw.full, src[q]);
+          lw.frac = __shfl_sync(0xffffffffu, smp.lw.frac, src[q]);
+          lw.floor_only = __shfl_sync(0xffffffffu, (int)smp.lw.floor_only, src[q]) != 0;
+          wl[q] = lod_weight_at(lw, lv[q]);
         }
+        float2 f[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          f[q] = ok[q] ? encode_level_h(p.grid, p.grid.table16, lv[q], su[q], sv[q], sw[q], wl[q])
+                       : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          if (ok[q])
+            *reinterpret_cast<__half2*>(const_cast<uint8_t*>(Abase) + core_off(src[q], lv[q] >> 2, 4) +
+                                        (lv[q] & 3) * 4) = __floats2half2_rn(f[q].x, f[q].y);
       }
     }
     ptx::fence_async_smem();
@@ -338,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_tc(RenderParams p) {
       continue;
     }
 
-    float v[64];
+    float v[32];
     // ---- density L1: [128x32] x [32x64] -> relu -------------------------------------------
     if (issuer) {
       ptx::tc_fence_after();
@@ -348,13 +379,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_tc(RenderParams p) {
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) ptx::tmem_ld16(t_lane + 16 * q, v + 16 * q);
-    ptx::tmem_ld_wait();
-#pragma unroll
-    for (int j = 0; j < 64; ++j) v[j] = fmaxf(v[j] + s.b1[j], 0.f);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) st_shared16(s.A, core_off(tid, j, 8), pack8(v + 8 * j));
+    relu64_to_A(t_lane, s.b1, s.A, tid);
     ptx::fence_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
@@ -393,13 +418,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_tc(RenderParams p) {
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) ptx::tmem_ld16(t_lane + 16 * q, v + 16 * q);
-    ptx::tmem_ld_wait();
-#pragma unroll
-    for (int j = 0; j < 64; ++j) v[j] = fmaxf(v[j] + s.cb1[j], 0.f);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) st_shared16(s.A, core_off(tid, j, 8), pack8(v + 8 * j));
+    relu64_to_A(t_lane, s.cb1, s.A, tid);
     ptx::fence_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
@@ -413,13 +432,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_tc(RenderParams p) {
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) ptx::tmem_ld16(t_lane + 16 * q, v + 16 * q);
-    ptx::tmem_ld_wait();
-#pragma unroll
-    for (int j = 0; j < 64; ++j) v[j] = fmaxf(v[j] + s.cb2[j], 0.f);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) st_shared16(s.A, core_off(tid, j, 8), pack8(v + 8 * j));
+    relu64_to_A(t_lane, s.cb2, s.A, tid);
     ptx::fence_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
