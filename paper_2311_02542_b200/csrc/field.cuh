@@ -116,19 +116,23 @@ __device__ __forceinline__ float2 encode_level_h(const GridDev& g, const __half2
   __half2 e[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) e[k] = __ldg(base + idx[k]);
-  const double fu = dsub(pu, (double)iu), fv = dsub(pv, (double)iv), fs = dsub(ps, (double)is);
-  const double gu = dsub(1.0, fu), gv = dsub(1.0, fv), gs = dsub(1.0, fs);
-  const double w00 = dmul(gu, gv), w10 = dmul(fu, gv), w01 = dmul(gu, fv), w11 = dmul(fu, fv);
-  const double wuv[4] = {w00, w10, w01, w11};
+  // Fractions exact in double, trilinear weights and accumulation in fp32 FMA: within a few
+  // fp32 ulp of the reference's double-product-then-round features, far below the fp16
+  // operand rounding that follows.
+  const float fu = __double2float_rn(dsub(pu, (double)iu)),
+              fv = __double2float_rn(dsub(pv, (double)iv)),
+              fs = __double2float_rn(dsub(ps, (double)is));
+  const float gu = 1.f - fu, gv = 1.f - fv, gs = 1.f - fs;
+  const float wuv[4] = {gu * gv, fu * gv, gu * fv, fu * fv};
   float a0 = 0.f, a1 = 0.f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const float tri = __double2float_rn(dmul(wuv[k & 3], (k >> 2) ? fs : gs));
+    const float tri = wuv[k & 3] * ((k >> 2) ? fs : gs);
     const float2 ef = __half22float2(e[k]);
-    a0 = __fadd_rn(a0, __fmul_rn(tri, ef.x));
-    a1 = __fadd_rn(a1, __fmul_rn(tri, ef.y));
+    a0 = fmaf(tri, ef.x, a0);
+    a1 = fmaf(tri, ef.y, a1);
   }
-  return make_float2(__fmul_rn(a0, wl), __fmul_rn(a1, wl));
+  return make_float2(a0 * wl, a1 * wl);
 }
 
 // Full encode of one contracted point into 2*levels features (zero for masked levels,

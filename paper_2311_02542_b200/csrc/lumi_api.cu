@@ -181,6 +181,16 @@ struct DeviceGuard {
   }
 };
 
+// The per-launch march masks come from the stream-ordered allocator; keep freed blocks in
+// the device's default pool instead of returning them at every synchronisation.
+cudaError_t keep_pool_memory(int device) {
+  cudaMemPool_t pool;
+  cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = UINT64_MAX;
+  return cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+}
+
 // Exponential sample distances and step ratio (renderer.h:135-142) on the host.
 int get_ts(LumiModel* m, double tn, double tf, int n, const double** d_ts, double* ratio) {
   std::lock_guard<std::mutex> lk(m->mu);
@@ -367,6 +377,7 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
                       cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemset(m->d_counter, 0, kCounterSlots * 32 * sizeof(unsigned int))) != cudaSuccess ||
       (e = cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess ||
+      (e = keep_pool_memory(device)) != cudaSuccess ||
       (e = cudaMalloc(&m->d_table16, lay.total_floats * 2)) != cudaSuccess ||
       (e = launch_to_half(m->d_table, m->d_table16, lay.total_floats, nullptr)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess)
