@@ -96,6 +96,60 @@ __device__ __forceinline__ double contracted_footprint(d3 o, d3 d, d3 nd, double
   return dmul(0.5, dnorm(d3{dsub(a.x, b.x), dsub(a.y, b.y), dsub(a.z, b.z)}));
 }
 
+// ---- fast variants for the tensor-core renderer ----------------------------------------
+// Contraction with one reciprocal instead of four divisions (within 1 ulp of contract()).
+__device__ __forceinline__ d3 contract_fast(d3 x, int mode) {
+  if (mode == 0) return x;
+  const double m = dlinf(x);
+  if (!(m <= 1.0)) {
+    const double inv = 1.0 / m;
+    d3 out{x.x * inv, x.y * inv, x.z * inv};
+    const double mapped = 2.0 - inv;
+    if (fabs(x.x) == m)
+      out.x = copysign(mapped, x.x);
+    else if (fabs(x.y) == m)
+      out.y = copysign(mapped, x.y);
+    else
+      out.z = copysign(mapped, x.z);
+    return out;
+  }
+  return x;
+}
+
+__device__ __forceinline__ float3 contract_f(float3 x, int mode) {
+  if (mode == 0) return x;
+  const float m = fmaxf(fabsf(x.x), fmaxf(fabsf(x.y), fabsf(x.z)));
+  if (!(m <= 1.f)) {
+    const float inv = __frcp_rn(m);
+    float3 out = make_float3(x.x * inv, x.y * inv, x.z * inv);
+    const float mapped = 2.f - inv;
+    if (fabsf(x.x) == m)
+      out.x = copysignf(mapped, x.x);
+    else if (fabsf(x.y) == m)
+      out.y = copysignf(mapped, x.y);
+    else
+      out.z = copysignf(mapped, x.z);
+    return out;
+  }
+  return x;
+}
+
+// Effective LOD level L* + bias (grid.cpp:8-13, camera.cpp:68-73) from an fp32 footprint:
+// the weights are continuous in L*, and the ~1e-4 relative error of the fp32 footprint
+// moves them by less than the fp16 rounding of the features they scale.
+__device__ __forceinline__ float lod_eff_fast(d3 o, d3 d, d3 nd, double t, int mode,
+                                              float two_base, float inv_log_scale, int levels,
+                                              float bias) {
+  const float3 a = contract_f(make_float3((float)(o.x + d.x * t), (float)(o.y + d.y * t),
+                                          (float)(o.z + d.z * t)), mode);
+  const float3 b = contract_f(make_float3((float)(o.x + nd.x * t), (float)(o.y + nd.y * t),
+                                          (float)(o.z + nd.z * t)), mode);
+  const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+  const float rc = fmaxf(0.5f * sqrtf(dx * dx + dy * dy + dz * dz), 1e-12f);
+  const float l = fminf(-__logf(two_base * rc) * inv_log_scale, (float)(levels - 1));
+  return l + bias;
+}
+
 // lod_level (grid.cpp:8-13); log_scale = std::log(per_level_scale) precomputed on the host
 // with the same libm the reference uses.
 __device__ __forceinline__ double lod_level(double r, double two_base, double log_scale,
@@ -136,6 +190,26 @@ __device__ __forceinline__ LodW lod_weights(double l_star, double bias, int leve
 __device__ __forceinline__ int active_levels(const LodW& w, int levels) {
   if (w.floor_only) return 1;
   return min(levels, w.full + (w.frac > 0.f ? 1 : 0));
+}
+
+// lod_weights (grid.cpp:15-37) on an fp32 effective level.
+__device__ __forceinline__ LodW lod_weights_f(float eff, int levels) {
+  LodW w;
+  if (eff >= (float)(levels - 1)) {
+    w.full = levels;
+    w.frac = 0.f;
+    w.floor_only = false;
+  } else if (eff < 0.f) {
+    w.full = 0;
+    w.frac = 0.f;
+    w.floor_only = true;
+  } else {
+    const float fl = floorf(eff);
+    w.full = (int)fl + 1;
+    w.frac = eff - fl;
+    w.floor_only = false;
+  }
+  return w;
 }
 
 __device__ __forceinline__ float lod_weight_at(const LodW& w, int l) {

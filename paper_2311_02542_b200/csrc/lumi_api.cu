@@ -254,6 +254,7 @@ int make_params(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions
   p->t_cut = o->termination_transmittance;
   for (int c = 0; c < 3; ++c) p->bg[c] = o->background[c];
   p->contraction = o->contraction;
+  if (const char* dbg = std::getenv("LUMI_DEBUG_SKIP")) p->debug_flags = std::atoi(dbg);
   p->chunk = o->chunk_size;
   p->row_begin = b;
   p->row_end = e;

@@ -23,6 +23,7 @@ struct RenderParams {
   double t_cut;
   double bg[3];
   int contraction;
+  int debug_flags;  // profiling ablations only (LUMI_DEBUG_SKIP): 1 = no gather, 2 = no MLP
   int chunk;
   int row_begin, row_end;
   // target (LumiFrameTarget)

@@ -179,14 +179,14 @@ __device__ __forceinline__ bool advance(const RenderParams& p, const double* ts,
   r.word &= r.word - 1;
   const d3 o{p.cam.origin[0], p.cam.origin[1], p.cam.origin[2]};
   const double t = ts[i];
-  smp.c = contract(ray_at(o, r.d, t), p.contraction);
+  smp.c = contract_fast(ray_at(o, r.d, t), p.contraction);
   smp.t = t;
   smp.delta = (i + 1 < p.n) ? dsub(ts[i + 1], t) : dmul(t, dsub(p.ratio, 1.0));
   if (p.lod_enabled) {
-    const double rc = contracted_footprint(o, r.d, r.nd, t, p.contraction);
-    smp.lw = lod_weights(lod_level(dmax(rc, 1e-12), p.grid.two_base, p.grid.log_scale,
-                                   p.grid.levels),
-                         p.lod_bias, p.grid.levels);
+    smp.lw = lod_weights_f(lod_eff_fast(o, r.d, r.nd, t, p.contraction, (float)p.grid.two_base,
+                                        (float)(1.0 / p.grid.log_scale), p.grid.levels,
+                                        (float)p.lod_bias),
+                           p.grid.levels);
   } else {
     smp.lw = LodW{p.grid.levels, 0.f, false};
   }
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
         float2 f[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q)
-          f[q] = ok[q] ? encode_level_h(p.grid, p.grid.table16, lv[q], su[q], sv[q], sw[q], wl[q])
+          f[q] = ok[q] && !(p.debug_flags & 1) ? encode_level_h(p.grid, p.grid.table16, lv[q], su[q], sv[q], sw[q], wl[q])
                        : make_float2(0.f, 0.f);
 #pragma unroll
         for (int q = 0; q < 2; ++q)
@@ -370,6 +370,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     }
 
     float v[32];
+    float sigma = 1.f;
+    if (!(p.debug_flags & 2)) {
     // ---- density L1: [128x32] x [32x64] -> relu -------------------------------------------
     if (issuer) {
       ptx::tc_fence_after();
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     ptx::tmem_ld16(t_lane, v);
     ptx::tmem_ld16(t_lane + 16, v + 16);
     ptx::tmem_ld_wait();
-    const float sigma = trunc_exp(v[0] + s.b2[0]);
+    sigma = trunc_exp(v[0] + s.b2[0]);
     {
       float cin[32];
 #pragma unroll
@@ -449,6 +451,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     ptx::tmem_ld16(t_lane, v);
     ptx::tmem_ld_wait();
     ptx::tc_fence_before();
+    } else {
+      v[0] = v[1] = v[2] = 0.f;
+    }
 
     // ---- C: front-to-back compositing (renderer.h:170-190), double ----------------------
     if (have) {
