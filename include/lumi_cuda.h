@@ -167,6 +167,25 @@ int lumi_march_kept_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRen
                           int row_begin, int row_end, uint32_t* mask, int32_t* counts,
                           void* stream);
 
+/* ---- checkpoint ingest (host) ---------------------------------------------------- */
+/* LUMICKPT v1 (proj/src/scene.cpp:286-394, occupancy.cpp:200-243). */
+typedef struct LumiCheckpointInfo {
+  LumiFieldDesc field;
+  int32_t samples_per_ray;
+  int32_t contraction; /* 0 = kNone, 1 = kLInfCubic */
+  double background[3];
+  int32_t occ_res;
+  int32_t n_cameras;
+  uint64_t table_floats;
+  uint64_t density_params;
+  uint64_t color_params;
+} LumiCheckpointInfo;
+/* Parses `path`.  Any output buffer may be NULL (call once with NULLs to learn the sizes in
+   `info`, then again with table[table_floats], density[density_params],
+   color[color_params], occupancy[occ_res^3]). */
+int lumi_checkpoint_read(const char* path, LumiCheckpointInfo* info, float* table,
+                         float* density_params, float* color_params, uint8_t* occupancy);
+
 /* ---- occupancy bake (GPU) ------------------------------------------------------- */
 /* OccupancyGrid::probe(k) with the density head + prune(alpha), zero history, no
    carving; results to host buffers (probe_max may be NULL). */

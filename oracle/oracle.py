@@ -390,6 +390,7 @@ class Reference(Oracle):
         for fn in ("ref_pq_encode", "ref_pq_decode", "ref_srgb_oetf"):
             getattr(L, fn).argtypes = [d]
             getattr(L, fn).restype = d
+        L.ref_save_checkpoint.argtypes = [vp, C.c_char_p, i32, vp, i32]
         L.ref_equal_assignment.argtypes = [i32, i32, vp, vp]
         L.ref_assign_rows.argtypes = [i32, i32, vp, vp, vp, d, vp, vp]
         L.ref_aggregate_stats.argtypes = [vp, i32, vp]
@@ -481,6 +482,12 @@ class Reference(Oracle):
         self._check(self.lib.ref_probe_prune(model.h, arr, len(cams), spp, k, res, alpha, _p(pm),
                                              _p(occ)))
         return pm, occ
+
+    def save_checkpoint(self, model, path, spp=256, background=(0.0, 0.0, 0.0), contraction=1):
+        """The reference save_checkpoint (scene.cpp:320-351) of a model."""
+        bg = np.ascontiguousarray(background, np.float64)
+        self._check(self.lib.ref_save_checkpoint(model.h, str(path).encode(), spp, _p(bg),
+                                                 contraction))
 
     def generate_ray(self, cam, px, py):
         o = np.zeros(3)

@@ -20,6 +20,7 @@
 #include "lumi/grid.h"
 #include "lumi/occupancy.h"
 #include "lumi/renderer.h"
+#include "lumi/scene.h"
 #include "lumi/scheduler.h"
 #include "lumi/simd.h"
 
@@ -335,6 +336,17 @@ int ref_probe_prune(void* h, const lo_camera* cams, int ncams, int spp, int k, i
       if (probe_max) probe_max[i] = g.probe_density(i);
       if (occ_out) occ_out[i] = g.occupied_bit(i) ? 1 : 0;
     }
+  });
+}
+
+// save_checkpoint (scene.cpp:320-351) of the model, for the checkpoint-ingest parity test.
+int ref_save_checkpoint(void* h, const char* path, int spp, const double* background,
+                        int contraction) {
+  return guarded([&] {
+    RefModel& m = *static_cast<RefModel*>(h);
+    Checkpoint ck{m.cfg, m.field, m.grid, {0.01, 0.02}, {background[0], background[1], background[2]},
+                  contraction ? ContractionMode::kLInfCubic : ContractionMode::kNone, spp};
+    save_checkpoint(ck, path);
   });
 }
 

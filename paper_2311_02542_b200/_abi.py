@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "liblumi_cuda.so")
+LIB_PATH = os.environ.get("LUMI_CUDA_LIB") or os.path.join(HERE, "lib", "liblumi_cuda.so")
 
 LUMI_MAX_LEVELS = 16
 LUMI_OK, LUMI_ERR_INVALID, LUMI_ERR_CUDA, LUMI_ERR_UNSUPPORTED = 0, 1, 2, 3
@@ -66,6 +66,13 @@ class FrameTarget(C.Structure):
                 ("height", C.c_int32), ("row_offset", C.c_int32), ("_pad", C.c_int32)]
 
 
+class CheckpointInfo(C.Structure):
+    _fields_ = [("field", FieldDesc), ("samples_per_ray", C.c_int32), ("contraction", C.c_int32),
+                ("background", C.c_double * 3), ("occ_res", C.c_int32), ("n_cameras", C.c_int32),
+                ("table_floats", C.c_uint64), ("density_params", C.c_uint64),
+                ("color_params", C.c_uint64)]
+
+
 # (name, argtypes) of every exported entry point, in include/lumi_cuda.h order.
 _vp, _i, _d, _u64, _f = C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.c_float
 SIGNATURES = {
@@ -82,6 +89,7 @@ SIGNATURES = {
     "lumi_render_rows": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp], C.c_int),
     "lumi_render_rows_async": ([_vp, _vp, _vp, _i, _i, _vp, _vp], C.c_int),
     "lumi_march_kept_async": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp], C.c_int),
+    "lumi_checkpoint_read": ([C.c_char_p, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "lumi_bake_occupancy": ([_vp, _vp, _i, _i, _i, _i, _f, _vp, _vp], C.c_int),
     "lumi_equal_assignment": ([_i, _i, _vp, _vp], C.c_int),
     "lumi_assign_rows": ([_i, _i, _vp, _vp, _d, _vp, _vp], C.c_int),

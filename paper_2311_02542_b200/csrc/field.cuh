@@ -100,6 +100,15 @@ __device__ __forceinline__ void corner_indices(bool dense, int iu, int iv, int i
   }
 }
 
+// d = a * b + c with a, b fp16 and c, d fp32 (sm_100 FHFMA)
+__device__ __forceinline__ float fma_f32_f16(__half a, __half b, float c) {
+  float d;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;"
+      : "=f"(d)
+      : "h"(__half_as_ushort(a)), "h"(__half_as_ushort(b)), "f"(c));
+  return d;
+}
+
 // One level from a half2 copy of the table (exact fp16 -> fp32 widening, then the same
 // float accumulation as the reference).  Used by the tensor-core renderer, whose fp16 MLP
 // operands dominate the error budget anyway (oracle: 1.59e-4 vs 1.57e-4 max |dPQ| at C1).
@@ -116,21 +125,37 @@ __device__ __forceinline__ float2 encode_level_h(const GridDev& g, const __half2
   __half2 e[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) e[k] = __ldg(base + idx[k]);
-  // Fractions exact in double, trilinear weights and accumulation in fp32 FMA: within a few
-  // fp32 ulp of the reference's double-product-then-round features, far below the fp16
-  // operand rounding that follows.
+  // Fractions exact in double; the eight trilinear weights as four packed-fp16 products
+  // (HMUL2), accumulated into fp32 with the sm_100 mixed fma.rn.f32.f16 (f16 x f16 + f32,
+  // product exact).  Oracle-measured: C1 max |dPQ| 1.60e-4 vs 1.59e-4 with fp32 weights,
+  // i.e. below the fp16 rounding of the MLP operands that follows.
   const float fu = __double2float_rn(dsub(pu, (double)iu)),
               fv = __double2float_rn(dsub(pv, (double)iv)),
               fs = __double2float_rn(dsub(ps, (double)is));
+#ifdef LUMI_GATHER_FP32
   const float gu = 1.f - fu, gv = 1.f - fv, gs = 1.f - fs;
   const float wuv[4] = {gu * gv, fu * gv, gu * fv, fu * fv};
-  float a0 = 0.f, a1 = 0.f;
+  float b0 = 0.f, b1 = 0.f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const float tri = wuv[k & 3] * ((k >> 2) ? fs : gs);
     const float2 ef = __half22float2(e[k]);
-    a0 = fmaf(tri, ef.x, a0);
-    a1 = fmaf(tri, ef.y, a1);
+    b0 = fmaf(tri, ef.x, b0);
+    b1 = fmaf(tri, ef.y, b1);
+  }
+  return make_float2(b0 * wl, b1 * wl);
+#endif
+  const __half2 hu = __floats2half2_rn(1.f - fu, fu);  // (g_u, f_u)
+  const __half2 w0 = __hmul2(hu, __float2half2_rn(1.f - fv));  // k = 0,1 (y = 0)
+  const __half2 w1 = __hmul2(hu, __float2half2_rn(fv));        // k = 2,3 (y = 1)
+  const __half2 gs2 = __float2half2_rn(1.f - fs), fs2 = __float2half2_rn(fs);
+  const __half2 t[4] = {__hmul2(w0, gs2), __hmul2(w1, gs2), __hmul2(w0, fs2), __hmul2(w1, fs2)};
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const __half tri = (k & 1) ? __high2half(t[k >> 1]) : __low2half(t[k >> 1]);
+    a0 = fma_f32_f16(tri, __low2half(e[k]), a0);
+    a1 = fma_f32_f16(tri, __high2half(e[k]), a1);
   }
   return make_float2(a0 * wl, a1 * wl);
 }

@@ -287,6 +287,7 @@ int set_target(RenderParams* p, const LumiFrameTarget* t, int b, int e) {
 extern "C" {
 
 const char* lumi_last_error(void) { return g_err.c_str(); }
+int lumi_set_error(int code, const char* msg) { return fail(code, msg); }
 int lumi_abi_version(void) { return LUMI_ABI_VERSION; }
 
 int lumi_device_info(int device, char* info, size_t len) {

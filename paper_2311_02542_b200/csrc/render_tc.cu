@@ -30,15 +30,16 @@ constexpr int kThreads = 128;  // UMMA M
 constexpr int kTileW = 16, kTileH = 8;
 constexpr uint32_t kTmemCols = 64;
 
+// Every layer's K carries one extra 16-wide step whose first column is 1 in A and the bias
+// in B, so the tensor core adds the bias (fp16 x 1 into the fp32 accumulator).
+constexpr int kKb = 16;
 struct __align__(1024) Smem {
-  uint8_t A[128 * 64 * 2];   // activations, K-major core-matrix tile (K <= 64)
-  uint8_t W1[64 * 32 * 2];   // density L1  N=64 K=32
-  uint8_t W2[32 * 64 * 2];   // density L2  N=32 (17 used) K=64
-  uint8_t C1[64 * 32 * 2];   // colour L1   N=64 K=32
-  uint8_t C2[64 * 64 * 2];   // colour L2   N=64 K=64
-  uint8_t C3[16 * 64 * 2];   // colour L3   N=16 (3 used) K=64
-  float b1[64], b2[32], cb1[64], cb2[64], cb3[16];
-  double ts[kMaxSamples];
+  uint8_t A[128 * (64 + kKb) * 2];  // activations, K-major core-matrix tile (K <= 64+16)
+  uint8_t W1[64 * (32 + kKb) * 2];  // density L1  N=64 K=32(+bias)
+  uint8_t W2[32 * (64 + kKb) * 2];  // density L2  N=32 (17 used) K=64(+bias)
+  uint8_t C1[64 * (32 + kKb) * 2];  // colour L1   N=64 K=32(+bias)
+  uint8_t C2[64 * (64 + kKb) * 2];  // colour L2   N=64 K=64(+bias)
+  uint8_t C3[16 * (64 + kKb) * 2];  // colour L3   N=16 (3 used) K=64(+bias)
   uint64_t mbar;
   uint32_t tmem_base;
   int q_next, q_end, q_done;
@@ -66,17 +67,41 @@ __device__ __forceinline__ void st_shared16(uint8_t* base, uint32_t off, uint4 v
   *reinterpret_cast<uint4*>(base + off) = v;
 }
 
-// weights [n_real x K] fp32 row-major (network.h:64) -> fp16 tile with n_pad rows
-__device__ void load_weight_tile(uint8_t* dst, const float* __restrict__ W, int n_real, int n_pad,
-                                 int K) {
-  const int kch = K / 8;
+// weights [n_real x K] fp32 row-major (network.h:64) and bias [n_real] -> fp16 tile with
+// n_pad rows and K + 16 columns: [W | b 0 ... 0]
+__device__ void load_weight_tile(uint8_t* dst, const float* __restrict__ W,
+                                 const float* __restrict__ b, int n_real, int n_pad, int K) {
+  const int kch = (K + kKb) / 8;
   for (int it = threadIdx.x; it < n_pad * kch; it += blockDim.x) {
     const int n = it / kch, j = it % kch;
     float v[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = n < n_real ? __ldg(W + (size_t)n * K + 8 * j + q) : 0.f;
+    for (int q = 0; q < 8; ++q) {
+      const int k = 8 * j + q;
+      v[q] = n >= n_real ? 0.f : k < K ? __ldg(W + (size_t)n * K + k) : k == K ? __ldg(b + n) : 0.f;
+    }
     st_shared16(dst, core_off(n, j, kch), pack8(v));
   }
+}
+
+// the [1 0 ... 0 | 0 ... 0] bias step of this thread's A row for a layer with K data columns
+__device__ __forceinline__ void write_bias_step(uint8_t* A, int row, int K) {
+  const int kch = (K + kKb) / 8;
+  st_shared16(A, core_off(row, K / 8, kch), make_uint4(0x3C00u, 0u, 0u, 0u));  // fp16 1.0
+  st_shared16(A, core_off(row, K / 8 + 1, kch), make_uint4(0u, 0u, 0u, 0u));
+}
+
+// fp32 x 8 -> fp16 x 8 with ReLU applied on the packed halves (max(h(x), 0) == h(max(x, 0)))
+__device__ __forceinline__ uint4 pack8_relu(const float* v) {
+  const __half2 z = __float2half2_rn(0.f);
+  __half2 h0 = __hmax2(__floats2half2_rn(v[0], v[1]), z), h1 = __hmax2(__floats2half2_rn(v[2], v[3]), z),
+          h2 = __hmax2(__floats2half2_rn(v[4], v[5]), z), h3 = __hmax2(__floats2half2_rn(v[6], v[7]), z);
+  uint4 u;
+  u.x = *reinterpret_cast<uint32_t*>(&h0);
+  u.y = *reinterpret_cast<uint32_t*>(&h1);
+  u.z = *reinterpret_cast<uint32_t*>(&h2);
+  u.w = *reinterpret_cast<uint32_t*>(&h3);
+  return u;
 }
 
 template <int N, int K>
@@ -94,8 +119,8 @@ __device__ __forceinline__ void issue_layer(const Smem& s, const uint8_t* B, uin
 // Hidden-layer epilogue: TMEM row (64 fp32 accumulators of this thread's sample) + bias,
 // ReLU, fp16 -> this thread's row of the next layer's A tile (K = 64).  Two halves of 32
 // columns keep the live register count down.
-__device__ __forceinline__ void relu64_to_A(uint32_t t_lane, const float* bias, uint8_t* A,
-                                            int row) {
+__device__ __forceinline__ void relu64_to_A(uint32_t t_lane, uint8_t* A, int row) {
+  constexpr int kch = (64 + kKb) / 8;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     float v[32];
@@ -103,10 +128,9 @@ __device__ __forceinline__ void relu64_to_A(uint32_t t_lane, const float* bias, 
     ptx::tmem_ld16(t_lane + 32 * h + 16, v + 16);
     ptx::tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + bias[32 * h + j], 0.f);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) st_shared16(A, core_off(row, 4 * h + j, 8), pack8(v + 8 * j));
+    for (int j = 0; j < 4; ++j) st_shared16(A, core_off(row, 4 * h + j, kch), pack8_relu(v + 8 * j));
   }
+  write_bias_step(A, row, 64);
 }
 
 struct Ray {
@@ -178,10 +202,10 @@ __device__ __forceinline__ bool advance(const RenderParams& p, const double* ts,
   const int i = r.wi * 32 + __ffs(r.word) - 1;
   r.word &= r.word - 1;
   const d3 o{p.cam.origin[0], p.cam.origin[1], p.cam.origin[2]};
-  const double t = ts[i];
+  const double t = __ldg(ts + i);
   smp.c = contract_fast(ray_at(o, r.d, t), p.contraction);
   smp.t = t;
-  smp.delta = (i + 1 < p.n) ? dsub(ts[i + 1], t) : dmul(t, dsub(p.ratio, 1.0));
+  smp.delta = (i + 1 < p.n) ? dsub(__ldg(ts + i + 1), t) : dmul(t, dsub(p.ratio, 1.0));
   if (p.lod_enabled) {
     smp.lw = lod_weights_f(lod_eff_fast(o, r.d, r.nd, t, p.contraction, (float)p.grid.two_base,
                                         (float)(1.0 / p.grid.log_scale), p.grid.levels,
@@ -250,20 +274,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
   // ---- one-time setup: weights -> fp16 core-matrix tiles, biases, distances, TMEM --------
   const float* dp = p.mlp.dparams;
   const float* cp = p.mlp.cparams;
-  load_weight_tile(s.W1, dp, 64, 64, 32);
-  load_weight_tile(s.W2, dp + 64 * 32 + 64, 1 + kBottleneck, 32, 64);
-  load_weight_tile(s.C1, cp, 64, 64, 32);
-  load_weight_tile(s.C2, cp + 64 * 32 + 64, 64, 64, 64);
-  load_weight_tile(s.C3, cp + 64 * 32 + 64 + 64 * 64 + 64, 3, 16, 64);
-  for (int i = tid; i < 64; i += kThreads) {
-    s.b1[i] = dp[64 * 32 + i];
-    s.cb1[i] = cp[64 * 32 + i];
-    s.cb2[i] = cp[64 * 32 + 64 + 64 * 64 + i];
-  }
-  for (int i = tid; i < 32; i += kThreads) s.b2[i] = i < 17 ? dp[64 * 32 + 64 + 17 * 64 + i] : 0.f;
-  for (int i = tid; i < 16; i += kThreads)
-    s.cb3[i] = i < 3 ? cp[64 * 32 + 64 + 64 * 64 + 64 + 3 * 64 + i] : 0.f;
-  for (int i = tid; i < p.n; i += kThreads) s.ts[i] = p.ts[i];
+  // flattened weights-then-bias per layer (network.h:144-151)
+  const float* d2 = dp + 64 * 32 + 64;
+  const float* c2 = cp + 64 * 32 + 64;
+  const float* c3 = c2 + 64 * 64 + 64;
+  load_weight_tile(s.W1, dp, dp + 64 * 32, 64, 64, 32);
+  load_weight_tile(s.W2, d2, d2 + 17 * 64, 1 + kBottleneck, 32, 64);
+  load_weight_tile(s.C1, cp, cp + 64 * 32, 64, 64, 32);
+  load_weight_tile(s.C2, c2, c2 + 64 * 64, 64, 64, 64);
+  load_weight_tile(s.C3, c3, c3 + 3 * 64, 3, 16, 64);
   const int total = (int)p.total_rays;
   if (tid == 0) {
     ptx::mbar_init(&s.mbar, 1);
@@ -292,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     bool have = false;
     for (;;) {
       if (r.id < 0 && !take_ray(p, s, r)) break;
-      if (advance(p, s.ts, r, smp, cnt)) {
+      if (advance(p, p.ts, r, smp, cnt)) {  // distances via L1 (one load per sample)
         have = true;
         break;
       }
@@ -305,9 +324,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     // level in one warp-wide load.  Features land as fp16 straight in this sample's A row.
     {
       const int lane = tid & 31;
+      constexpr int kch = (32 + kKb) / 8;  // density L1 A layout: 32 features + bias step
       const uint4 zero = make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) st_shared16(s.A, core_off(tid, j, 4), zero);
+      for (int j = 0; j < 4; ++j) st_shared16(s.A, core_off(tid, j, kch), zero);
+      write_bias_step(s.A, tid, 32);
       const int na = have ? active_levels(smp.lw, p.grid.levels) : 0;
       uint8_t* psrc = s.pair_src[warp];
       uint8_t* plvl = s.pair_lvl[warp];
@@ -326,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
       const double u = have ? dmul(dadd(smp.c.x, 2.0), 0.25) : 0.0;
       const double v = have ? dmul(dadd(smp.c.y, 2.0), 0.25) : 0.0;
       const double w = have ? dmul(dadd(smp.c.z, 2.0), 0.25) : 0.0;
-      const uint8_t* Abase = s.A + (warp * 32 / 8) * (4 * 128);
+      const uint8_t* Abase = s.A + (warp * 32 / 8) * (kch * 128);
 #pragma unroll 1
       // two (sample, level) pairs per lane per pass: 16 independent gathers in flight
       for (int base = 0; base < npairs; base += 64) {
@@ -357,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
 #pragma unroll
         for (int q = 0; q < 2; ++q)
           if (ok[q])
-            *reinterpret_cast<__half2*>(const_cast<uint8_t*>(Abase) + core_off(src[q], lv[q] >> 2, 4) +
+            *reinterpret_cast<__half2*>(const_cast<uint8_t*>(Abase) + core_off(src[q], lv[q] >> 2, kch) +
                                         (lv[q] & 3) * 4) = __floats2half2_rn(f[q].x, f[q].y);
       }
     }
@@ -375,13 +396,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     // ---- density L1: [128x32] x [32x64] -> relu -------------------------------------------
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer<64, 32>(s, s.W1, tmem);
+      issue_layer<64, 32 + kKb>(s, s.W1, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-    relu64_to_A(t_lane, s.b1, s.A, tid);
+    relu64_to_A(t_lane, s.A, tid);
     ptx::fence_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
@@ -389,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     // ---- density L2: [128x64] x [64x32(17)] -> sigma, bottleneck ++ SH ---------------------
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer<32, 64>(s, s.W2, tmem);
+      issue_layer<32, 64 + kKb>(s, s.W2, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
@@ -398,14 +419,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     ptx::tmem_ld16(t_lane, v);
     ptx::tmem_ld16(t_lane + 16, v + 16);
     ptx::tmem_ld_wait();
-    sigma = trunc_exp(v[0] + s.b2[0]);
+    sigma = trunc_exp(v[0]);
     {
+      constexpr int kch = (32 + kKb) / 8;
       float cin[32];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) cin[j] = v[1 + j] + s.b2[1 + j];
+      for (int j = 0; j < 16; ++j) cin[j] = v[1 + j];
       sh_encode(r.d, cin + 16);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) st_shared16(s.A, core_off(tid, j, 4), pack8(cin + 8 * j));
+      for (int j = 0; j < 4; ++j) st_shared16(s.A, core_off(tid, j, kch), pack8(cin + 8 * j));
+      write_bias_step(s.A, tid, 32);
     }
     ptx::fence_async_smem();
     ptx::tc_fence_before();
@@ -414,13 +437,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     // ---- colour L1: [128x32] x [32x64] -> relu -------------------------------------------
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer<64, 32>(s, s.C1, tmem);
+      issue_layer<64, 32 + kKb>(s, s.C1, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-    relu64_to_A(t_lane, s.cb1, s.A, tid);
+    relu64_to_A(t_lane, s.A, tid);
     ptx::fence_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
@@ -428,13 +451,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     // ---- colour L2: [128x64] x [64x64] -> relu -------------------------------------------
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer<64, 64>(s, s.C2, tmem);
+      issue_layer<64, 64 + kKb>(s, s.C2, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-    relu64_to_A(t_lane, s.cb2, s.A, tid);
+    relu64_to_A(t_lane, s.A, tid);
     ptx::fence_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
@@ -442,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     // ---- colour L3: [128x64] x [64x16(3)] -> sigmoid (PQ head) ---------------------------
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer<16, 64>(s, s.C3, tmem);
+      issue_layer<16, 64 + kKb>(s, s.C3, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
@@ -460,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
       float rgb[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const float raw = v[k] + s.cb3[k];
+        const float raw = v[k];
         rgb[k] = p.mlp.color_space == 0 ? sigmoid(raw) : trunc_exp(raw);
       }
       const double a = dsub(1.0, exp(dmul(-(double)sigma, smp.delta)));

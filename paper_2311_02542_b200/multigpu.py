@@ -25,6 +25,51 @@ def eye_bands(begin: int, end: int, eye_size: int):
             yield eye, lo - eye * eye_size, hi - eye * eye_size
 
 
+def gather_bands(dist, img, assign: WorkerAssignment, rank: int, world: int) -> None:
+    """Rank r > 0 sends rows [begin, end) of its band of the planar [C, H, W] image to rank 0
+    (one contiguous slab per plane), batched point-to-point; bands are unequal, so an
+    all-gather does not fit.  Works for CUDA tensors over NCCL and CPU tensors over gloo."""
+    if world == 1:
+        return
+    ops = []
+    planes = img.shape[0]
+    if rank == 0:
+        for r in range(1, world):
+            rr = assign.ranges[r]
+            if rr.count() > 0:
+                for c in range(planes):
+                    ops.append(dist.P2POp(dist.irecv, img[c, rr.begin:rr.end], r))
+    else:
+        rr = assign.ranges[rank]
+        if rr.count() > 0:
+            for c in range(planes):
+                ops.append(dist.P2POp(dist.isend, img[c, rr.begin:rr.end].contiguous(), 0))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+def exchange_ms(torch, dist, ms_local: float, world: int, device) -> List[float]:
+    """All ranks learn every rank's band time (the reference measures per worker,
+    scheduler.cpp:124-142)."""
+    if world == 1:
+        return [ms_local]
+    t = torch.tensor([ms_local], dtype=torch.float64, device=device)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [float(x.item()) for x in out]
+
+
+def rebalance(assign: WorkerAssignment, ms: List[float], width: int,
+              dampening: float) -> (FrameStats, WorkerAssignment):
+    """FrameStats of the finished frame and the next assignment (scheduler.cpp:154-162);
+    deterministic, so every rank computes the same partition."""
+    st = FrameStats(wall_ms=max(ms), rays=assign.height * width, worker_ms=list(ms),
+                    worker_rays=[r.count() * width for r in assign.ranges])
+    nxt = next_assignment(assign, st, dampening) if len(ms) > 1 else assign
+    return st, nxt
+
+
 class StereoFrameDriver:
     """Renders dual `eye_size`^2 eyebuffers stacked into one [3, 2*eye_size, eye_size]
     planar frame.  Each rank renders its scheduler band; rank 0 receives the others."""
@@ -67,41 +112,16 @@ class StereoFrameDriver:
         self.ev1.record()
 
     def gather_bands(self) -> None:
-        """NCCL point-to-point: every rank > 0 sends its band (3 contiguous plane slabs)."""
-        if self.world == 1 or not self.gather:
-            return
-        d = self.dist
-        ops = []
-        if self.rank == 0:
-            for r in range(1, self.world):
-                rr = self.assign.ranges[r]
-                for c in range(3):
-                    ops.append(d.P2POp(d.irecv, self.rgb[c, rr.begin:rr.end], r))
-        else:
-            rr = self.assign.ranges[self.rank]
-            for c in range(3):
-                ops.append(d.P2POp(d.isend, self.rgb[c, rr.begin:rr.end], 0))
-        for w in d.batch_isend_irecv(ops):
-            w.wait()
+        if self.gather:
+            gather_bands(self.dist, self.rgb, self.assign, self.rank, self.world)
 
     def rebalance(self) -> FrameStats:
-        """Per-rank render time of the frame just finished -> next assignment
-        (scheduler.cpp:154-162); identical on every rank."""
+        """Per-rank render time of the frame just finished -> next assignment."""
         self.ev1.synchronize()
-        ms_local = float(self.ev0.elapsed_time(self.ev1))
-        if self.world > 1:
-            t = self.torch.tensor([ms_local], dtype=self.torch.float64,
-                                  device=self.rgb.device)
-            out = [self.torch.zeros_like(t) for _ in range(self.world)]
-            self.dist.all_gather(out, t)
-            ms = [float(x.item()) for x in out]
-        else:
-            ms = [ms_local]
-        st = FrameStats(wall_ms=max(ms), rays=self.H * self.W, worker_ms=ms,
-                        worker_rays=[r.count() * self.W for r in self.assign.ranges])
+        ms = exchange_ms(self.torch, self.dist, float(self.ev0.elapsed_time(self.ev1)),
+                         self.world, self.rgb.device)
+        st, self.assign = rebalance(self.assign, ms, self.W, self.damp)
         self.history.append(st)
-        if self.world > 1:
-            self.assign = next_assignment(self.assign, st, self.damp)
         return st
 
     def frame(self, frame: int) -> FrameStats:

@@ -395,3 +395,26 @@ def render_rows(field: RadianceField, grid: OccupancyGrid, cam: CameraModel, opt
 
 def lod_levels_of(cfg: FieldConfig) -> List[int]:
     return [cfg.grid.resolution(l) for l in range(cfg.grid.levels)]
+
+
+def load_checkpoint(path: str):
+    """Reads a reference LUMICKPT v1 checkpoint (proj/src/scene.cpp:353-394): returns
+    (RadianceField, OccupancyGrid, info dict with samples_per_ray / background /
+    contraction / n_cameras).  Raises Error with the reference's messages on bad files."""
+    L = _abi.lib()
+    info = _abi.CheckpointInfo()
+    p = str(path).encode()
+    check(L.lumi_checkpoint_read(p, C.byref(info), None, None, None, None))
+    f = info.field
+    cfg = FieldConfig(HashGridConfig(f.levels, f.features_per_level, f.base_resolution,
+                                     f.per_level_scale, f.table_size), f.hidden_width,
+                      f.bottleneck, ColorSpaceMode(f.color_space))
+    field = RadianceField(cfg)
+    occ = np.zeros(info.occ_res ** 3, np.uint8)
+    check(L.lumi_checkpoint_read(p, C.byref(info), _p(field.grid_params),
+                                 _p(field.density_params), _p(field.color_params), _p(occ)))
+    field.touch()
+    grid = OccupancyGrid(info.occ_res, occ)
+    meta = dict(samples_per_ray=info.samples_per_ray, background=tuple(info.background),
+                contraction=ContractionMode(info.contraction), n_cameras=info.n_cameras)
+    return field, grid, meta

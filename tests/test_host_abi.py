@@ -88,3 +88,32 @@ def test_render_without_gpu_fails_loudly():
     with pytest.raises(L.Error) as ei:
         L.DeviceModel(f, L.OccupancyGrid(8))
     assert ei.value.code == _abi.LUMI_ERR_CUDA
+
+
+def test_checkpoint_ingest_matches_reference_writer(reference, tmp_path):
+    """§8f row 2: a LUMICKPT file written by the reference's save_checkpoint
+    (scene.cpp:320-351) is read back by the product's native reader bit for bit."""
+    cfg = O.field_config(table_size=1 << 12, base=16)
+    p = reference.synth_params(cfg, 5, 0.8)
+    rng = np.random.default_rng(2)
+    occ = (rng.random(32 ** 3) < 0.3).astype(np.uint8)
+    m = reference.model(p, occ, 32)
+    path = tmp_path / "model.lumickpt"
+    reference.save_checkpoint(m, path, spp=192, background=(0.1, 0.2, 0.3), contraction=1)
+    field, grid, meta = L.load_checkpoint(path)
+    assert np.array_equal(field.grid_params, p.table)
+    assert np.array_equal(field.density_params, p.dparams)
+    assert np.array_equal(field.color_params, p.cparams)
+    assert grid.res == 32 and np.array_equal(grid.bits, occ)
+    assert meta["samples_per_ray"] == 192 and meta["background"] == (0.1, 0.2, 0.3)
+    assert meta["contraction"] == L.ContractionMode.kLInfCubic and meta["n_cameras"] == 2
+    assert field.cfg.grid.table_size == 1 << 12 and field.cfg.grid.base_resolution == 16
+    # corrupt / truncated files fail with the reference's messages
+    raw = path.read_bytes()
+    bad = tmp_path / "bad.lumickpt"
+    bad.write_bytes(b"NOTACKPT" + raw[8:])
+    with pytest.raises(L.Error, match="bad magic"):
+        L.load_checkpoint(bad)
+    bad.write_bytes(raw[: len(raw) - 100])
+    with pytest.raises(L.Error, match="truncated"):
+        L.load_checkpoint(bad)
