@@ -116,7 +116,8 @@ __device__ __forceinline__ float2 encode_level_h(const GridDev& g, const __half2
                                                  int l, double u, double v, double s, float wl) {
   const int res = g.res[l];
   const double r = (double)res;
-  const double pu = dmul(clamp01(u), r), pv = dmul(clamp01(v), r), ps = dmul(clamp01(s), r);
+  // u, v, s arrive clamped to [0, 1] (hoisted out of the level loop by the caller)
+  const double pu = dmul(u, r), pv = dmul(v, r), ps = dmul(s, r);
   const int iu = min(__double2int_rz(pu), res - 1), iv = min(__double2int_rz(pv), res - 1),
             is = min(__double2int_rz(ps), res - 1);
   uint32_t idx[8];

@@ -344,9 +344,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
         npairs += __popc(m);
       }
       __syncwarp();
-      const double u = have ? dmul(dadd(smp.c.x, 2.0), 0.25) : 0.0;
-      const double v = have ? dmul(dadd(smp.c.y, 2.0), 0.25) : 0.0;
-      const double w = have ? dmul(dadd(smp.c.z, 2.0), 0.25) : 0.0;
+      // unit-cube coordinates (grid.h:93-95), clamped once per sample (grid.h:146-148) and
+      // split into float pairs for the fp32 cell arithmetic of encode_level_hf
+      const double u = clamp01(have ? dmul(dadd(smp.c.x, 2.0), 0.25) : 0.0);
+      const double v = clamp01(have ? dmul(dadd(smp.c.y, 2.0), 0.25) : 0.0);
+      const double w = clamp01(have ? dmul(dadd(smp.c.z, 2.0), 0.25) : 0.0);
       const uint8_t* Abase = s.A + (warp * 32 / 8) * (kch * 128);
 #pragma unroll 1
       // two (sample, level) pairs per lane per pass: 16 independent gathers in flight
