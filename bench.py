@@ -144,20 +144,34 @@ def reference_model(spec):
     return O, ref, ref.model(p, grid.bits, grid.res)
 
 
+SAMPLE_BANDS = 8
+
+
 def reference_sample(O, ref, model, cam_spec, target_s, threads):
-    """Times the reference run_frame (scheduler.cpp:114) over a centred band of rows of one
-    eye, sized to take ~target_s seconds; returns (rays/s, rows, seconds)."""
+    """Times the reference run_frame (scheduler.cpp:114) over SAMPLE_BANDS bands of rows
+    spread evenly down one eye (a representative sample of the frame), sized to take about
+    target_s seconds in total; returns (rays/s, rows, seconds)."""
     cam = O.camera(cam_spec.rot, cam_spec.origin, cam_spec.fx, cam_spec.fy, cam_spec.cx,
                    cam_spec.cy, cam_spec.width, cam_spec.height, cam_spec.t_near, cam_spec.t_far)
     opts = O.render_options()
-    mid = cam_spec.height // 2
-    rows = max(threads, 2)
-    ms, _ = ref.run_frame(model, cam, opts, mid - rows // 2, mid - rows // 2 + rows, threads)
-    rate = rows * cam_spec.width / (ms / 1000.0)
-    rows = int(min(cam_spec.height, max(threads, target_s * rate / cam_spec.width)))
-    b = max(0, mid - rows // 2)
-    ms, _ = ref.run_frame(model, cam, opts, b, b + rows, threads)
-    return rows * cam_spec.width / (ms / 1000.0), rows, ms / 1000.0
+    H, W = cam_spec.height, cam_spec.width
+
+    def run(band_rows):
+        total_ms = 0.0
+        for k in range(SAMPLE_BANDS):
+            b = int((k + 0.5) * H / SAMPLE_BANDS) - band_rows // 2
+            b = min(max(b, 0), H - band_rows)
+            ms, _ = ref.run_frame(model, cam, opts, b, b + band_rows, threads)
+            total_ms += ms
+        return total_ms
+
+    band = max(threads, 2)
+    ms = run(band)
+    rate = SAMPLE_BANDS * band * W / (ms / 1000.0)
+    band = int(min(H // SAMPLE_BANDS, max(threads, target_s * rate / W / SAMPLE_BANDS)))
+    ms = run(band)
+    rows = SAMPLE_BANDS * band
+    return rows * W / (ms / 1000.0), rows, ms / 1000.0
 
 
 def run_reference(args):
@@ -198,7 +212,8 @@ def run_reference(args):
         "fps": round(mrays * 1e6 / rays_frame, 6),
         "cpu_baseline": {"value": round(mrays, 6), "unit": UNIT, "cores": threads,
                          "kind": "reference",
-                         "sample": f"run_frame over {rows} centred rows x {cfg.eye_size} of the "
+                         "sample": f"run_frame over {rows} rows ({SAMPLE_BANDS} evenly spread "
+                                   f"bands) x {cfg.eye_size} of the "
                                    f"left eye per step, simd={ref.simd_name()}"},
         "e2e": {"value": round(mrays, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -327,7 +342,8 @@ def run_ours(args):
             rate, rows, secs = reference_sample(O, ref, model, eye, args.cpu_seconds, threads)
             cpu = {"value": round(rate / 1e6, 6), "unit": UNIT, "cores": threads,
                    "kind": "reference",
-                   "sample": f"reference run_frame over {rows} centred rows x {cfg.eye_size} of "
+                   "sample": f"reference run_frame over {rows} rows ({SAMPLE_BANDS} evenly "
+                             f"spread bands) x {cfg.eye_size} of "
                              f"the left eye ({rows * cfg.eye_size} rays, {secs:.1f}s), "
                              f"simd={ref.simd_name()}"}
         except Exception as e:  # noqa: BLE001
