@@ -235,3 +235,68 @@ def test_gpu_bake_vs_reference_bake(lumi, torch_cuda, small):
     samp = z["probe_sample"]
     got = pm[z["probe_sample_idx"]]
     assert np.allclose(got, samp, rtol=1e-3, atol=1e-3)
+
+
+def test_display_epilogue_srgb8(lumi, torch_cuda, small, oracle):
+    """§8f row 3: the fused PQ -> scene-linear -> 2^bias -> sRGB8 eyebuffer store matches
+    pq_to_srgb_float (trainer.cpp:175-182) + tonemap_srgb rounding (color.cpp:104-115)
+    applied to the kernel's own PQ output, within one code value."""
+    W = H = 64
+    cam = lumi.CameraModel.from_spec(scenes.pinhole(W, H))
+    rgb = torch_cuda.zeros((3, H, W), dtype=torch_cuda.float32, device="cuda")
+    srgb = torch_cuda.zeros((H, W, 3), dtype=torch_cuda.uint8, device="cuda")
+    for bias in (0.0, 1.5):
+        t = lumi.renderer._abi.FrameTarget()
+        t.rgb, t.srgb8, t.width, t.height = rgb.data_ptr(), srgb.data_ptr(), W, H
+        t.exposure_bias_stops = bias
+        small["dm"].render_rows_async(cam, lumi.RenderOptions(), 0, H, t,
+                                      torch_cuda.cuda.current_stream().cuda_stream)
+        torch_cuda.cuda.synchronize()
+        pq = rgb.cpu().numpy()
+        want = np.zeros((H, W, 3), np.int32)
+        for c in range(3):
+            for y in range(H):
+                for x in range(W):
+                    lin = oracle.pq_decode(min(max(float(pq[c, y, x]), 0.0), 1.0))
+                    want[y, x, c] = int(round(oracle.srgb_oetf(min(lin * 2 ** bias, 1.0)) * 255))
+        got = srgb.cpu().numpy().astype(np.int32)
+        assert np.abs(got - want).max() <= 1, bias
+
+
+def test_linear_color_head_vs_oracle(lumi, torch_cuda, small_scene, oracle):
+    """field.h:135-136: the kLinear ablation head (trunc_exp instead of sigmoid)."""
+    import oracle as O
+    s = small_scene["spec"]
+    cfg = lumi.FieldConfig(grid=lumi.HashGridConfig(table_size=s.table_size),
+                           color_space=lumi.ColorSpaceMode.kLinear)
+    field = lumi.RadianceField.synthetic(cfg, s.seed, s.amplitude)
+    dm = lumi.DeviceModel(field, lumi.OccupancyGrid(small_scene["res"], small_scene["occ"]), 0)
+    spec = scenes.pinhole(48, 40)
+    cam = lumi.CameraModel.from_spec(spec)
+    out = np.zeros((3, 40, 48), np.float32)
+    dm.render_rows(cam, lumi.RenderOptions(), 0, 40, out)
+    ocfg = O.field_config(table_size=s.table_size, color_space=1)
+    om = oracle.model(oracle.synth_params(ocfg, s.seed, s.amplitude), small_scene["occ"],
+                      small_scene["res"])
+    ref = oracle.render_rows(om, ocam(spec), O.render_options(), 0, 40)
+    scale = max(1.0, float(np.abs(ref["out"]).max()))
+    assert np.abs(out - ref["out"]).max() <= 1e-3 * scale
+
+
+def test_stress_dense_occupancy_4k_rows(lumi, torch_cuda, small, oracle):
+    """C5 flavour: all-occupied grid (no skipping, little early termination) on a band of a
+    4096^2 eye against the oracle."""
+    grid = lumi.OccupancyGrid(128)
+    dm = lumi.DeviceModel(small["field"], grid, 0)
+    spec = scenes.pinhole(4096, 4096)
+    cam = lumi.CameraModel.from_spec(spec)
+    out = np.zeros((3, 4096, 4096), np.float32)
+    stats = []
+    dm.render_rows(cam, lumi.RenderOptions(), 2040, 2048, out, None, None, stats)
+    ones = np.ones(128 ** 3, np.uint8)
+    import oracle as O
+    om = oracle.model(small["params"], ones, 128)
+    ref = oracle.render_rows(om, ocam(spec), O.render_options(), 2040, 2048)
+    band = slice(2040, 2048)
+    assert np.abs(out[:, band] - ref["out"][:, band]).max() <= PIX_TOL
+    assert sum(s.evals for s in stats) == pytest.approx(int(ref["row_evals"].sum()), rel=0.01)
