@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -29,6 +30,10 @@ namespace tc {
 constexpr int kThreads = 128;  // UMMA M
 constexpr int kTileW = 16, kTileH = 8;
 constexpr uint32_t kTmemCols = 64;
+#ifndef LUMI_PPP
+#define LUMI_PPP 2
+#endif
+constexpr int kPPP = LUMI_PPP;  // gather pairs per lane per pass
 
 // Every layer's K carries one extra 16-wide step whose first column is 1 in A and the bias
 // in B, so the tensor core adds the bias (fp16 x 1 into the fp32 accumulator).
@@ -351,14 +356,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
       const double w = clamp01(have ? dmul(dadd(smp.c.z, 2.0), 0.25) : 0.0);
       const uint8_t* Abase = s.A + (warp * 32 / 8) * (kch * 128);
 #pragma unroll 1
-      // two (sample, level) pairs per lane per pass: 16 independent gathers in flight
-      for (int base = 0; base < npairs; base += 64) {
-        int src[2], lv[2];
-        bool ok[2];
-        double su[2], sv[2], sw[2];
-        float wl[2];
+      // kPPP (sample, level) pairs per lane per pass: 8 * kPPP independent gathers in flight
+      for (int base = 0; base < npairs; base += 32 * kPPP) {
+        int src[kPPP], lv[kPPP];
+        bool ok[kPPP];
+        double su[kPPP], sv[kPPP], sw[kPPP];
+        float wl[kPPP];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < kPPP; ++q) {
           const int pi = base + 32 * q + lane;
           ok[q] = pi < npairs;
           src[q] = ok[q] ? psrc[pi] : lane;
@@ -372,13 +377,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
           lw.floor_only = __shfl_sync(0xffffffffu, (int)smp.lw.floor_only, src[q]) != 0;
           wl[q] = lod_weight_at(lw, lv[q]);
         }
-        float2 f[2];
+        float2 f[kPPP];
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
+        for (int q = 0; q < kPPP; ++q)
           f[q] = ok[q] && !(p.debug_flags & 1) ? encode_level_h(p.grid, p.grid.table16, lv[q], su[q], sv[q], sw[q], wl[q])
                        : make_float2(0.f, 0.f);
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
+        for (int q = 0; q < kPPP; ++q)
           if (ok[q])
             *reinterpret_cast<__half2*>(const_cast<uint8_t*>(Abase) + core_off(src[q], lv[q] >> 2, kch) +
                                         (lv[q] & 3) * 4) = __floats2half2_rn(f[q].x, f[q].y);
@@ -545,6 +550,14 @@ cudaError_t launch_render_tc(RenderParams p, cudaStream_t s, int num_sms) {
     const int by_regs = 65536 / (regs_per_warp * (tc::kThreads / 32));
     const int by_smem = (228 * 1024) / (int)(smem + 1024);
     blocks_per_sm = std::max(blocks_per_sm, std::max(1, std::min(by_regs, by_smem)));
+    // Shared memory and L1 share one 256 KB array: reserve only what the resident CTAs need
+    // so the rest stays L1 for the hash-table gathers (LUMI_MAX_CTAS caps residency).
+    if (const char* cap = std::getenv("LUMI_MAX_CTAS"))
+      blocks_per_sm = std::max(1, std::min(blocks_per_sm, std::atoi(cap)));
+    const int carve = (int)std::ceil(100.0 * blocks_per_sm * (double)(smem + 1024) / (228.0 * 1024));
+    if ((e = cudaFuncSetAttribute(tc::k_render_tc, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  std::min(100, carve))) != cudaSuccess)
+      return e;
     if (std::getenv("LUMI_DEBUG")) {
       cudaFuncAttributes fa;
       cudaFuncGetAttributes(&fa, tc::k_render_tc);
