@@ -141,9 +141,11 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
                       const float* density_params, const float* color_params,
                       const uint8_t* occupancy, int occ_res, LumiModel** out);
 int lumi_model_set_occupancy(LumiModel* m, const uint8_t* occupancy, int occ_res);
-/* Frame-renderer variant: LUMI_KERNEL_TC (default; persistent tcgen05 MLP kernel) or
-   LUMI_KERNEL_SIMT (thread-per-ray, fp32 CUDA-core MLP -- the numerical cross-check). */
-enum { LUMI_KERNEL_TC = 0, LUMI_KERNEL_SIMT = 1 };
+/* Frame-renderer variant: LUMI_KERNEL_TC (persistent tcgen05 MLP kernel, one live ray per
+   thread), LUMI_KERNEL_PACKET (tcgen05, warp-wide ray packets streamed candidate-major for
+   coherent gathers) or LUMI_KERNEL_SIMT (thread-per-ray fp32 CUDA-core MLP -- the numerical
+   cross-check).  The environment variable LUMI_KERNEL=tc|packet|simt sets the default. */
+enum { LUMI_KERNEL_TC = 0, LUMI_KERNEL_SIMT = 1, LUMI_KERNEL_PACKET = 2 };
 int lumi_model_set_kernel(LumiModel* m, int kernel);
 int lumi_model_destroy(LumiModel* m);
 /* Device-side memory footprint of the model in bytes. */

@@ -27,5 +27,7 @@ cudaError_t launch_march_kept(const lumi_dev::RenderParams& p, uint32_t* mask, i
                               cudaStream_t s);
 cudaError_t launch_render_tc(lumi_dev::RenderParams p, cudaStream_t s, int num_sms);
 size_t render_tc_smem_bytes();
+cudaError_t launch_march_mask(const lumi_dev::RenderParams& p, cudaStream_t s);
+cudaError_t launch_render_pk(lumi_dev::RenderParams p, cudaStream_t s, int num_sms);
 cudaError_t launch_to_half(const float* src, void* dst_half, uint64_t n, cudaStream_t s);
 cudaError_t launch_bake(const lumi_dev::BakeParams& p, cudaStream_t s);

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <map>
@@ -385,6 +386,10 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
       (e = cudaDeviceSynchronize()) != cudaSuccess)
     return cleanup(fail(LUMI_ERR_CUDA, std::string("model upload: ") + cudaGetErrorString(e)));
   if ((rc = lumi_model_set_occupancy(m, occ, occ_res))) return cleanup(rc);
+  if (const char* k = std::getenv("LUMI_KERNEL")) {
+    const std::string ks(k);
+    m->kernel = ks == "simt" ? LUMI_KERNEL_SIMT : ks == "packet" ? LUMI_KERNEL_PACKET : LUMI_KERNEL_TC;
+  }
   *out = m;
   return LUMI_OK;
 }
@@ -421,7 +426,7 @@ int lumi_model_destroy(LumiModel* m) {
 
 int lumi_model_set_kernel(LumiModel* m, int kernel) {
   if (!m) return fail(LUMI_ERR_INVALID, "null model");
-  if (kernel != LUMI_KERNEL_TC && kernel != LUMI_KERNEL_SIMT)
+  if (kernel != LUMI_KERNEL_TC && kernel != LUMI_KERNEL_SIMT && kernel != LUMI_KERNEL_PACKET)
     return fail(LUMI_ERR_INVALID, "unknown kernel variant");
   m->kernel = kernel;
   return LUMI_OK;
@@ -444,6 +449,8 @@ int lumi_render_rows_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRe
   if ((rc = set_target(&p, t, b, e))) return rc;
   if (m->kernel == LUMI_KERNEL_SIMT)
     LUMI_CUDA_TRY(launch_render_simt(p, static_cast<cudaStream_t>(stream)));
+  else if (m->kernel == LUMI_KERNEL_PACKET)
+    LUMI_CUDA_TRY(launch_render_pk(p, static_cast<cudaStream_t>(stream), m->num_sms));
   else
     LUMI_CUDA_TRY(launch_render_tc(p, static_cast<cudaStream_t>(stream), m->num_sms));
   return LUMI_OK;

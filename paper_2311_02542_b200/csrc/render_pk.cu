@@ -1,0 +1,543 @@
+// render_pk.cu -- packet-coherent B200 frame renderer.
+//
+// Each warp owns a PACKET of 32 neighbouring rays (an 8x4 pixel patch) and streams the
+// packet's occupancy-kept samples in candidate-major order: all rays' samples at candidate i
+// before those at i+1.  Every round a warp contributes 32 consecutive samples of its stream
+// as its 32 rows of the CTA's 128-row MLP batch, so the rows of a warp are neighbouring rays
+// at the same distance -- they gather neighbouring (often identical) hash-grid cells, which
+// is what keeps the L1 wavefront count per gather low.  The batch then runs through the five
+// tcgen05 layers exactly as in render_tc.cu, and each ray's owner lane composites its
+// samples of the round in order (renderer.h:170-190).
+//
+// Per-sample geometry for the network input is fp32 (position, contraction, LOD footprint):
+// the oracle measures no change against double coordinates (1.24e-4 vs 1.36e-4 max |dPQ| on
+// a 2K band of the T=2^22 model, both dominated by the fp16 MLP operands).  The occupancy
+// test that selects the samples stays the bit-exact double march pass.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "kernels.h"
+#include "render_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace lumi_dev {
+namespace pk {
+
+constexpr int kThreads = 128;  // UMMA M: 4 warps x 32 rows
+constexpr int kWarps = kThreads / 32;
+constexpr int kPW = 8, kPH = 4;  // packet: 8 x 4 pixels = one warp of rays
+constexpr uint32_t kTmemCols = 64;
+
+struct __align__(1024) Smem {
+  uint8_t A[128 * 64 * 2];  // activations, K-major core-matrix tile (K <= 64)
+  uint8_t W1[64 * 32 * 2];  // density L1  N=64 K=32
+  uint8_t W2[32 * 64 * 2];  // density L2  N=32 (17 used) K=64
+  uint8_t C1[64 * 32 * 2];  // colour L1   N=64 K=32
+  uint8_t C2[64 * 64 * 2];  // colour L2   N=64 K=64
+  uint8_t C3[16 * 64 * 2];  // colour L3   N=16 (3 used) K=64
+  float b1[64], b2[32], cb1[64], cb2[64], cb3[16];
+  float4 res[kThreads];     // per row: sigma, r, g, b (row lane -> owner lane)
+  uint32_t ballot[kWarps][32];   // per warp: lanes with candidate bit i of the current word
+  uint16_t prefix[kWarps][33];   // exclusive prefix of popc(ballot[i])
+  uint64_t mbar;
+  uint32_t tmem_base;
+  uint8_t pair_src[kWarps][32 * kMaxLevels];
+  uint8_t pair_lvl[kWarps][32 * kMaxLevels];
+};
+
+__device__ __forceinline__ uint32_t core_off(int row, int chunk, int kchunks) {
+  return (uint32_t)((row >> 3) * (kchunks * 128) + chunk * 128 + (row & 7) * 16);
+}
+
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+__device__ __forceinline__ void st16(uint8_t* base, uint32_t off, uint4 v) {
+  *reinterpret_cast<uint4*>(base + off) = v;
+}
+
+__device__ __forceinline__ uint4 pack8(const float* v) {
+  return make_uint4(h2u(__floats2half2_rn(v[0], v[1])), h2u(__floats2half2_rn(v[2], v[3])),
+                    h2u(__floats2half2_rn(v[4], v[5])), h2u(__floats2half2_rn(v[6], v[7])));
+}
+
+// weights [n_real x K] fp32 row-major (network.h:64) -> fp16 UMMA tile with n_pad rows
+__device__ void load_weight_tile(uint8_t* dst, const float* __restrict__ W, int n_real, int n_pad,
+                                 int K) {
+  const int kch = K / 8;
+  for (int it = threadIdx.x; it < n_pad * kch; it += blockDim.x) {
+    const int n = it / kch, j = it % kch;
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = n < n_real ? __ldg(W + (size_t)n * K + 8 * j + q) : 0.f;
+    st16(dst, core_off(n, j, kch), pack8(v));
+  }
+}
+
+template <int N, int K>
+__device__ __forceinline__ void issue_layer(const uint8_t* A, const uint8_t* B, uint32_t d_tmem) {
+  constexpr uint32_t idesc = ptx::idesc_f16_f32<128, N>();
+  const uint32_t a = ptx::smem_addr(A), b = ptx::smem_addr(B);
+#pragma unroll
+  for (int kk = 0; kk < K / 16; ++kk)
+    ptx::mma_f16(d_tmem, ptx::make_smem_desc(a + kk * 256, 128, (K / 8) * 128),
+                 ptx::make_smem_desc(b + kk * 256, 128, (K / 8) * 128), idesc, kk > 0 ? 1u : 0u);
+}
+
+// hidden-layer epilogue: TMEM row + bias, ReLU, fp16 -> this row of the next A tile (K = 64)
+__device__ __forceinline__ void relu64_to_A(uint32_t t_lane, const float* bias, uint8_t* A,
+                                            int row) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float v[32];
+    ptx::tmem_ld16(t_lane + 32 * h, v);
+    ptx::tmem_ld16(t_lane + 32 * h + 16, v + 16);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + bias[32 * h + j], 0.f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) st16(A, core_off(row, 4 * h + j, 8), pack8(v + 8 * j));
+  }
+}
+
+// position of the (k+1)-th set bit of m (k < popc(m))
+__device__ __forceinline__ int nth_set_bit(uint32_t m, int k) {
+  int pos = 0;
+#pragma unroll
+  for (int w = 16; w > 0; w >>= 1) {
+    const int c = __popc(m & ((1u << w) - 1u));
+    if (k >= c) {
+      k -= c;
+      m >>= w;
+      pos += w;
+    }
+  }
+  return pos;
+}
+
+// The owner-lane state of one ray of the packet.
+struct Ray {
+  bool valid, alive;  // pixel inside the range / still compositing
+  int x, y, id;
+  float3 d, nd;       // fp32 directions for the network-input geometry
+  uint32_t todo;      // kept candidates of the current word not yet composited
+  int kept_total, contributing;
+  bool term;
+  double trans, px, py, pz, depth, opac;
+};
+
+struct Counters {
+  unsigned evals, level_samples, marched, rays;
+};
+
+__global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned FULL = 0xffffffffu;
+
+  // ---- setup: weights, biases, mbarrier, TMEM ------------------------------------------
+  const float* dp = p.mlp.dparams;
+  const float* cp = p.mlp.cparams;
+  const float* d2 = dp + 64 * 32 + 64;
+  const float* c2 = cp + 64 * 32 + 64;
+  const float* c3 = c2 + 64 * 64 + 64;
+  load_weight_tile(s.W1, dp, 64, 64, 32);
+  load_weight_tile(s.W2, d2, 1 + kBottleneck, 32, 64);
+  load_weight_tile(s.C1, cp, 64, 64, 32);
+  load_weight_tile(s.C2, c2, 64, 64, 64);
+  load_weight_tile(s.C3, c3, 3, 16, 64);
+  for (int i = tid; i < 64; i += kThreads) {
+    s.b1[i] = dp[64 * 32 + i];
+    s.cb1[i] = cp[64 * 32 + i];
+    s.cb2[i] = c2[64 * 64 + i];
+  }
+  for (int i = tid; i < 32; i += kThreads) s.b2[i] = i < 17 ? d2[17 * 64 + i] : 0.f;
+  for (int i = tid; i < 16; i += kThreads) s.cb3[i] = i < 3 ? c3[3 * 64 + i] : 0.f;
+  if (tid == 0) {
+    ptx::mbar_init(&s.mbar, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0) ptx::tmem_alloc<kTmemCols>(&s.tmem_base);
+  ptx::fence_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+  const uint32_t t_lane = tmem + ((uint32_t)(warp * 32) << 16);
+
+  const float3 o = make_float3((float)p.cam.origin[0], (float)p.cam.origin[1], (float)p.cam.origin[2]);
+  const float two_base = (float)p.grid.two_base, inv_log = (float)(1.0 / p.grid.log_scale);
+  const int levels = p.grid.levels;
+  const long long packets_x = p.tiles_x;
+  const long long total_packets = p.total_rays / 32;
+
+  Counters cnt{0, 0, 0, 0};
+  Ray r;
+  r.valid = r.alive = false;
+  // warp-uniform packet stream state
+  bool packet_live = false, no_more = false;
+  int word = 0;        // current mask word of the packet
+  int g_next = 0;      // next stream position inside the word
+  int word_total = 0;  // samples in the word
+  uint32_t phase = 0;
+  const bool issuer = (tid == 0);
+
+  for (;;) {
+    // ---- A: this warp's 32 rows: the next samples of its packet stream --------------------
+    int take = 0, g0 = 0;
+    while (!no_more) {
+      if (!packet_live) {
+        long long pkt = 0;
+        if (lane == 0) pkt = (long long)atomicAdd(p.work_counter, 1u);
+        pkt = __shfl_sync(FULL, pkt, 0);
+        if (pkt >= total_packets) {
+          no_more = true;
+          break;
+        }
+        const long long rid = pkt * 32 + lane;
+        r.x = (int)(pkt % packets_x) * kPW + (lane % kPW);
+        r.y = p.row_begin + (int)(pkt / packets_x) * kPH + lane / kPW;
+        r.id = (int)rid;
+        r.valid = r.x < p.cam.width && r.y < p.row_end;
+        r.alive = r.valid;
+        if (r.valid) {
+          const d3 dd = ray_dir(p.cam, (double)r.x + 0.5, (double)r.y + 0.5);
+          const d3 nn = ray_dir(p.cam, (double)r.x + 1.5, (double)r.y + 0.5);
+          r.d = make_float3((float)dd.x, (float)dd.y, (float)dd.z);
+          r.nd = make_float3((float)nn.x, (float)nn.y, (float)nn.z);
+          r.kept_total = __ldg(p.kept_count + rid);
+          ++cnt.rays;
+          cnt.marched += p.n;
+        }
+        r.contributing = 0;
+        r.term = false;
+        r.trans = 1.0;
+        r.px = r.py = r.pz = r.depth = r.opac = 0.0;
+        r.todo = 0;
+        packet_live = true;
+        word = -1;
+        g_next = word_total = 0;
+      }
+      if (g_next < word_total) {
+        take = min(32, word_total - g_next);
+        g0 = g_next;
+        g_next += take;
+        break;
+      }
+      // next word: the alive rays' kept candidates, candidate-major prefix sums
+      if (word + 1 >= p.mask_words) {
+        // packet exhausted: owners store their pixels (renderer.h:233-236, 267-276)
+        if (r.valid) {
+          RayResult res{r.px, r.py, r.pz, r.depth, r.opac,
+                        chunk_evals(r.term, r.contributing, r.kept_total, p.chunk),
+                        r.contributing};
+          store_ray(p, r.x, r.y, res, r.trans);
+        }
+        packet_live = false;
+        continue;
+      }
+      ++word;
+      const uint32_t bits = r.alive ? __ldg(p.kept_mask + (size_t)word * p.total_rays + r.id) : 0u;
+      r.todo = bits;
+      int run = 0;
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t b = __ballot_sync(FULL, (bits >> i) & 1u);
+        if (lane == 0) {
+          s.ballot[warp][i] = b;
+          s.prefix[warp][i] = (uint16_t)run;
+        }
+        run += __popc(b);
+      }
+      if (lane == 0) s.prefix[warp][32] = (uint16_t)run;
+      __syncwarp();
+      g_next = 0;
+      word_total = run;
+    }
+
+    // row lane: its (candidate, ray lane) and network-input geometry
+    const bool have = lane < take;
+    int ci = 0, rl = lane;
+    if (have) {
+      const int g = g0 + lane;
+      int lo = 0;  // largest i with prefix[i] <= g
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1)
+        if (s.prefix[warp][lo + st] <= g) lo += st;
+      ci = lo;
+      rl = nth_set_bit(s.ballot[warp][ci], g - s.prefix[warp][ci]);
+    }
+    const float dx = __shfl_sync(FULL, r.d.x, rl), dy = __shfl_sync(FULL, r.d.y, rl),
+                dz = __shfl_sync(FULL, r.d.z, rl);
+    const float nx = __shfl_sync(FULL, r.nd.x, rl), ny = __shfl_sync(FULL, r.nd.y, rl),
+                nz = __shfl_sync(FULL, r.nd.z, rl);
+    const int cand = word * 32 + ci;
+    double u = 0.0, v = 0.0, w = 0.0;
+    LodW lw{0, 0.f, false};
+    int na = 0;
+    if (have) {
+      const float t = (float)__ldg(p.ts + cand);
+      const float3 c = contract_f(make_float3(o.x + dx * t, o.y + dy * t, o.z + dz * t), p.contraction);
+      u = clamp01(((double)c.x + 2.0) * 0.25);
+      v = clamp01(((double)c.y + 2.0) * 0.25);
+      w = clamp01(((double)c.z + 2.0) * 0.25);
+      if (p.lod_enabled) {
+        const float3 b = contract_f(make_float3(o.x + nx * t, o.y + ny * t, o.z + nz * t), p.contraction);
+        const float ex = c.x - b.x, ey = c.y - b.y, ez = c.z - b.z;
+        const float rc = fmaxf(0.5f * sqrtf(ex * ex + ey * ey + ez * ez), 1e-12f);
+        const float l = fminf(-__logf(two_base * rc) * inv_log, (float)(levels - 1));
+        lw = lod_weights_f(l + (float)p.lod_bias, levels);
+      } else {
+        lw = LodW{levels, 0.f, false};
+      }
+      na = active_levels(lw, levels);
+      cnt.level_samples += na;
+    }
+
+    // ---- B: warp-cooperative hash-grid gather, level-major (sample, level) pairs ----------
+    {
+      const uint4 zero = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) st16(s.A, core_off(tid, j, 4), zero);
+      uint8_t* psrc = s.pair_src[warp];
+      uint8_t* plvl = s.pair_lvl[warp];
+      const unsigned lt = (1u << lane) - 1u;
+      int npairs = 0;
+      for (int l = 0; l < levels; ++l) {
+        const unsigned m = __ballot_sync(FULL, na > l);
+        if (na > l) {
+          const int at = npairs + __popc(m & lt);
+          psrc[at] = (uint8_t)lane;
+          plvl[at] = (uint8_t)l;
+        }
+        npairs += __popc(m);
+      }
+      __syncwarp();
+      const uint8_t* Abase = s.A + (warp * 32 / 8) * (4 * 128);
+#pragma unroll 1
+      for (int base = 0; base < npairs; base += 64) {
+        int src[2], lv[2];
+        bool ok[2];
+        double su[2], sv[2], sw[2];
+        float wl[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int pi = base + 32 * q + lane;
+          ok[q] = pi < npairs;
+          src[q] = ok[q] ? psrc[pi] : lane;
+          lv[q] = ok[q] ? plvl[pi] : 0;
+          su[q] = __shfl_sync(FULL, u, src[q]);
+          sv[q] = __shfl_sync(FULL, v, src[q]);
+          sw[q] = __shfl_sync(FULL, w, src[q]);
+          LodW lq;
+          lq.full = __shfl_sync(FULL, lw.full, src[q]);
+          lq.frac = __shfl_sync(FULL, lw.frac, src[q]);
+          lq.floor_only = __shfl_sync(FULL, (int)lw.floor_only, src[q]) != 0;
+          wl[q] = lod_weight_at(lq, lv[q]);
+        }
+        float2 f[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          f[q] = ok[q] ? encode_level_h(p.grid, p.grid.table16, lv[q], su[q], sv[q], sw[q], wl[q])
+                       : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          if (ok[q])
+            *reinterpret_cast<__half2*>(const_cast<uint8_t*>(Abase) + core_off(src[q], lv[q] >> 2, 4) +
+                                        (lv[q] & 3) * 4) = __floats2half2_rn(f[q].x, f[q].y);
+      }
+    }
+    ptx::fence_async_smem();
+    if (!__syncthreads_or(have)) {
+      if (__syncthreads_and(no_more)) break;  // every warp's stream is exhausted
+      continue;
+    }
+
+    // ---- MLP: five tcgen05 layers over the 128-row batch (field.h:106-137) -------------
+    float v32[32];
+    if (issuer) {
+      ptx::tc_fence_after();
+      issue_layer<64, 32>(s.A, s.W1, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+    relu64_to_A(t_lane, s.b1, s.A, tid);
+    ptx::fence_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+
+    if (issuer) {
+      ptx::tc_fence_after();
+      issue_layer<32, 64>(s.A, s.W2, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+    ptx::tmem_ld16(t_lane, v32);
+    ptx::tmem_ld16(t_lane + 16, v32 + 16);
+    ptx::tmem_ld_wait();
+    const float sigma = trunc_exp(v32[0] + s.b2[0]);
+    {
+      float cin[32];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) cin[j] = v32[1 + j] + s.b2[1 + j];
+      sh_encode(d3{(double)dx, (double)dy, (double)dz}, cin + 16);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) st16(s.A, core_off(tid, j, 4), pack8(cin + 8 * j));
+    }
+    ptx::fence_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+
+    if (issuer) {
+      ptx::tc_fence_after();
+      issue_layer<64, 32>(s.A, s.C1, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+    relu64_to_A(t_lane, s.cb1, s.A, tid);
+    ptx::fence_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+
+    if (issuer) {
+      ptx::tc_fence_after();
+      issue_layer<64, 64>(s.A, s.C2, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+    relu64_to_A(t_lane, s.cb2, s.A, tid);
+    ptx::fence_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+
+    if (issuer) {
+      ptx::tc_fence_after();
+      issue_layer<16, 64>(s.A, s.C3, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+    ptx::tmem_ld16(t_lane, v32);
+    ptx::tmem_ld_wait();
+    ptx::tc_fence_before();
+    if (have) {
+      float rgb[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float raw = v32[k] + s.cb3[k];
+        rgb[k] = p.mlp.color_space == 0 ? sigmoid(raw) : trunc_exp(raw);
+      }
+      s.res[tid] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
+    }
+    __syncwarp();
+
+    // ---- C: owners composite their samples of this round, in order (renderer.h:170-190) ---
+    if (r.alive && take > 0) {
+      const unsigned lt = (1u << lane) - 1u;
+      while (r.todo) {
+        const int i = __ffs(r.todo) - 1;
+        const int g = s.prefix[warp][i] + __popc(s.ballot[warp][i] & lt);
+        if (g >= g0 + take) break;  // later rounds
+        r.todo &= r.todo - 1;
+        const float4 e = s.res[warp * 32 + (g - g0)];
+        const int cnd = word * 32 + i;
+        const double t = __ldg(p.ts + cnd);
+        const double delta = (cnd + 1 < p.n) ? dsub(__ldg(p.ts + cnd + 1), t) : dmul(t, dsub(p.ratio, 1.0));
+        const double a = dsub(1.0, exp(dmul(-(double)e.x, delta)));
+        const double wgt = dmul(r.trans, a);
+        r.px = dadd(r.px, dmul(wgt, (double)e.y));
+        r.py = dadd(r.py, dmul(wgt, (double)e.z));
+        r.pz = dadd(r.pz, dmul(wgt, (double)e.w));
+        r.depth = dadd(r.depth, dmul(wgt, t));
+        r.opac = dadd(r.opac, wgt);
+        r.trans = dmul(r.trans, dsub(1.0, a));
+        ++r.contributing;
+        if (p.t_cut > 0 && r.trans < p.t_cut) {
+          r.term = true;
+          r.alive = false;
+          r.todo = 0;
+          break;
+        }
+      }
+    }
+    cnt.evals += have ? 1u : 0u;
+    __syncthreads();  // res[] and the A tile are rewritten next round
+  }
+
+  // ---- teardown --------------------------------------------------------------------------
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 0) ptx::tmem_dealloc<kTmemCols>(tmem);
+  add_work_stats(p, cnt.evals, cnt.level_samples, cnt.marched, cnt.rays);
+}
+
+}  // namespace pk
+}  // namespace lumi_dev
+
+using namespace lumi_dev;
+
+size_t render_pk_smem_bytes() { return sizeof(pk::Smem) + 1024; }
+
+// march pass over packet-ordered ray ids + the packet kernel
+cudaError_t launch_render_pk(RenderParams p, cudaStream_t s, int num_sms) {
+  const long long rays = (long long)(p.row_end - p.row_begin) * p.cam.width;
+  if (rays <= 0) return cudaSuccess;
+  static int blocks_per_sm = -1;
+  const size_t smem = render_pk_smem_bytes();
+  cudaError_t e;
+  if (blocks_per_sm < 0) {
+    if ((e = cudaFuncSetAttribute(pk::k_render_pk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem)) != cudaSuccess)
+      return e;
+    cudaFuncAttributes fa;
+    if ((e = cudaFuncGetAttributes(&fa, pk::k_render_pk)) != cudaSuccess) return e;
+    const int regs_per_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+    const int by_regs = 65536 / (regs_per_warp * (pk::kThreads / 32));
+    const int by_smem = (228 * 1024) / (int)(smem + 1024);
+    blocks_per_sm = std::max(1, std::min(by_regs, by_smem));
+    if (const char* cap = std::getenv("LUMI_MAX_CTAS"))
+      blocks_per_sm = std::max(1, std::min(blocks_per_sm, std::atoi(cap)));
+    const int carve = (int)std::ceil(100.0 * blocks_per_sm * (double)(smem + 1024) / (228.0 * 1024));
+    if ((e = cudaFuncSetAttribute(pk::k_render_pk, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  std::min(100, carve))) != cudaSuccess)
+      return e;
+    if (std::getenv("LUMI_DEBUG"))
+      std::fprintf(stderr, "[lumi] k_render_pk: %zu B smem, %d regs, %d CTAs/SM\n", smem,
+                   fa.numRegs, blocks_per_sm);
+  }
+  p.tile_w = pk::kPW;
+  p.tile_h = pk::kPH;
+  p.tiles_x = (p.cam.width + pk::kPW - 1) / pk::kPW;
+  const long long packets =
+      (long long)p.tiles_x * ((p.row_end - p.row_begin + pk::kPH - 1) / pk::kPH);
+  p.total_rays = packets * 32;
+  if (p.total_rays >= (1ll << 31)) return cudaErrorInvalidValue;
+  p.mask_words = (p.n + 31) / 32;
+  if ((e = cudaMallocAsync(&p.kept_mask, (size_t)p.total_rays * p.mask_words * 4, s)) != cudaSuccess)
+    return e;
+  if ((e = cudaMallocAsync(&p.kept_count, (size_t)p.total_rays * 2, s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(p.work_counter, 0, sizeof(unsigned int), s)) != cudaSuccess) return e;
+  // the march pass's work counters are reported by the packet kernel (per ray), not here
+  RenderParams pm = p;
+  pm.work_stats = nullptr;
+  if ((e = launch_march_mask(pm, s)) != cudaSuccess) return e;
+  const long long grid = std::min<long long>((long long)blocks_per_sm * num_sms, (packets + 3) / 4);
+  pk::k_render_pk<<<(unsigned)grid, pk::kThreads, smem, s>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  cudaFreeAsync(p.kept_mask, s);
+  cudaFreeAsync(p.kept_count, s);
+  return cudaGetLastError();
+}

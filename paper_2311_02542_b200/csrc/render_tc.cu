@@ -34,6 +34,11 @@ constexpr uint32_t kTmemCols = 64;
 #define LUMI_PPP 2
 #endif
 constexpr int kPPP = LUMI_PPP;  // gather pairs per lane per pass
+#ifdef LUMI_PHASE_TIMING
+// per-phase warp-cycles (instrumented builds only): advance, gather, CTA sync, MLP,
+// composite, round barrier
+__device__ unsigned long long g_phase_cycles[6];
+#endif
 
 // Every layer's K carries one extra 16-wide step whose first column is 1 in A and the bias
 // in B, so the tensor core adds the bias (fp16 x 1 into the fp32 accumulator).
@@ -165,10 +170,11 @@ __device__ __forceinline__ bool occupied(const RenderParams& p, d3 c) {
 // ray id (tile-major: 16x8 tiles, row-major inside a tile) -> pixel; false for the padding
 // ids of partial edge tiles
 __device__ __forceinline__ bool ray_pixel(const RenderParams& p, long long idx, int& x, int& y) {
-  const long long tile = idx / (kTileW * kTileH);
-  const int w = (int)(idx % (kTileW * kTileH));
-  x = (int)(tile % p.tiles_x) * kTileW + (w % kTileW);
-  y = p.row_begin + (int)(tile / p.tiles_x) * kTileH + w / kTileW;
+  const int tw = p.tile_w, th = p.tile_h;
+  const long long tile = idx / (tw * th);
+  const int w = (int)(idx % (tw * th));
+  x = (int)(tile % p.tiles_x) * tw + (w % tw);
+  y = p.row_begin + (int)(tile / p.tiles_x) * th + w / tw;
   return x < p.cam.width && y < p.row_end;
 }
 
@@ -309,6 +315,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
   r.id = -1;
   uint32_t phase = 0;
   const bool issuer = (tid == 0);
+#ifdef LUMI_PHASE_TIMING
+  long long pt[6] = {0, 0, 0, 0, 0, 0}, pt_last = clock64();
+#define PT_MARK(k)                          \
+  do {                                      \
+    const long long _t = clock64();         \
+    pt[k] += _t - pt_last;                  \
+    pt_last = _t;                           \
+  } while (0)
+#else
+#define PT_MARK(k) \
+  do {             \
+  } while (0)
+#endif
 
   for (;;) {
     // ---- A: every thread brings one kept sample (refilling finished rays) ------------------
@@ -322,6 +341,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
       }
       finish(p, r, cnt);
     }
+    __syncwarp();
+    PT_MARK(0);
     // ---- B: warp-cooperative hash-grid gather (grid.h:90-167) ------------------------------
     // The warp's 32 samples have different numbers of active LOD levels; their (sample,
     // level) pairs are listed level-major and dealt round-robin to the 32 lanes, so every
@@ -390,12 +411,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
       }
     }
     ptx::fence_async_smem();
+    __syncwarp();
+    PT_MARK(1);
     if (!__syncthreads_or(have)) {
       if (tid == 0) refill(p, s, total);
       __syncthreads();
       if (s.q_done && s.q_next >= s.q_end) break;
       continue;
     }
+    PT_MARK(2);
 
     float v[32];
     float sigma = 1.f;
@@ -484,6 +508,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
     } else {
       v[0] = v[1] = v[2] = 0.f;
     }
+    PT_MARK(3);
 
     // ---- C: front-to-back compositing (renderer.h:170-190), double ----------------------
     if (have) {
@@ -508,8 +533,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
         r.cut_limit = ((r.contributing + p.chunk - 1) / p.chunk) * p.chunk;
       }
     }
+    __syncwarp();
+    PT_MARK(4);
     if (tid == 0) refill(p, s, total);
     __syncthreads();
+    PT_MARK(5);
   }
 
   // ---- teardown --------------------------------------------------------------------------
@@ -518,6 +546,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
   ptx::tc_fence_after();
   if (warp == 0) ptx::tmem_dealloc<kTmemCols>(tmem);
   add_work_stats(p, cnt.evals, cnt.level_samples, cnt.marched, cnt.rays);
+#ifdef LUMI_PHASE_TIMING
+  if ((tid & 31) == 0)
+    for (int k = 0; k < 6; ++k) atomicAdd(&g_phase_cycles[k], (unsigned long long)pt[k]);
+#endif
+#undef PT_MARK
 }
 
 }  // namespace tc
@@ -584,12 +617,34 @@ cudaError_t launch_render_tc(RenderParams p, cudaStream_t s, int num_sms) {
     return e;
   if ((e = cudaMallocAsync(&p.kept_count, (size_t)p.total_rays * 2, s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(p.work_counter, 0, sizeof(unsigned int), s)) != cudaSuccess) return e;
-  tc::k_march_mask<<<(unsigned)((p.total_rays + 127) / 128), 128, 0, s>>>(p);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = launch_march_mask(p, s)) != cudaSuccess) return e;
   const long long grid = std::min<long long>((long long)blocks_per_sm * num_sms, tiles);
+#ifdef LUMI_PHASE_TIMING
+  unsigned long long zero6[6] = {0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbolAsync(tc::g_phase_cycles, zero6, sizeof(zero6), 0, cudaMemcpyHostToDevice, s);
+#endif
   tc::k_render_tc<<<(unsigned)grid, tc::kThreads, smem, s>>>(p);
+#ifdef LUMI_PHASE_TIMING
+  {
+    unsigned long long pc[6];
+    cudaMemcpyFromSymbolAsync(pc, tc::g_phase_cycles, sizeof(pc), 0, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double tot = 0;
+    for (int k = 0; k < 6; ++k) tot += (double)pc[k];
+    std::fprintf(stderr, "[lumi] phase warp-cycles %%: advance %.1f gather %.1f ctasync %.1f mlp %.1f "
+                 "composite %.1f roundbar %.1f\n", 100 * pc[0] / tot, 100 * pc[1] / tot,
+                 100 * pc[2] / tot, 100 * pc[3] / tot, 100 * pc[4] / tot, 100 * pc[5] / tot);
+  }
+#endif
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   cudaFreeAsync(p.kept_mask, s);
   cudaFreeAsync(p.kept_count, s);
+  return cudaGetLastError();
+}
+
+// The exact march pass (k_march_mask) over p.total_rays tile-ordered ray ids
+// (p.tile_w x p.tile_h tiles) into p.kept_mask / p.kept_count.
+cudaError_t launch_march_mask(const RenderParams& p, cudaStream_t s) {
+  tc::k_march_mask<<<(unsigned)((p.total_rays + 127) / 128), 128, 0, s>>>(p);
   return cudaGetLastError();
 }

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 import math
 import threading
 import weakref
@@ -278,12 +279,13 @@ class DeviceModel:
         self.h = h
         self.field_version = field.version
         self.grid_version = grid.version
-        self.kernel = "tc"
+        self.kernel = os.environ.get("LUMI_KERNEL", "tc")
         self._lock = threading.Lock()
 
     def set_kernel(self, kernel: str) -> None:
         """'tc' (persistent tcgen05 kernel, default) or 'simt' (fp32 CUDA-core cross-check)."""
-        k = {"tc": _abi.LUMI_KERNEL_TC, "simt": _abi.LUMI_KERNEL_SIMT}[kernel]
+        k = {"tc": _abi.LUMI_KERNEL_TC, "simt": _abi.LUMI_KERNEL_SIMT,
+             "packet": _abi.LUMI_KERNEL_PACKET}[kernel]
         check(_abi.lib().lumi_model_set_kernel(self.h, k))
         self.kernel = kernel
 
