@@ -325,7 +325,8 @@ def run_ours(args):
     evals, level_samples, candidates, rays = (float(x) for x in counters)
     # the tensor-core kernel gathers the fp16 copy of the table (32 B per level-sample), the
     # SIMT cross-check the reference fp32 layout (64 B)
-    bytes_per_ls = GATHER_BYTES_PER_LEVEL_SAMPLE // (2 if dm.kernel == "tc" else 1)
+    bytes_per_ls = GATHER_BYTES_PER_LEVEL_SAMPLE // (1 if dm.kernel == "simt" else 2)
+    kname = {"tc": "k_render_tc", "packet": "k_render_pk", "simt": "k_render_simt"}[dm.kernel]
     gather_bytes = level_samples * bytes_per_ls
     kernel_s = kernel_ms / 1000.0  # rank-0 render launches (this rank's share at N>1)
     frac_rank = 1.0 / world
@@ -359,7 +360,7 @@ def run_ours(args):
                    "eyes": cfg.eyes, "table_size": spec.table_size, "rays_per_frame": rays_frame,
                    "samples_per_ray": opts.samples_per_ray, "parallelism": f"rows{world}",
                    "l2": "inputs larger than L2 (hash table %.0f MB fp32)" % (field.grid_params.nbytes / 1e6),
-                   "kernel": dm.kernel},
+                   "kernel": kname},
         "fps": round(fps, 3),
         "render_ms_per_step": round(kernel_ms / args.steps, 3),  # rank-0 march+render span
         "work": {"evals_per_ray": round(evals / max(rays, 1), 3),
@@ -368,10 +369,10 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": None if achieved is None else round(achieved, 1),
                      "peak": hbm, "unit": "GB/s",
                      "frac": None if achieved is None else round(achieved / hbm, 4),
-                     "traffic": ncu_traffic("k_render_" + dm.kernel),
+                     "traffic": ncu_traffic(kname),
                      "algorithmic": f"{bytes_per_ls} B per active (w_l>0) level-sample: 8 corners "
                                     f"x 2 features x {bytes_per_ls // 16} B "
-                                    f"({'fp16 table copy' if dm.kernel == 'tc' else 'fp32 table'}); "
+                                    f"({'fp32 table' if dm.kernel == 'simt' else 'fp16 table copy'}); "
                                     f"{level_samples / max(world, 1):.3e} level-samples in "
                                     f"{kernel_ms:.1f} ms of render launches"},
         "roofline_mlp": {"bound": "tensor", "achieved": None if mlp_tflops is None else round(mlp_tflops, 2),

@@ -163,7 +163,7 @@ struct LumiModel {
   int occ_res = 0;
   unsigned int* d_counter = nullptr;  // kCounterSlots per-launch tile counters
   std::atomic<unsigned> counter_slot{0};
-  int kernel = LUMI_KERNEL_TC;
+  int kernel = LUMI_KERNEL_PACKET;
   int num_sms = 148;
   std::mutex mu;
   std::map<std::tuple<double, double, int>, std::pair<double*, double>> ts_cache;
@@ -388,7 +388,7 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
   if ((rc = lumi_model_set_occupancy(m, occ, occ_res))) return cleanup(rc);
   if (const char* k = std::getenv("LUMI_KERNEL")) {
     const std::string ks(k);
-    m->kernel = ks == "simt" ? LUMI_KERNEL_SIMT : ks == "packet" ? LUMI_KERNEL_PACKET : LUMI_KERNEL_TC;
+    m->kernel = ks == "simt" ? LUMI_KERNEL_SIMT : ks == "tc" ? LUMI_KERNEL_TC : LUMI_KERNEL_PACKET;
   }
   *out = m;
   return LUMI_OK;

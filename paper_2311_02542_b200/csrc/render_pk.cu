@@ -32,7 +32,9 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kPW = 8, kPH = 4;  // packet: 8 x 4 pixels = one warp of rays
 constexpr uint32_t kTmemCols = 64;
 
-struct __align__(1024) Smem {
+// UMMA no-swizzle operands need 16-byte alignment only; the struct is used straight from
+// the dynamic __shared__ array so every access compiles to LDS/STS (not generic LD/ST).
+struct __align__(16) Smem {
   uint8_t A[128 * 64 * 2];  // activations, K-major core-matrix tile (K <= 64)
   uint8_t W1[64 * 32 * 2];  // density L1  N=64 K=32
   uint8_t W2[32 * 64 * 2];  // density L2  N=32 (17 used) K=64
@@ -134,8 +136,8 @@ struct Counters {
 };
 
 __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned FULL = 0xffffffffu;
 
@@ -489,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
 
 using namespace lumi_dev;
 
-size_t render_pk_smem_bytes() { return sizeof(pk::Smem) + 1024; }
+size_t render_pk_smem_bytes() { return sizeof(pk::Smem); }
 
 // march pass over packet-ordered ray ids + the packet kernel
 cudaError_t launch_render_pk(RenderParams p, cudaStream_t s, int num_sms) {

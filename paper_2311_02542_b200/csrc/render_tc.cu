@@ -43,7 +43,7 @@ __device__ unsigned long long g_phase_cycles[6];
 // Every layer's K carries one extra 16-wide step whose first column is 1 in A and the bias
 // in B, so the tensor core adds the bias (fp16 x 1 into the fp32 accumulator).
 constexpr int kKb = 16;
-struct __align__(1024) Smem {
+struct __align__(16) Smem {  // used straight from the __shared__ array: LDS/STS, not LD/ST
   uint8_t A[128 * (64 + kKb) * 2];  // activations, K-major core-matrix tile (K <= 64+16)
   uint8_t W1[64 * (32 + kKb) * 2];  // density L1  N=64 K=32(+bias)
   uint8_t W2[32 * (64 + kKb) * 2];  // density L2  N=32 (17 used) K=64(+bias)
@@ -278,8 +278,8 @@ __device__ void refill(const RenderParams& p, Smem& s, int total) {
 }
 
 __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
 
   // ---- one-time setup: weights -> fp16 core-matrix tiles, biases, distances, TMEM --------
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_tc(RenderParams p) {
 
 using namespace lumi_dev;
 
-size_t render_tc_smem_bytes() { return sizeof(tc::Smem) + 1024; }
+size_t render_tc_smem_bytes() { return sizeof(tc::Smem); }
 
 cudaError_t launch_render_tc(RenderParams p, cudaStream_t s, int num_sms) {
   const long long rays = (long long)(p.row_end - p.row_begin) * p.cam.width;

@@ -108,7 +108,7 @@ class StereoFrameDriver:
         self.ev0.record()
         for eye, b, e in eye_bands(band.begin, band.end, self.S):
             self.dm.render_rows_async(cams[eye], self.opts, b, e, self._target(eye), stream)
-            self.launches += 2 if self.dm.kernel == "tc" else 1  # march pass + render
+            self.launches += 1 if self.dm.kernel == "simt" else 2  # march pass + render
         self.ev1.record()
 
     def gather_bands(self) -> None:

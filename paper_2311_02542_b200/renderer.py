@@ -279,7 +279,7 @@ class DeviceModel:
         self.h = h
         self.field_version = field.version
         self.grid_version = grid.version
-        self.kernel = os.environ.get("LUMI_KERNEL", "tc")
+        self.kernel = os.environ.get("LUMI_KERNEL", "packet")
         self._lock = threading.Lock()
 
     def set_kernel(self, kernel: str) -> None:

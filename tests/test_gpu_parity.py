@@ -149,7 +149,7 @@ def test_render_counts_vs_reference(lumi, torch_cuda, small, golden_c1):
     assert ev_match > 0.99 and co_match > 0.99
 
 
-@pytest.mark.parametrize("kernel", ["tc", "simt"])
+@pytest.mark.parametrize("kernel", ["packet", "tc", "simt"])
 def test_both_kernels_vs_reference_golden(lumi, torch_cuda, small, golden_c1, kernel):
     """The tcgen05 production kernel and the fp32 CUDA-core cross-check kernel."""
     cam = lumi.CameraModel.from_spec(scenes.pinhole(256, 256))
@@ -157,7 +157,7 @@ def test_both_kernels_vs_reference_golden(lumi, torch_cuda, small, golden_c1, ke
     try:
         out, _, opac, stats = _render(lumi, small["dm"], cam, lumi.RenderOptions())
     finally:
-        small["dm"].set_kernel("tc")
+        small["dm"].set_kernel("packet")
     err = np.abs(out - golden_c1["out"]).max()
     print(f"{kernel}: C1 max|dPQ|={err:.3e} PSNR={psnr(out, golden_c1['out']):.1f} dB")
     assert err <= (1e-6 if kernel == "simt" else PIX_TOL)
