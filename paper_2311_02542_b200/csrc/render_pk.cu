@@ -30,7 +30,13 @@ namespace pk {
 constexpr int kThreads = 128;  // UMMA M: 4 warps x 32 rows
 constexpr int kWarps = kThreads / 32;
 constexpr int kPW = 8, kPH = 4;  // packet: 8 x 4 pixels = one warp of rays
-constexpr uint32_t kTmemCols = 64;
+constexpr uint32_t kTmemCols = 128;  // [0,64): fp32 accumulators, [64,96): fp16 A operand
+constexpr uint32_t kAcol = 64;
+#ifdef LUMI_PHASE_TIMING
+// per-phase warp-cycles (instrumented builds only): fill, geometry, gather, CTA sync, MLP,
+// composite, round barrier
+__device__ unsigned long long g_phase_cycles_pk[7];
+#endif
 
 // UMMA no-swizzle operands need 16-byte alignment only; the struct is used straight from
 // the dynamic __shared__ array so every access compiles to LDS/STS (not generic LD/ST).
@@ -103,6 +109,34 @@ __device__ __forceinline__ void relu64_to_A(uint32_t t_lane, const float* bias, 
 #pragma unroll
     for (int j = 0; j < 4; ++j) st16(A, core_off(row, 4 * h + j, 8), pack8(v + 8 * j));
   }
+}
+
+template <int N, int K>
+__device__ __forceinline__ void issue_layer_ts(uint32_t a_tmem, const uint8_t* B, uint32_t d_tmem) {
+  constexpr uint32_t idesc = ptx::idesc_f16_f32<128, N>();
+  const uint32_t b = ptx::smem_addr(B);
+#pragma unroll
+  for (int kk = 0; kk < K / 16; ++kk)  // 16 fp16 of K = 8 TMEM columns per step
+    ptx::mma_f16_ts(d_tmem, a_tmem + kk * 8, ptx::make_smem_desc(b + kk * 256, 128, (K / 8) * 128),
+                    idesc, kk > 0 ? 1u : 0u);
+}
+
+// hidden-layer epilogue into TMEM: D row (64 fp32) + bias, ReLU, fp16 pairs -> the A columns
+// of this thread's lane for the next layer
+__device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, const float* bias, uint32_t a_lane) {
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    float v[16];
+    ptx::tmem_ld16(t_lane + 16 * h, v);
+    ptx::tmem_ld_wait();
+    uint32_t w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      w[j] = h2u(__floats2half2_rn(fmaxf(v[2 * j] + bias[16 * h + 2 * j], 0.f),
+                                   fmaxf(v[2 * j + 1] + bias[16 * h + 2 * j + 1], 0.f)));
+    ptx::tmem_st8(a_lane + 8 * h, w);
+  }
+  ptx::tmem_st_wait();
 }
 
 // position of the (k+1)-th set bit of m (k < popc(m))
@@ -187,6 +221,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
   int word_total = 0;  // samples in the word
   uint32_t phase = 0;
   const bool issuer = (tid == 0);
+#ifdef LUMI_PHASE_TIMING
+  long long pt[7] = {0, 0, 0, 0, 0, 0, 0}, pt_last = clock64();
+#define PT_MARK(k)                  \
+  do {                              \
+    __syncwarp();                   \
+    const long long _t = clock64(); \
+    pt[k] += _t - pt_last;          \
+    pt_last = _t;                   \
+  } while (0)
+#else
+#define PT_MARK(k) \
+  do {             \
+  } while (0)
+#endif
 
   for (;;) {
     // ---- A: this warp's 32 rows: the next samples of its packet stream --------------------
@@ -259,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
       g_next = 0;
       word_total = run;
     }
+    PT_MARK(0);
 
     // row lane: its (candidate, ray lane) and network-input geometry
     const bool have = lane < take;
@@ -299,6 +348,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
       cnt.level_samples += na;
     }
 
+    PT_MARK(1);
     // ---- B: warp-cooperative hash-grid gather, level-major (sample, level) pairs ----------
     {
       const uint4 zero = make_uint4(0, 0, 0, 0);
@@ -353,13 +403,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
       }
     }
     ptx::fence_async_smem();
+    PT_MARK(2);
     if (!__syncthreads_or(have)) {
       if (__syncthreads_and(no_more)) break;  // every warp's stream is exhausted
       continue;
     }
+    PT_MARK(3);
 
     // ---- MLP: five tcgen05 layers over the 128-row batch (field.h:106-137) -------------
     float v32[32];
+    // layer 1 reads the gathered features from shared memory (SS form); the hidden layers
+    // keep their fp16 activations in TMEM columns [kAcol, kAcol + K/2) as the A operand
+    // (TS form), so epilogues store with tcgen05.st and never touch shared memory.
+    const uint32_t a_tmem = tmem + kAcol;
+    const uint32_t a_lane = t_lane + kAcol;
     if (issuer) {
       ptx::tc_fence_after();
       issue_layer<64, 32>(s.A, s.W1, tmem);
@@ -368,14 +425,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-    relu64_to_A(t_lane, s.b1, s.A, tid);
-    ptx::fence_async_smem();
+    relu64_to_tmem(t_lane, s.b1, a_lane);
     ptx::tc_fence_before();
     __syncthreads();
 
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer<32, 64>(s.A, s.W2, tmem);
+      issue_layer_ts<32, 64>(a_tmem, s.W2, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
@@ -390,42 +446,42 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) cin[j] = v32[1 + j] + s.b2[1 + j];
       sh_encode(d3{(double)dx, (double)dy, (double)dz}, cin + 16);
+      uint32_t wv[16];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) st16(s.A, core_off(tid, j, 4), pack8(cin + 8 * j));
+      for (int j = 0; j < 16; ++j) wv[j] = h2u(__floats2half2_rn(cin[2 * j], cin[2 * j + 1]));
+      ptx::tmem_st16(a_lane, wv);
+      ptx::tmem_st_wait();
     }
-    ptx::fence_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
 
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer<64, 32>(s.A, s.C1, tmem);
+      issue_layer_ts<64, 32>(a_tmem, s.C1, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-    relu64_to_A(t_lane, s.cb1, s.A, tid);
-    ptx::fence_async_smem();
+    relu64_to_tmem(t_lane, s.cb1, a_lane);
     ptx::tc_fence_before();
     __syncthreads();
 
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer<64, 64>(s.A, s.C2, tmem);
+      issue_layer_ts<64, 64>(a_tmem, s.C2, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-    relu64_to_A(t_lane, s.cb2, s.A, tid);
-    ptx::fence_async_smem();
+    relu64_to_tmem(t_lane, s.cb2, a_lane);
     ptx::tc_fence_before();
     __syncthreads();
 
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer<16, 64>(s.A, s.C3, tmem);
+      issue_layer_ts<16, 64>(a_tmem, s.C3, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
@@ -445,6 +501,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     }
     __syncwarp();
 
+    PT_MARK(4);
     // ---- C: owners composite their samples of this round, in order (renderer.h:170-190) ---
     if (r.alive && take > 0) {
       const unsigned lt = (1u << lane) - 1u;
@@ -475,7 +532,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
       }
     }
     cnt.evals += have ? 1u : 0u;
+    PT_MARK(5);
     __syncthreads();  // res[] and the A tile are rewritten next round
+    PT_MARK(6);
   }
 
   // ---- teardown --------------------------------------------------------------------------
@@ -484,6 +543,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
   ptx::tc_fence_after();
   if (warp == 0) ptx::tmem_dealloc<kTmemCols>(tmem);
   add_work_stats(p, cnt.evals, cnt.level_samples, cnt.marched, cnt.rays);
+#ifdef LUMI_PHASE_TIMING
+  if (lane == 0)
+    for (int k = 0; k < 7; ++k) atomicAdd(&g_phase_cycles_pk[k], (unsigned long long)pt[k]);
+#endif
+#undef PT_MARK
 }
 
 }  // namespace pk
@@ -537,7 +601,24 @@ cudaError_t launch_render_pk(RenderParams p, cudaStream_t s, int num_sms) {
   pm.work_stats = nullptr;
   if ((e = launch_march_mask(pm, s)) != cudaSuccess) return e;
   const long long grid = std::min<long long>((long long)blocks_per_sm * num_sms, (packets + 3) / 4);
+#ifdef LUMI_PHASE_TIMING
+  unsigned long long zero7[7] = {0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbolAsync(pk::g_phase_cycles_pk, zero7, sizeof(zero7), 0, cudaMemcpyHostToDevice, s);
+#endif
   pk::k_render_pk<<<(unsigned)grid, pk::kThreads, smem, s>>>(p);
+#ifdef LUMI_PHASE_TIMING
+  {
+    unsigned long long pc[7];
+    cudaMemcpyFromSymbolAsync(pc, pk::g_phase_cycles_pk, sizeof(pc), 0, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double tot = 0;
+    for (int k = 0; k < 7; ++k) tot += (double)pc[k];
+    std::fprintf(stderr, "[lumi] pk phase %%: fill %.1f geom %.1f gather %.1f ctasync %.1f mlp %.1f "
+                 "composite %.1f roundbar %.1f\n", 100 * pc[0] / tot, 100 * pc[1] / tot,
+                 100 * pc[2] / tot, 100 * pc[3] / tot, 100 * pc[4] / tot, 100 * pc[5] / tot,
+                 100 * pc[6] / tot);
+  }
+#endif
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   cudaFreeAsync(p.kept_mask, s);
   cudaFreeAsync(p.kept_count, s);
