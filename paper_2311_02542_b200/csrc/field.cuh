@@ -161,6 +161,38 @@ __device__ __forceinline__ float2 encode_level_h(const GridDev& g, const __half2
   return make_float2(a0 * wl, a1 * wl);
 }
 
+// encode_level_h with fp32 grid coordinates (u, v, s in [0, 1]): cell index and fractions from
+// one FMUL per axis (the fraction pu - floor(pu) is exact in fp32).  Interpolation is
+// continuous across cells, so a boundary flip from the 2^-24 coordinate rounding moves the
+// feature by O(2^-24 * res) -- far below the fp16 weights that follow.
+__device__ __forceinline__ float2 encode_level_hf(const GridDev& g, const __half2* __restrict__ t16,
+                                                  int l, float u, float v, float s, float wl) {
+  const int res = g.res[l];
+  const float r = (float)res;
+  const float pu = u * r, pv = v * r, ps = s * r;
+  const int iu = min((int)pu, res - 1), iv = min((int)pv, res - 1), is = min((int)ps, res - 1);
+  uint32_t idx[8];
+  corner_indices((g.dense_mask >> l) & 1u, iu, iv, is, (uint32_t)res + 1u, g.hash_mask[l], idx);
+  const __half2* base = t16 + g.offset2[l];
+  __half2 e[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) e[k] = __ldg(base + idx[k]);
+  const float fu = pu - (float)iu, fv = pv - (float)iv, fs = ps - (float)is;
+  const __half2 hu = __floats2half2_rn(1.f - fu, fu);
+  const __half2 w0 = __hmul2(hu, __float2half2_rn(1.f - fv));
+  const __half2 w1 = __hmul2(hu, __float2half2_rn(fv));
+  const __half2 gs2 = __float2half2_rn(1.f - fs), fs2 = __float2half2_rn(fs);
+  const __half2 t[4] = {__hmul2(w0, gs2), __hmul2(w1, gs2), __hmul2(w0, fs2), __hmul2(w1, fs2)};
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const __half tri = (k & 1) ? __high2half(t[k >> 1]) : __low2half(t[k >> 1]);
+    a0 = fma_f32_f16(tri, __low2half(e[k]), a0);
+    a1 = fma_f32_f16(tri, __high2half(e[k]), a1);
+  }
+  return make_float2(a0 * wl, a1 * wl);
+}
+
 // Full encode of one contracted point into 2*levels features (zero for masked levels,
 // which touch no memory -- grid.h:98-101).
 __device__ __forceinline__ void encode(const GridDev& g, d3 c, const LodW& lw, float* feat) {

@@ -32,6 +32,10 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kPW = 8, kPH = 4;  // packet: 8 x 4 pixels = one warp of rays
 constexpr uint32_t kTmemCols = 128;  // [0,64): fp32 accumulators, [64,96): fp16 A operand
 constexpr uint32_t kAcol = 64;
+#ifndef LUMI_PK_PAIRS
+#define LUMI_PK_PAIRS 2
+#endif
+constexpr int kPairs = LUMI_PK_PAIRS;  // (sample, level) pairs per lane per gather step
 #ifdef LUMI_PHASE_TIMING
 // per-phase warp-cycles (instrumented builds only): fill, geometry, gather, CTA sync, MLP,
 // composite, round barrier
@@ -326,15 +330,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     const float nx = __shfl_sync(FULL, r.nd.x, rl), ny = __shfl_sync(FULL, r.nd.y, rl),
                 nz = __shfl_sync(FULL, r.nd.z, rl);
     const int cand = word * 32 + ci;
-    double u = 0.0, v = 0.0, w = 0.0;
+    float u = 0.f, v = 0.f, w = 0.f;
     LodW lw{0, 0.f, false};
     int na = 0;
     if (have) {
       const float t = (float)__ldg(p.ts + cand);
       const float3 c = contract_f(make_float3(o.x + dx * t, o.y + dy * t, o.z + dz * t), p.contraction);
-      u = clamp01(((double)c.x + 2.0) * 0.25);
-      v = clamp01(((double)c.y + 2.0) * 0.25);
-      w = clamp01(((double)c.z + 2.0) * 0.25);
+      u = __saturatef((c.x + 2.f) * 0.25f);
+      v = __saturatef((c.y + 2.f) * 0.25f);
+      w = __saturatef((c.z + 2.f) * 0.25f);
       if (p.lod_enabled) {
         const float3 b = contract_f(make_float3(o.x + nx * t, o.y + ny * t, o.z + nz * t), p.contraction);
         const float ex = c.x - b.x, ey = c.y - b.y, ez = c.z - b.z;
@@ -370,13 +374,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
       __syncwarp();
       const uint8_t* Abase = s.A + (warp * 32 / 8) * (4 * 128);
 #pragma unroll 1
-      for (int base = 0; base < npairs; base += 64) {
-        int src[2], lv[2];
-        bool ok[2];
-        double su[2], sv[2], sw[2];
-        float wl[2];
+      for (int base = 0; base < npairs; base += 32 * kPairs) {
+        int src[kPairs], lv[kPairs];
+        bool ok[kPairs];
+        float su[kPairs], sv[kPairs], sw[kPairs];
+        float wl[kPairs];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < kPairs; ++q) {
           const int pi = base + 32 * q + lane;
           ok[q] = pi < npairs;
           src[q] = ok[q] ? psrc[pi] : lane;
@@ -390,13 +394,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
           lq.floor_only = __shfl_sync(FULL, (int)lw.floor_only, src[q]) != 0;
           wl[q] = lod_weight_at(lq, lv[q]);
         }
-        float2 f[2];
+        float2 f[kPairs];
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
-          f[q] = ok[q] ? encode_level_h(p.grid, p.grid.table16, lv[q], su[q], sv[q], sw[q], wl[q])
+        for (int q = 0; q < kPairs; ++q)
+          f[q] = ok[q] ? encode_level_hf(p.grid, p.grid.table16, lv[q], su[q], sv[q], sw[q], wl[q])
                        : make_float2(0.f, 0.f);
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
+        for (int q = 0; q < kPairs; ++q)
           if (ok[q])
             *reinterpret_cast<__half2*>(const_cast<uint8_t*>(Abase) + core_off(src[q], lv[q] >> 2, 4) +
                                         (lv[q] & 3) * 4) = __floats2half2_rn(f[q].x, f[q].y);
