@@ -354,6 +354,8 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
   int rc = lumi_field_layout(desc, &lay);
   if (rc) return rc;
   if (!table || !dparams || !cparams) return fail(LUMI_ERR_INVALID, "null parameter buffer");
+  if (lay.total_floats / 2 >= (1ull << 32))  // the gather indexes table pairs with 32 bits
+    return fail(LUMI_ERR_INVALID, "hash-grid table exceeds 2^32 feature pairs");
   int ndev = 0;
   LUMI_CUDA_TRY(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(LUMI_ERR_CUDA, "no such CUDA device");

@@ -45,7 +45,7 @@ __device__ unsigned long long g_phase_cycles_pk[7];
 // UMMA no-swizzle operands need 16-byte alignment only; the struct is used straight from
 // the dynamic __shared__ array so every access compiles to LDS/STS (not generic LD/ST).
 struct __align__(16) Smem {
-  uint8_t A[128 * 64 * 2];  // activations, K-major core-matrix tile (K <= 64)
+  uint8_t A[128 * 32 * 2];  // layer-1 input: hash-grid features, K-major core-matrix tile
   uint8_t W1[64 * 32 * 2];  // density L1  N=64 K=32
   uint8_t W2[32 * 64 * 2];  // density L2  N=32 (17 used) K=64
   uint8_t C1[64 * 32 * 2];  // colour L1   N=64 K=32
@@ -57,8 +57,9 @@ struct __align__(16) Smem {
   uint16_t prefix[kWarps][33];   // exclusive prefix of popc(ballot[i])
   uint64_t mbar;
   uint32_t tmem_base;
-  uint8_t pair_src[kWarps][32 * kMaxLevels];
-  uint8_t pair_lvl[kWarps][32 * kMaxLevels];
+  uint4 lvl[kMaxLevels];         // per level: res, hash mask (0 = dense), pair offset, (float)res
+  float4 samp[kWarps][32];       // per row: grid coordinates u, v, w and the LOD fraction
+  uint16_t pairs[kWarps][32 * kMaxLevels];  // (sample, level) gather list: row | l<<5 | class<<9
 };
 
 __device__ __forceinline__ uint32_t core_off(int row, int chunk, int kchunks) {
@@ -99,22 +100,6 @@ __device__ __forceinline__ void issue_layer(const uint8_t* A, const uint8_t* B, 
                  ptx::make_smem_desc(b + kk * 256, 128, (K / 8) * 128), idesc, kk > 0 ? 1u : 0u);
 }
 
-// hidden-layer epilogue: TMEM row + bias, ReLU, fp16 -> this row of the next A tile (K = 64)
-__device__ __forceinline__ void relu64_to_A(uint32_t t_lane, const float* bias, uint8_t* A,
-                                            int row) {
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    float v[32];
-    ptx::tmem_ld16(t_lane + 32 * h, v);
-    ptx::tmem_ld16(t_lane + 32 * h + 16, v + 16);
-    ptx::tmem_ld_wait();
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + bias[32 * h + j], 0.f);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) st16(A, core_off(row, 4 * h + j, 8), pack8(v + 8 * j));
-  }
-}
-
 template <int N, int K>
 __device__ __forceinline__ void issue_layer_ts(uint32_t a_tmem, const uint8_t* B, uint32_t d_tmem) {
   constexpr uint32_t idesc = ptx::idesc_f16_f32<128, N>();
@@ -141,6 +126,36 @@ __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, const float* bia
     ptx::tmem_st8(a_lane + 8 * h, w);
   }
   ptx::tmem_st_wait();
+}
+
+// One hash-grid level of one sample from the fp16 table (grid.h:96-113, 144-167): fp32 grid
+// coordinates, 32-bit entry indices off the level's pair offset, fp16 trilinear weights
+// (HMUL2) accumulated in fp32 by FHFMA in two interleaved chains per feature.
+__device__ __forceinline__ float2 gather_level(const __half2* __restrict__ t16, uint4 L, float u,
+                                               float v, float s, float wl) {
+  const int res = (int)L.x;
+  const float r = __uint_as_float(L.w);
+  const float pu = u * r, pv = v * r, ps = s * r;
+  const int iu = min((int)pu, res - 1), iv = min((int)pv, res - 1), is = min((int)ps, res - 1);
+  uint32_t idx[8];
+  corner_indices(L.y == 0u, iu, iv, is, (uint32_t)res + 1u, L.y, idx);
+  __half2 e[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) e[k] = __ldg(t16 + (L.z + idx[k]));
+  const float fu = pu - (float)iu, fv = pv - (float)iv, fs = ps - (float)is;
+  const __half2 hu = __floats2half2_rn(1.f - fu, fu);
+  const __half2 w0 = __hmul2(hu, __float2half2_rn(1.f - fv));
+  const __half2 w1 = __hmul2(hu, __float2half2_rn(fv));
+  const __half2 gs2 = __float2half2_rn(1.f - fs), fs2 = __float2half2_rn(fs);
+  const __half2 t[4] = {__hmul2(w0, gs2), __hmul2(w1, gs2), __hmul2(w0, fs2), __hmul2(w1, fs2)};
+  float a[2] = {0.f, 0.f}, b[2] = {0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const __half tri = (k & 1) ? __high2half(t[k >> 1]) : __low2half(t[k >> 1]);
+    a[k & 1] = fma_f32_f16(tri, __low2half(e[k]), a[k & 1]);
+    b[k & 1] = fma_f32_f16(tri, __high2half(e[k]), b[k & 1]);
+  }
+  return make_float2((a[0] + a[1]) * wl, (b[0] + b[1]) * wl);
 }
 
 // position of the (k+1)-th set bit of m (k < popc(m))
@@ -197,6 +212,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
   }
   for (int i = tid; i < 32; i += kThreads) s.b2[i] = i < 17 ? d2[17 * 64 + i] : 0.f;
   for (int i = tid; i < 16; i += kThreads) s.cb3[i] = i < 3 ? c3[3 * 64 + i] : 0.f;
+  for (int l = tid; l < kMaxLevels; l += kThreads) {
+    const int res = l < p.grid.levels ? p.grid.res[l] : 1;
+    const bool dense = (p.grid.dense_mask >> l) & 1u;
+    s.lvl[l] = make_uint4((uint32_t)res, dense ? 0u : p.grid.hash_mask[l],
+                          (uint32_t)p.grid.offset2[l], __float_as_uint((float)res));
+  }
   if (tid == 0) {
     ptx::mbar_init(&s.mbar, 1);
     ptx::fence_mbar_init();
@@ -358,52 +379,47 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
       const uint4 zero = make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int j = 0; j < 4; ++j) st16(s.A, core_off(tid, j, 4), zero);
-      uint8_t* psrc = s.pair_src[warp];
-      uint8_t* plvl = s.pair_lvl[warp];
+      if (have) s.samp[warp][lane] = make_float4(u, v, w, lw.frac);
+      uint16_t* pc = s.pairs[warp];
       const unsigned lt = (1u << lane) - 1u;
       int npairs = 0;
       for (int l = 0; l < levels; ++l) {
         const unsigned m = __ballot_sync(FULL, na > l);
+        if (m == 0u) break;  // active levels are a prefix [0, na)
         if (na > l) {
-          const int at = npairs + __popc(m & lt);
-          psrc[at] = (uint8_t)lane;
-          plvl[at] = (uint8_t)l;
+          const uint32_t cls = lw.floor_only ? 2u : (l < lw.full ? 0u : 1u);
+          pc[npairs + __popc(m & lt)] = (uint16_t)(lane | (l << 5) | (cls << 9));
         }
         npairs += __popc(m);
       }
       __syncwarp();
-      const uint8_t* Abase = s.A + (warp * 32 / 8) * (4 * 128);
+      uint8_t* Abase = s.A + (warp * 32 / 8) * (4 * 128);
 #pragma unroll 1
       for (int base = 0; base < npairs; base += 32 * kPairs) {
-        int src[kPairs], lv[kPairs];
-        bool ok[kPairs];
-        float su[kPairs], sv[kPairs], sw[kPairs];
-        float wl[kPairs];
+        uint32_t code[kPairs];
+        float2 f[kPairs];
 #pragma unroll
         for (int q = 0; q < kPairs; ++q) {
           const int pi = base + 32 * q + lane;
-          ok[q] = pi < npairs;
-          src[q] = ok[q] ? psrc[pi] : lane;
-          lv[q] = ok[q] ? plvl[pi] : 0;
-          su[q] = __shfl_sync(FULL, u, src[q]);
-          sv[q] = __shfl_sync(FULL, v, src[q]);
-          sw[q] = __shfl_sync(FULL, w, src[q]);
-          LodW lq;
-          lq.full = __shfl_sync(FULL, lw.full, src[q]);
-          lq.frac = __shfl_sync(FULL, lw.frac, src[q]);
-          lq.floor_only = __shfl_sync(FULL, (int)lw.floor_only, src[q]) != 0;
-          wl[q] = lod_weight_at(lq, lv[q]);
+          code[q] = pi < npairs ? (uint32_t)pc[pi] : 0xffffu;
         }
-        float2 f[kPairs];
+#pragma unroll
+        for (int q = 0; q < kPairs; ++q) {
+          f[q] = make_float2(0.f, 0.f);
+          if (code[q] != 0xffffu) {
+            const float4 P = s.samp[warp][code[q] & 31u];
+            const uint32_t cls = code[q] >> 9;
+            const float wl = cls == 0u ? 1.f : (cls == 1u ? P.w : 1e-4f);
+            f[q] = gather_level(p.grid.table16, s.lvl[(code[q] >> 5) & 15u], P.x, P.y, P.z, wl);
+          }
+        }
 #pragma unroll
         for (int q = 0; q < kPairs; ++q)
-          f[q] = ok[q] ? encode_level_hf(p.grid, p.grid.table16, lv[q], su[q], sv[q], sw[q], wl[q])
-                       : make_float2(0.f, 0.f);
-#pragma unroll
-        for (int q = 0; q < kPairs; ++q)
-          if (ok[q])
-            *reinterpret_cast<__half2*>(const_cast<uint8_t*>(Abase) + core_off(src[q], lv[q] >> 2, 4) +
-                                        (lv[q] & 3) * 4) = __floats2half2_rn(f[q].x, f[q].y);
+          if (code[q] != 0xffffu) {
+            const int src = code[q] & 31u, lv = (code[q] >> 5) & 15u;
+            *reinterpret_cast<__half2*>(Abase + core_off(src, lv >> 2, 4) + (lv & 3) * 4) =
+                __floats2half2_rn(f[q].x, f[q].y);
+          }
       }
     }
     ptx::fence_async_smem();
