@@ -465,7 +465,12 @@ int lumi_march_kept_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRen
   RenderParams p;
   int rc = make_params(m, cam, o, b, e, &p);
   if (rc) return rc;
-  LUMI_CUDA_TRY(launch_march_kept(p, mask, counts, static_cast<cudaStream_t>(stream)));
+  // the SIMT cross-check model marches exactly per ray; the tensor-core renderers consume the
+  // filtered mask pass, which is what this entry point then reports
+  if (m->kernel == LUMI_KERNEL_SIMT)
+    LUMI_CUDA_TRY(launch_march_kept(p, mask, counts, static_cast<cudaStream_t>(stream)));
+  else
+    LUMI_CUDA_TRY(launch_march_public(p, mask, counts, static_cast<cudaStream_t>(stream)));
   return LUMI_OK;
 }
 

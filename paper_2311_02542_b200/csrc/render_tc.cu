@@ -265,6 +265,129 @@ __global__ void __launch_bounds__(128) k_march_mask(RenderParams p) {
   add_work_stats(p, 0, 0, valid ? (unsigned long long)p.n : 0ull, 0);
 }
 
+// Filtered march pass: the same kept bitmask, decided in fp32 with a certified error bound
+// and the exact double test only where fp32 cannot decide.
+//
+// x = o + d t in fp32 differs from the exact value by at most ex = 8 * 2^-24 * (|o| + t)
+// (o, d, t rounded to fp32 plus one FMA rounding, 2x slack).  The contraction
+// (camera.cpp:34-49) is 1-Lipschitz up to 2/max(1, m), so the contracted point is off by at
+// most ec = 2 ex / max(1, m) + 2^-21 (reciprocal and product roundings), and the voxel
+// coordinate g = (c + 2) * res / 4 by eg = res/4 * ec + res * 2^-23.  If every axis of g is
+// further than 4 eg from an integer, floor(g) -- hence the voxel and its occupancy bit, and
+// the domain test for the uncontracted mode -- equals the double computation's.  The
+// contraction's max-axis choice is discontinuous at ties (|x_i| == |x_j| == m), so a second
+// axis within 4 ex of the max is also undecided.  ~1e-3 of candidates are undecided; the
+// warp re-tests them cooperatively in double (below), so a rare fallback never serialises
+// a whole warp behind one lane.
+// Returns 0 (empty), 1 (occupied) or 2 (undecided in fp32).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ int occupied_filtered(const RenderParams& p, float3 of, float3 df,
+                                                 float onorm, float tf) {
+  const float x = fmaf(df.x, tf, of.x), y = fmaf(df.y, tf, of.y), z = fmaf(df.z, tf, of.z);
+  const float ax = fabsf(x), ay = fabsf(y), az = fabsf(z);
+  const float m = fmaxf(ax, fmaxf(ay, az));
+  const float ex = 4.76837158e-07f * (onorm + tf);  // 8 * 2^-24 * (|o| + t)
+  const bool contract = p.contraction != 0 && m > 1.f;
+  const float inv = contract ? rcp_approx(m) : 1.f;  // ~1 ulp, inside the 2^-21 term
+  const float mapped = 2.f - inv;
+  // the reference maps the FIRST axis with |x_i| == m (camera.cpp:42-47)
+  const bool isx = ax == m, isy = !isx && ay == m, isz = !isx && !isy;
+  const float cx = contract && isx ? copysignf(mapped, x) : x * inv;
+  const float cy = contract && isy ? copysignf(mapped, y) : y * inv;
+  const float cz = contract && isz ? copysignf(mapped, z) : z * inv;
+  const float m2 = isx ? fmaxf(ay, az) : (isy ? fmaxf(ax, az) : fmaxf(ax, ay));
+  const float res = (float)p.occ_res, q = 0.25f * res;
+  const float ec = 2.f * ex * inv + 4.76837158e-07f;
+  const float eps = 4.f * (q * ec + res * 1.1920929e-07f);
+  const float gx = fmaf(cx, q, 2.f * q), gy = fmaf(cy, q, 2.f * q), gz = fmaf(cz, q, 2.f * q);
+  // Rounding by the 1.5 * 2^23 magic constant keeps the whole test on the FMA/ALU pipes
+  // (no FRND/F2I on the narrow XU pipe): |g - rint(g)| is the distance to the nearest voxel
+  // boundary, and rint(g - 1/2) = floor(g) for every certified g.
+  constexpr float kMagic = 12582912.f;
+  const float rx = __fsub_rn(__fadd_rn(gx, kMagic), kMagic), ry = __fsub_rn(__fadd_rn(gy, kMagic), kMagic),
+              rz = __fsub_rn(__fadd_rn(gz, kMagic), kMagic);
+  const float dmin = fminf(fabsf(gx - rx), fminf(fabsf(gy - ry), fabsf(gz - rz)));
+  if (dmin <= eps || (contract && m - m2 <= 4.f * ex)) return 2;
+  if (fminf(gx, fminf(gy, gz)) < 0.f || fmaxf(gx, fmaxf(gy, gz)) > res) return 0;
+  const uint32_t r = (uint32_t)p.occ_res;  // res^3 < 2^32 (checked on the host)
+  const uint32_t ix = (uint32_t)(__float_as_int(__fadd_rn(gx - 0.5f, kMagic)) - 0x4B400000),
+                 iy = (uint32_t)(__float_as_int(__fadd_rn(gy - 0.5f, kMagic)) - 0x4B400000),
+                 iz = (uint32_t)(__float_as_int(__fadd_rn(gz - 0.5f, kMagic)) - 0x4B400000);
+  return __ldg(p.occ + ((iz * r + iy) * r + ix)) != 0 ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(128) k_march_mask_fast(RenderParams p) {
+  __shared__ double s_ts[kMaxSamples];
+  __shared__ float s_tf[kMaxSamples];
+  __shared__ double s_dir[4][32][3];        // per lane: exact direction (undecided re-tests)
+  __shared__ uint16_t s_queue[4][32 * 32];  // per warp: undecided (lane, bit) of one word
+  __shared__ uint32_t s_add[4][32];         // per lane: bits confirmed by the re-test
+  for (int i = threadIdx.x; i < p.n; i += blockDim.x) {
+    s_ts[i] = p.ts[i];
+    s_tf[i] = (float)p.ts[i];
+  }
+  __syncthreads();
+  const unsigned FULL = 0xffffffffu;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int x = 0, y = 0;
+  const bool valid = idx < p.total_rays && ray_pixel(p, idx, x, y);
+  const d3 o{p.cam.origin[0], p.cam.origin[1], p.cam.origin[2]};
+  const d3 d = valid ? ray_dir(p.cam, (double)x + 0.5, (double)y + 0.5) : d3{0, 0, 1};
+  s_dir[warp][lane][0] = d.x;
+  s_dir[warp][lane][1] = d.y;
+  s_dir[warp][lane][2] = d.z;
+  const float3 of = make_float3((float)o.x, (float)o.y, (float)o.z);
+  const float3 df = make_float3((float)d.x, (float)d.y, (float)d.z);
+  const float onorm = fabsf(of.x) + fabsf(of.y) + fabsf(of.z);
+  int count = 0;
+  for (int w0 = 0; w0 < p.mask_words; ++w0) {
+    uint32_t bits = 0, unsure = 0;
+    if (valid) {
+      const int hi = min(32, p.n - w0 * 32);
+#pragma unroll 4
+      for (int b = 0; b < hi; ++b) {
+        const int r = occupied_filtered(p, of, df, onorm, s_tf[w0 * 32 + b]);
+        bits |= (uint32_t)(r & 1) << b;
+        unsure |= (uint32_t)(r >> 1) << b;
+      }
+    }
+    // undecided candidates of the whole warp, re-tested exactly one per lane
+    if (__any_sync(FULL, unsure != 0)) {
+      const int mine = __popc(unsure);
+      int incl = mine;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(FULL, incl, off);
+        if (lane >= off) incl += v;
+      }
+      const int total = __shfl_sync(FULL, incl, 31);
+      int at = incl - mine;
+      for (uint32_t u = unsure; u; u &= u - 1) s_queue[warp][at++] = (uint16_t)(lane << 5 | (__ffs(u) - 1));
+      s_add[warp][lane] = 0;
+      __syncwarp();
+      for (int j = lane; j < total; j += 32) {
+        const int e = s_queue[warp][j], ol = e >> 5, b = e & 31;
+        const d3 od{s_dir[warp][ol][0], s_dir[warp][ol][1], s_dir[warp][ol][2]};
+        if (occupied(p, contract(ray_at(o, od, s_ts[w0 * 32 + b]), p.contraction)))
+          atomicOr(&s_add[warp][ol], 1u << b);
+      }
+      __syncwarp();
+      bits |= s_add[warp][lane];
+      __syncwarp();
+    }
+    count += __popc(bits);
+    if (idx < p.total_rays) p.kept_mask[(size_t)w0 * p.total_rays + idx] = bits;
+  }
+  if (idx < p.total_rays) p.kept_count[idx] = (uint16_t)count;
+  add_work_stats(p, 0, 0, valid ? (unsigned long long)p.n : 0ull, 0);
+}
+
 __device__ void refill(const RenderParams& p, Smem& s, int total) {
   if (s.q_next < s.q_end || s.q_done) return;
   const int base = (int)atomicAdd(p.work_counter, (unsigned)(kTileW * kTileH));
@@ -645,6 +768,46 @@ cudaError_t launch_render_tc(RenderParams p, cudaStream_t s, int num_sms) {
 // The exact march pass (k_march_mask) over p.total_rays tile-ordered ray ids
 // (p.tile_w x p.tile_h tiles) into p.kept_mask / p.kept_count.
 cudaError_t launch_march_mask(const RenderParams& p, cudaStream_t s) {
-  tc::k_march_mask<<<(unsigned)((p.total_rays + 127) / 128), 128, 0, s>>>(p);
+  static const bool exact = std::getenv("LUMI_MARCH_EXACT") != nullptr;  // A/B and tests
+  if (exact)
+    tc::k_march_mask<<<(unsigned)((p.total_rays + 127) / 128), 128, 0, s>>>(p);
+  else
+    tc::k_march_mask_fast<<<(unsigned)((p.total_rays + 127) / 128), 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+namespace lumi_dev {
+namespace tc {
+// [word][ray] production mask (row-major ray ids) -> the public [pixel][word] layout
+__global__ void k_unpack_kept(RenderParams p, uint32_t* mask, int32_t* counts) {
+  const long long ray = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ray >= p.total_rays) return;
+  const size_t pix = (size_t)p.row_begin * p.cam.width + ray;
+  if (mask)
+    for (int w = 0; w < p.mask_words; ++w)
+      mask[pix * p.mask_words + w] = p.kept_mask[(size_t)w * p.total_rays + ray];
+  if (counts) counts[pix] = p.kept_count[ray];
+}
+}  // namespace tc
+}  // namespace lumi_dev
+
+// lumi_march_kept_async through the production march pass (the one the renderers consume)
+cudaError_t launch_march_public(RenderParams p, uint32_t* mask, int32_t* counts, cudaStream_t s) {
+  const long long rays = (long long)(p.row_end - p.row_begin) * p.cam.width;
+  if (rays <= 0) return cudaSuccess;
+  p.tile_w = p.cam.width;
+  p.tile_h = 1;
+  p.tiles_x = 1;
+  p.total_rays = rays;
+  p.mask_words = (p.n + 31) / 32;
+  p.work_stats = nullptr;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&p.kept_mask, (size_t)rays * p.mask_words * 4, s)) != cudaSuccess) return e;
+  if ((e = cudaMallocAsync(&p.kept_count, (size_t)rays * 2, s)) != cudaSuccess) return e;
+  if ((e = launch_march_mask(p, s)) != cudaSuccess) return e;
+  tc::k_unpack_kept<<<(unsigned)((rays + 127) / 128), 128, 0, s>>>(p, mask, counts);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  cudaFreeAsync(p.kept_mask, s);
+  cudaFreeAsync(p.kept_count, s);
   return cudaGetLastError();
 }

@@ -107,6 +107,26 @@ def test_march_kept_bitexact_c2_full_size(lumi, torch_cuda, small, oracle):
     assert counts.sum() > 0
 
 
+@pytest.mark.parametrize("frame,contraction", [(0, 1), (37, 1), (90, 1), (11, 0)])
+def test_filtered_march_equals_exact_full_eye(lumi, torch_cuda, small, frame, contraction):
+    """The production march pass (fp32 with a certified error bound, exact double fallback)
+    against the exact double march, bit for bit, over full 2048^2 eyebuffers of the
+    head-motion path."""
+    rot, org = scenes.head_pose(frame)
+    cam = lumi.CameraModel.from_spec(scenes.eye_cameras(2048, rot, org)[frame % 2])
+    opts = lumi.RenderOptions(contraction=contraction)
+    dm = small["dm"]
+    dm.set_kernel("simt")
+    try:
+        em, ec = march_kept_gpu(torch_cuda, lumi, dm, cam, opts, 0, 2048)
+    finally:
+        dm.set_kernel("packet")
+    fm, fc = march_kept_gpu(torch_cuda, lumi, dm, cam, opts, 0, 2048)
+    assert ec.sum() > 0
+    assert np.array_equal(fc, ec)
+    assert np.array_equal(fm, em)
+
+
 def _render(lumi, dm, cam, opts, b=0, e=None):
     e = cam.height if e is None else e
     out = np.zeros((3, cam.height, cam.width), np.float32)
