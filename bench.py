@@ -256,6 +256,8 @@ def run_ours(args):
     drv.stats.zero_()
     drv.launches = 0
     kernel_ms = 0.0
+    dm.take_timing()
+    dm.set_timing(True)  # events around each launch's march pass and render kernel
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -267,6 +269,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+    dm.set_timing(False)
+    march_ms, render_ms, render_launches = dm.take_timing()
     elapsed = float(t_start.elapsed_time(t_end))
     if world > 1:
         t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
@@ -328,7 +332,9 @@ def run_ours(args):
     bytes_per_ls = GATHER_BYTES_PER_LEVEL_SAMPLE // (1 if dm.kernel == "simt" else 2)
     kname = {"tc": "k_render_tc", "packet": "k_render_pk", "simt": "k_render_simt"}[dm.kernel]
     gather_bytes = level_samples * bytes_per_ls
-    kernel_s = kernel_ms / 1000.0  # rank-0 render launches (this rank's share at N>1)
+    # the render kernel's own launches on rank 0 (CUDA events on the launch stream around
+    # each launch, march pass excluded); counters are summed over ranks, so scale by 1/world
+    kernel_s = render_ms / 1000.0
     frac_rank = 1.0 / world
     achieved = gather_bytes * frac_rank / kernel_s / 1e9 if kernel_s > 0 else None
     mlp_tflops = evals * frac_rank * MLP_FLOP_PER_SAMPLE / kernel_s / 1e12 if kernel_s > 0 else None
@@ -363,6 +369,10 @@ def run_ours(args):
                    "kernel": kname},
         "fps": round(fps, 3),
         "render_ms_per_step": round(kernel_ms / args.steps, 3),  # rank-0 march+render span
+        "kernels": {"march_ms_per_launch": round(march_ms / max(render_launches, 1), 3),
+                    f"{kname}_ms_per_launch": round(render_ms / max(render_launches, 1), 3),
+                    "launches": render_launches,
+                    "render_share_of_step": round(render_ms / max(elapsed, 1e-9), 4)},
         "work": {"evals_per_ray": round(evals / max(rays, 1), 3),
                  "active_levels_per_eval": round(level_samples / max(evals, 1), 3),
                  "candidates_per_ray": round(candidates / max(rays, 1), 3)},
@@ -374,7 +384,8 @@ def run_ours(args):
                                     f"x 2 features x {bytes_per_ls // 16} B "
                                     f"({'fp32 table' if dm.kernel == 'simt' else 'fp16 table copy'}); "
                                     f"{level_samples / max(world, 1):.3e} level-samples in "
-                                    f"{kernel_ms:.1f} ms of render launches"},
+                                    f"{render_launches} {kname} launches, {render_ms:.1f} ms "
+                                    f"(CUDA events on the launch stream)"},
         "roofline_mlp": {"bound": "tensor", "achieved": None if mlp_tflops is None else round(mlp_tflops, 2),
                          "peak": peaks.get("bf16_tflops_sustained", 1398.6), "unit": "TFLOP/s",
                          "algorithmic": "18,944 FLOP per evaluated sample"},

@@ -148,6 +148,12 @@ int lumi_model_set_occupancy(LumiModel* m, const uint8_t* occupancy, int occ_res
 enum { LUMI_KERNEL_TC = 0, LUMI_KERNEL_SIMT = 1, LUMI_KERNEL_PACKET = 2 };
 int lumi_model_set_kernel(LumiModel* m, int kernel);
 int lumi_model_destroy(LumiModel* m);
+/* Kernel timing (bench/profiling aid, no reference counterpart): while enabled, every
+ * render_rows launch records CUDA events around its march pass and its render kernel on the
+ * launch stream.  take_timing synchronises those events, returns the summed milliseconds and
+ * the number of render launches since the last take, and resets the accumulators. */
+int lumi_model_set_timing(LumiModel* m, int enable);
+int lumi_model_take_timing(LumiModel* m, double* march_ms, double* render_ms, int* launches);
 /* Device-side memory footprint of the model in bytes. */
 int lumi_model_bytes(const LumiModel* m, uint64_t* bytes);
 

@@ -86,6 +86,8 @@ SIGNATURES = {
     "lumi_model_set_kernel": ([_vp, _i], C.c_int),
     "lumi_model_destroy": ([_vp], C.c_int),
     "lumi_model_bytes": ([_vp, _vp], C.c_int),
+    "lumi_model_set_timing": ([_vp, _i], C.c_int),
+    "lumi_model_take_timing": ([_vp, _vp, _vp, _vp], C.c_int),
     "lumi_render_rows": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp], C.c_int),
     "lumi_render_rows_async": ([_vp, _vp, _vp, _i, _i, _vp, _vp], C.c_int),
     "lumi_march_kept_async": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp], C.c_int),

@@ -25,12 +25,15 @@ struct BakeParams {
 cudaError_t launch_render_simt(const lumi_dev::RenderParams& p, cudaStream_t s);
 cudaError_t launch_march_kept(const lumi_dev::RenderParams& p, uint32_t* mask, int32_t* counts,
                               cudaStream_t s);
-cudaError_t launch_render_tc(lumi_dev::RenderParams p, cudaStream_t s, int num_sms);
+// ev (optional): 3 events recorded before the march pass, between march and render, after render
+cudaError_t launch_render_tc(lumi_dev::RenderParams p, cudaStream_t s, int num_sms,
+                             cudaEvent_t* ev = nullptr);
 size_t render_tc_smem_bytes();
 cudaError_t launch_march_mask(const lumi_dev::RenderParams& p, cudaStream_t s);
 // public [pixel][word] kept mask through the production (filtered) march pass
 cudaError_t launch_march_public(lumi_dev::RenderParams p, uint32_t* mask, int32_t* counts,
                                 cudaStream_t s);
-cudaError_t launch_render_pk(lumi_dev::RenderParams p, cudaStream_t s, int num_sms);
+cudaError_t launch_render_pk(lumi_dev::RenderParams p, cudaStream_t s, int num_sms,
+                             cudaEvent_t* ev = nullptr);
 cudaError_t launch_to_half(const float* src, void* dst_half, uint64_t n, cudaStream_t s);
 cudaError_t launch_bake(const lumi_dev::BakeParams& p, cudaStream_t s);

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -167,6 +168,9 @@ struct LumiModel {
   int num_sms = 148;
   std::mutex mu;
   std::map<std::tuple<double, double, int>, std::pair<double*, double>> ts_cache;
+  bool timing = false;
+  std::vector<std::array<cudaEvent_t, 3>> ev_pool;  // [march start, render start, render end]
+  size_t ev_used = 0;
 };
 
 namespace {
@@ -422,6 +426,8 @@ int lumi_model_destroy(LumiModel* m) {
   cudaFree(m->d_occ);
   cudaFree(m->d_counter);
   for (auto& kv : m->ts_cache) cudaFree(kv.second.first);
+  for (auto& a : m->ev_pool)
+    for (auto x : a) cudaEventDestroy(x);
   delete m;
   return LUMI_OK;
 }
@@ -449,12 +455,54 @@ int lumi_render_rows_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRe
   int rc = make_params(m, cam, o, b, e, &p);
   if (rc) return rc;
   if ((rc = set_target(&p, t, b, e))) return rc;
-  if (m->kernel == LUMI_KERNEL_SIMT)
-    LUMI_CUDA_TRY(launch_render_simt(p, static_cast<cudaStream_t>(stream)));
-  else if (m->kernel == LUMI_KERNEL_PACKET)
-    LUMI_CUDA_TRY(launch_render_pk(p, static_cast<cudaStream_t>(stream), m->num_sms));
-  else
-    LUMI_CUDA_TRY(launch_render_tc(p, static_cast<cudaStream_t>(stream), m->num_sms));
+  cudaEvent_t* ev = nullptr;
+  if (m->timing) {
+    std::lock_guard<std::mutex> lk(m->mu);
+    if (m->ev_used == m->ev_pool.size()) {
+      std::array<cudaEvent_t, 3> a{};
+      for (auto& x : a) LUMI_CUDA_TRY(cudaEventCreate(&x));
+      m->ev_pool.push_back(a);
+    }
+    ev = m->ev_pool[m->ev_used++].data();
+  }
+  const auto st = static_cast<cudaStream_t>(stream);
+  if (m->kernel == LUMI_KERNEL_SIMT) {
+    if (ev) LUMI_CUDA_TRY(cudaEventRecord(ev[0], st));
+    if (ev) LUMI_CUDA_TRY(cudaEventRecord(ev[1], st));
+    LUMI_CUDA_TRY(launch_render_simt(p, st));
+    if (ev) LUMI_CUDA_TRY(cudaEventRecord(ev[2], st));
+  } else if (m->kernel == LUMI_KERNEL_PACKET) {
+    LUMI_CUDA_TRY(launch_render_pk(p, st, m->num_sms, ev));
+  } else {
+    LUMI_CUDA_TRY(launch_render_tc(p, st, m->num_sms, ev));
+  }
+  return LUMI_OK;
+}
+
+int lumi_model_set_timing(LumiModel* m, int enable) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  m->timing = enable != 0;
+  return LUMI_OK;
+}
+
+int lumi_model_take_timing(LumiModel* m, double* march_ms, double* render_ms, int* launches) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  DeviceGuard dg(m->device);
+  std::lock_guard<std::mutex> lk(m->mu);
+  double a = 0.0, b = 0.0;
+  for (size_t i = 0; i < m->ev_used; ++i) {
+    auto& ev = m->ev_pool[i];
+    LUMI_CUDA_TRY(cudaEventSynchronize(ev[2]));
+    float x = 0.f, y = 0.f;
+    LUMI_CUDA_TRY(cudaEventElapsedTime(&x, ev[0], ev[1]));
+    LUMI_CUDA_TRY(cudaEventElapsedTime(&y, ev[1], ev[2]));
+    a += x;
+    b += y;
+  }
+  if (march_ms) *march_ms = a;
+  if (render_ms) *render_ms = b;
+  if (launches) *launches = (int)m->ev_used;
+  m->ev_used = 0;
   return LUMI_OK;
 }
 

@@ -578,7 +578,7 @@ using namespace lumi_dev;
 size_t render_pk_smem_bytes() { return sizeof(pk::Smem); }
 
 // march pass over packet-ordered ray ids + the packet kernel
-cudaError_t launch_render_pk(RenderParams p, cudaStream_t s, int num_sms) {
+cudaError_t launch_render_pk(RenderParams p, cudaStream_t s, int num_sms, cudaEvent_t* ev) {
   const long long rays = (long long)(p.row_end - p.row_begin) * p.cam.width;
   if (rays <= 0) return cudaSuccess;
   static int blocks_per_sm = -1;
@@ -619,13 +619,16 @@ cudaError_t launch_render_pk(RenderParams p, cudaStream_t s, int num_sms) {
   // the march pass's work counters are reported by the packet kernel (per ray), not here
   RenderParams pm = p;
   pm.work_stats = nullptr;
+  if (ev) cudaEventRecord(ev[0], s);
   if ((e = launch_march_mask(pm, s)) != cudaSuccess) return e;
+  if (ev) cudaEventRecord(ev[1], s);
   const long long grid = std::min<long long>((long long)blocks_per_sm * num_sms, (packets + 3) / 4);
 #ifdef LUMI_PHASE_TIMING
   unsigned long long zero7[7] = {0, 0, 0, 0, 0, 0, 0};
   cudaMemcpyToSymbolAsync(pk::g_phase_cycles_pk, zero7, sizeof(zero7), 0, cudaMemcpyHostToDevice, s);
 #endif
   pk::k_render_pk<<<(unsigned)grid, pk::kThreads, smem, s>>>(p);
+  if (ev) cudaEventRecord(ev[2], s);
 #ifdef LUMI_PHASE_TIMING
   {
     unsigned long long pc[7];

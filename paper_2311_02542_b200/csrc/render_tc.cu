@@ -683,7 +683,7 @@ using namespace lumi_dev;
 
 size_t render_tc_smem_bytes() { return sizeof(tc::Smem); }
 
-cudaError_t launch_render_tc(RenderParams p, cudaStream_t s, int num_sms) {
+cudaError_t launch_render_tc(RenderParams p, cudaStream_t s, int num_sms, cudaEvent_t* ev) {
   const long long rays = (long long)(p.row_end - p.row_begin) * p.cam.width;
   if (rays <= 0) return cudaSuccess;
   static int blocks_per_sm = -1;
@@ -740,13 +740,16 @@ cudaError_t launch_render_tc(RenderParams p, cudaStream_t s, int num_sms) {
     return e;
   if ((e = cudaMallocAsync(&p.kept_count, (size_t)p.total_rays * 2, s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(p.work_counter, 0, sizeof(unsigned int), s)) != cudaSuccess) return e;
+  if (ev) cudaEventRecord(ev[0], s);
   if ((e = launch_march_mask(p, s)) != cudaSuccess) return e;
+  if (ev) cudaEventRecord(ev[1], s);
   const long long grid = std::min<long long>((long long)blocks_per_sm * num_sms, tiles);
 #ifdef LUMI_PHASE_TIMING
   unsigned long long zero6[6] = {0, 0, 0, 0, 0, 0};
   cudaMemcpyToSymbolAsync(tc::g_phase_cycles, zero6, sizeof(zero6), 0, cudaMemcpyHostToDevice, s);
 #endif
   tc::k_render_tc<<<(unsigned)grid, tc::kThreads, smem, s>>>(p);
+  if (ev) cudaEventRecord(ev[2], s);
 #ifdef LUMI_PHASE_TIMING
   {
     unsigned long long pc[6];

@@ -283,11 +283,22 @@ class DeviceModel:
         self._lock = threading.Lock()
 
     def set_kernel(self, kernel: str) -> None:
-        """'tc' (persistent tcgen05 kernel, default) or 'simt' (fp32 CUDA-core cross-check)."""
+        """'packet' (packet-coherent tcgen05 kernel, default), 'tc' (one ray per thread
+        tcgen05 kernel) or 'simt' (fp32 CUDA-core cross-check)."""
         k = {"tc": _abi.LUMI_KERNEL_TC, "simt": _abi.LUMI_KERNEL_SIMT,
              "packet": _abi.LUMI_KERNEL_PACKET}[kernel]
         check(_abi.lib().lumi_model_set_kernel(self.h, k))
         self.kernel = kernel
+
+    def set_timing(self, enable: bool) -> None:
+        """Record CUDA events around each launch's march pass and render kernel."""
+        check(_abi.lib().lumi_model_set_timing(self.h, 1 if enable else 0))
+
+    def take_timing(self):
+        """(march_ms, render_ms, launches) summed since the last call (synchronises)."""
+        a, b, n = C.c_double(), C.c_double(), C.c_int()
+        check(_abi.lib().lumi_model_take_timing(self.h, C.byref(a), C.byref(b), C.byref(n)))
+        return float(a.value), float(b.value), int(n.value)
 
     def set_occupancy(self, grid: OccupancyGrid) -> None:
         check(_abi.lib().lumi_model_set_occupancy(self.h, _p(grid.bits), grid.res))
