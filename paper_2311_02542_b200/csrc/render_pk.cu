@@ -30,8 +30,11 @@ namespace pk {
 constexpr int kThreads = 128;  // UMMA M: 4 warps x 32 rows
 constexpr int kWarps = kThreads / 32;
 constexpr int kPW = 8, kPH = 4;  // packet: 8 x 4 pixels = one warp of rays
-constexpr uint32_t kTmemCols = 128;  // [0,64): fp32 accumulators, [64,96): fp16 A operand
-constexpr uint32_t kAcol = 64;
+constexpr uint32_t kTmemCols = 128;  // [0,64): fp32 accumulators, [64,104): fp16 A operand
+constexpr uint32_t kAcol = 64;       // hidden activations: K/2 columns from here
+constexpr uint32_t kOnesCol = 96;    // the constant [1 0 ... 0] bias block (K = 16, 8 columns)
+constexpr int kKb = 16;              // every layer's bias is one extra K = 16 step
+constexpr int kAch = (32 + kKb) / 8; // 8-element K chunks of the layer-1 A tile
 #ifndef LUMI_PK_PAIRS
 #define LUMI_PK_PAIRS 2
 #endif
@@ -45,13 +48,14 @@ __device__ unsigned long long g_phase_cycles_pk[7];
 // UMMA no-swizzle operands need 16-byte alignment only; the struct is used straight from
 // the dynamic __shared__ array so every access compiles to LDS/STS (not generic LD/ST).
 struct __align__(16) Smem {
-  uint8_t A[128 * 32 * 2];  // layer-1 input: hash-grid features, K-major core-matrix tile
-  uint8_t W1[64 * 32 * 2];  // density L1  N=64 K=32
-  uint8_t W2[32 * 64 * 2];  // density L2  N=32 (17 used) K=64
-  uint8_t C1[64 * 32 * 2];  // colour L1   N=64 K=32
-  uint8_t C2[64 * 64 * 2];  // colour L2   N=64 K=64
-  uint8_t C3[16 * 64 * 2];  // colour L3   N=16 (3 used) K=64
-  float b1[64], b2[32], cb1[64], cb2[64], cb3[16];
+  // K-major core-matrix tiles; every layer carries its bias as one extra K = 16 block
+  // (bias in column K of B, a constant [1 0 ... 0] block in A), so epilogues add nothing
+  uint8_t A[128 * (32 + kKb) * 2];  // layer-1 input: hash-grid features + ones block
+  uint8_t W1[64 * (32 + kKb) * 2];  // density L1  N=64 K=32
+  uint8_t W2[32 * (64 + kKb) * 2];  // density L2  N=32 (17 used) K=64
+  uint8_t C1[64 * (32 + kKb) * 2];  // colour L1   N=64 K=32
+  uint8_t C2[64 * (64 + kKb) * 2];  // colour L2   N=64 K=64
+  uint8_t C3[16 * (64 + kKb) * 2];  // colour L3   N=16 (3 used) K=64
   float4 res[kThreads];     // per row: sigma, r, g, b (row lane -> owner lane)
   uint32_t ballot[kWarps][32];   // per warp: lanes with candidate bit i of the current word
   uint16_t prefix[kWarps][33];   // exclusive prefix of popc(ballot[i])
@@ -77,42 +81,66 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
                     h2u(__floats2half2_rn(v[4], v[5])), h2u(__floats2half2_rn(v[6], v[7])));
 }
 
-// weights [n_real x K] fp32 row-major (network.h:64) -> fp16 UMMA tile with n_pad rows
+// weights [n_real x K] fp32 row-major + bias [n_real] (network.h:64, 144-151) -> fp16 UMMA
+// tile [n_pad][K + 16] with the bias in column K
 __device__ void load_weight_tile(uint8_t* dst, const float* __restrict__ W, int n_real, int n_pad,
                                  int K) {
-  const int kch = K / 8;
+  const float* bias = W + (size_t)n_real * K;
+  const int kch = (K + kKb) / 8;
   for (int it = threadIdx.x; it < n_pad * kch; it += blockDim.x) {
     const int n = it / kch, j = it % kch;
     float v[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = n < n_real ? __ldg(W + (size_t)n * K + 8 * j + q) : 0.f;
+    for (int q = 0; q < 8; ++q) {
+      const int k = 8 * j + q;
+      v[q] = n >= n_real ? 0.f : k < K ? __ldg(W + (size_t)n * K + k) : k == K ? __ldg(bias + n) : 0.f;
+    }
     st16(dst, core_off(n, j, kch), pack8(v));
   }
 }
 
+// layer 1 (SS form): A = features + ones block in shared memory
 template <int N, int K>
 __device__ __forceinline__ void issue_layer(const uint8_t* A, const uint8_t* B, uint32_t d_tmem) {
   constexpr uint32_t idesc = ptx::idesc_f16_f32<128, N>();
+  constexpr uint32_t sbo = ((K + kKb) / 8) * 128;
   const uint32_t a = ptx::smem_addr(A), b = ptx::smem_addr(B);
 #pragma unroll
-  for (int kk = 0; kk < K / 16; ++kk)
-    ptx::mma_f16(d_tmem, ptx::make_smem_desc(a + kk * 256, 128, (K / 8) * 128),
-                 ptx::make_smem_desc(b + kk * 256, 128, (K / 8) * 128), idesc, kk > 0 ? 1u : 0u);
+  for (int kk = 0; kk < (K + kKb) / 16; ++kk)
+    ptx::mma_f16(d_tmem, ptx::make_smem_desc(a + kk * 256, 128, sbo),
+                 ptx::make_smem_desc(b + kk * 256, 128, sbo), idesc, kk > 0 ? 1u : 0u);
 }
 
+// hidden layers (TS form): A = activations in TMEM columns [a_tmem, a_tmem + K/2), then the
+// TMEM ones block against the bias column of B
 template <int N, int K>
-__device__ __forceinline__ void issue_layer_ts(uint32_t a_tmem, const uint8_t* B, uint32_t d_tmem) {
+__device__ __forceinline__ void issue_layer_ts(uint32_t a_tmem, uint32_t ones_tmem, const uint8_t* B,
+                                               uint32_t d_tmem) {
   constexpr uint32_t idesc = ptx::idesc_f16_f32<128, N>();
+  constexpr uint32_t sbo = ((K + kKb) / 8) * 128;
   const uint32_t b = ptx::smem_addr(B);
 #pragma unroll
   for (int kk = 0; kk < K / 16; ++kk)  // 16 fp16 of K = 8 TMEM columns per step
-    ptx::mma_f16_ts(d_tmem, a_tmem + kk * 8, ptx::make_smem_desc(b + kk * 256, 128, (K / 8) * 128),
-                    idesc, kk > 0 ? 1u : 0u);
+    ptx::mma_f16_ts(d_tmem, a_tmem + kk * 8, ptx::make_smem_desc(b + kk * 256, 128, sbo), idesc,
+                    kk > 0 ? 1u : 0u);
+  ptx::mma_f16_ts(d_tmem, ones_tmem, ptx::make_smem_desc(b + (K / 16) * 256, 128, sbo), idesc, 1u);
 }
 
-// hidden-layer epilogue into TMEM: D row (64 fp32) + bias, ReLU, fp16 pairs -> the A columns
-// of this thread's lane for the next layer
-__device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, const float* bias, uint32_t a_lane) {
+// two fp32 -> packed fp16 (lo, hi), optionally clamped at 0, in one F2FP
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+__device__ __forceinline__ uint32_t pack2_relu(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
+// hidden-layer epilogue into TMEM: D row (64 fp32, bias included), ReLU, fp16 pairs -> the A
+// columns of this thread's lane for the next layer
+__device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane) {
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
     float v[16];
@@ -120,9 +148,7 @@ __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, const float* bia
     ptx::tmem_ld_wait();
     uint32_t w[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      w[j] = h2u(__floats2half2_rn(fmaxf(v[2 * j] + bias[16 * h + 2 * j], 0.f),
-                                   fmaxf(v[2 * j + 1] + bias[16 * h + 2 * j + 1], 0.f)));
+    for (int j = 0; j < 8; ++j) w[j] = pack2_relu(v[2 * j], v[2 * j + 1]);
     ptx::tmem_st8(a_lane + 8 * h, w);
   }
   ptx::tmem_st_wait();
@@ -205,13 +231,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
   load_weight_tile(s.C1, cp, 64, 64, 32);
   load_weight_tile(s.C2, c2, 64, 64, 64);
   load_weight_tile(s.C3, c3, 3, 16, 64);
-  for (int i = tid; i < 64; i += kThreads) {
-    s.b1[i] = dp[64 * 32 + i];
-    s.cb1[i] = cp[64 * 32 + i];
-    s.cb2[i] = c2[64 * 64 + i];
-  }
-  for (int i = tid; i < 32; i += kThreads) s.b2[i] = i < 17 ? d2[17 * 64 + i] : 0.f;
-  for (int i = tid; i < 16; i += kThreads) s.cb3[i] = i < 3 ? c3[3 * 64 + i] : 0.f;
+  // this row's constant ones block of the layer-1 A tile (never overwritten)
+  st16(s.A, core_off(tid, 4, kAch), make_uint4(0x3C00u, 0u, 0u, 0u));  // fp16 1.0
+  st16(s.A, core_off(tid, 5, kAch), make_uint4(0u, 0u, 0u, 0u));
   for (int l = tid; l < kMaxLevels; l += kThreads) {
     const int res = l < p.grid.levels ? p.grid.res[l] : 1;
     const bool dense = (p.grid.dense_mask >> l) & 1u;
@@ -229,6 +251,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
   ptx::tc_fence_after();
   const uint32_t tmem = s.tmem_base;
   const uint32_t t_lane = tmem + ((uint32_t)(warp * 32) << 16);
+  {  // this lane's constant ones block of the hidden layers' TMEM A operand
+    const uint32_t ones[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    ptx::tmem_st8(t_lane + kOnesCol, ones);
+    ptx::tmem_st_wait();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+  }
 
   const float3 o = make_float3((float)p.cam.origin[0], (float)p.cam.origin[1], (float)p.cam.origin[2]);
   const float two_base = (float)p.grid.two_base, inv_log = (float)(1.0 / p.grid.log_scale);
@@ -378,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     {
       const uint4 zero = make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) st16(s.A, core_off(tid, j, 4), zero);
+      for (int j = 0; j < 4; ++j) st16(s.A, core_off(tid, j, kAch), zero);
       if (have) s.samp[warp][lane] = make_float4(u, v, w, lw.frac);
       uint16_t* pc = s.pairs[warp];
       const unsigned lt = (1u << lane) - 1u;
@@ -393,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
         npairs += __popc(m);
       }
       __syncwarp();
-      uint8_t* Abase = s.A + (warp * 32 / 8) * (4 * 128);
+      uint8_t* Abase = s.A + (warp * 32 / 8) * (kAch * 128);
 #pragma unroll 1
       for (int base = 0; base < npairs; base += 32 * kPairs) {
         uint32_t code[kPairs];
@@ -417,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
         for (int q = 0; q < kPairs; ++q)
           if (code[q] != 0xffffu) {
             const int src = code[q] & 31u, lv = (code[q] >> 5) & 15u;
-            *reinterpret_cast<__half2*>(Abase + core_off(src, lv >> 2, 4) + (lv & 3) * 4) =
+            *reinterpret_cast<__half2*>(Abase + core_off(src, lv >> 2, kAch) + (lv & 3) * 4) =
                 __floats2half2_rn(f[q].x, f[q].y);
           }
       }
@@ -435,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     // layer 1 reads the gathered features from shared memory (SS form); the hidden layers
     // keep their fp16 activations in TMEM columns [kAcol, kAcol + K/2) as the A operand
     // (TS form), so epilogues store with tcgen05.st and never touch shared memory.
-    const uint32_t a_tmem = tmem + kAcol;
+    const uint32_t a_tmem = tmem + kAcol, ones_tmem = tmem + kOnesCol;
     const uint32_t a_lane = t_lane + kAcol;
     if (issuer) {
       ptx::tc_fence_after();
@@ -445,13 +475,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-    relu64_to_tmem(t_lane, s.b1, a_lane);
+    relu64_to_tmem(t_lane, a_lane);
     ptx::tc_fence_before();
     __syncthreads();
 
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer_ts<32, 64>(a_tmem, s.W2, tmem);
+      issue_layer_ts<32, 64>(a_tmem, ones_tmem, s.W2, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
@@ -460,15 +490,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     ptx::tmem_ld16(t_lane, v32);
     ptx::tmem_ld16(t_lane + 16, v32 + 16);
     ptx::tmem_ld_wait();
-    const float sigma = trunc_exp(v32[0] + s.b2[0]);
+    const float sigma = trunc_exp(v32[0]);
     {
       float cin[32];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) cin[j] = v32[1 + j] + s.b2[1 + j];
+      for (int j = 0; j < 16; ++j) cin[j] = v32[1 + j];
       sh_encode(d3{(double)dx, (double)dy, (double)dz}, cin + 16);
       uint32_t wv[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) wv[j] = h2u(__floats2half2_rn(cin[2 * j], cin[2 * j + 1]));
+      for (int j = 0; j < 16; ++j) wv[j] = pack2(cin[2 * j], cin[2 * j + 1]);
       ptx::tmem_st16(a_lane, wv);
       ptx::tmem_st_wait();
     }
@@ -477,31 +507,31 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
 
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer_ts<64, 32>(a_tmem, s.C1, tmem);
+      issue_layer_ts<64, 32>(a_tmem, ones_tmem, s.C1, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-    relu64_to_tmem(t_lane, s.cb1, a_lane);
+    relu64_to_tmem(t_lane, a_lane);
     ptx::tc_fence_before();
     __syncthreads();
 
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer_ts<64, 64>(a_tmem, s.C2, tmem);
+      issue_layer_ts<64, 64>(a_tmem, ones_tmem, s.C2, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
-    relu64_to_tmem(t_lane, s.cb2, a_lane);
+    relu64_to_tmem(t_lane, a_lane);
     ptx::tc_fence_before();
     __syncthreads();
 
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer_ts<16, 64>(a_tmem, s.C3, tmem);
+      issue_layer_ts<16, 64>(a_tmem, ones_tmem, s.C3, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
@@ -514,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
       float rgb[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const float raw = v32[k] + s.cb3[k];
+        const float raw = v32[k];
         rgb[k] = p.mlp.color_space == 0 ? sigmoid(raw) : trunc_exp(raw);
       }
       s.res[tid] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
