@@ -215,6 +215,7 @@ __device__ __forceinline__ void encode(const GridDev& g, d3 c, const LodW& lw, f
 struct MlpDev {
   const float* dparams;
   const float* cparams;
+  const float* fused;  // [65 x 80] + [65]: density L2 folded into colour L1 (lumi_api.cu)
   int color_space;
 };
 

@@ -160,6 +160,7 @@ struct LumiModel {
   void* d_table16 = nullptr;  // half2 copy (tensor-core renderer)
   float* d_dparams = nullptr;
   float* d_cparams = nullptr;
+  float* d_fused = nullptr;  // density L2 folded into colour L1 (packet kernel), see fuse_l2_c1
   uint8_t* d_occ = nullptr;
   int occ_res = 0;
   unsigned int* d_counter = nullptr;  // kCounterSlots per-launch tile counters
@@ -249,6 +250,7 @@ int make_params(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions
   g.log_scale = std::log(m->desc.per_level_scale);
   p->mlp.dparams = m->d_dparams;
   p->mlp.cparams = m->d_cparams;
+  p->mlp.fused = m->d_fused;
   p->mlp.color_space = m->desc.color_space;
   p->occ = m->d_occ;
   p->occ_res = m->occ_res;
@@ -349,6 +351,39 @@ int lumi_synth_params(const LumiFieldDesc* desc, uint64_t seed, double amp, floa
   return LUMI_OK;
 }
 
+namespace {
+// The density network's output layer is linear (field.h:116-122: sigma = trunc_exp(out[0]),
+// bottleneck = out[1..17) straight into the colour input), so colour layer 1 applied to
+// [bottleneck, sh] equals one layer on [h1, sh]:
+//   C1a (W2' h1 + b2') + C1b sh + cb1 = (C1a W2') h1 + C1b sh + (C1a b2' + cb1),
+// with sigma's row W2[0] . h1 + b2[0] appended as output 64.  Returns [65 x 80] weights
+// then [65] biases (products accumulated in double).  The packet kernel runs this as one
+// tcgen05 layer (N = 80, K = 64 + 16), one MMA round trip fewer per batch.
+std::vector<float> fuse_l2_c1(const float* dp, const float* cp) {
+  constexpr int H = 64, B = 16, CIN = 32, K = H + 16;
+  const float* W2 = dp + H * 32 + H;  // [17 x 64]
+  const float* b2 = W2 + (1 + B) * H;
+  const float* C1 = cp;               // [64 x 32]
+  const float* cb1 = cp + H * CIN;
+  std::vector<float> f((H + 1) * K + (H + 1), 0.f);
+  float* bias = f.data() + (H + 1) * K;
+  for (int n = 0; n < H; ++n) {
+    for (int k = 0; k < H; ++k) {
+      double acc = 0.0;
+      for (int j = 0; j < B; ++j) acc += (double)C1[n * CIN + j] * (double)W2[(1 + j) * H + k];
+      f[n * K + k] = (float)acc;
+    }
+    for (int k = 0; k < 16; ++k) f[n * K + H + k] = C1[n * CIN + B + k];
+    double acc = cb1[n];
+    for (int j = 0; j < B; ++j) acc += (double)C1[n * CIN + j] * (double)b2[1 + j];
+    bias[n] = (float)acc;
+  }
+  for (int k = 0; k < H; ++k) f[H * K + k] = W2[k];
+  bias[H] = b2[0];
+  return f;
+}
+}  // namespace
+
 int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
                       const float* dparams, const float* cparams, const uint8_t* occ, int occ_res,
                       LumiModel** out) {
@@ -391,6 +426,13 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
       (e = launch_to_half(m->d_table, m->d_table16, lay.total_floats, nullptr)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess)
     return cleanup(fail(LUMI_ERR_CUDA, std::string("model upload: ") + cudaGetErrorString(e)));
+  {
+    const std::vector<float> fused = fuse_l2_c1(dparams, cparams);
+    if ((e = cudaMalloc(&m->d_fused, fused.size() * sizeof(float))) != cudaSuccess ||
+        (e = cudaMemcpy(m->d_fused, fused.data(), fused.size() * sizeof(float),
+                        cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cleanup(fail(LUMI_ERR_CUDA, std::string("model upload: ") + cudaGetErrorString(e)));
+  }
   if ((rc = lumi_model_set_occupancy(m, occ, occ_res))) return cleanup(rc);
   if (const char* k = std::getenv("LUMI_KERNEL")) {
     const std::string ks(k);
@@ -423,6 +465,7 @@ int lumi_model_destroy(LumiModel* m) {
   cudaFree(m->d_table16);
   cudaFree(m->d_dparams);
   cudaFree(m->d_cparams);
+  cudaFree(m->d_fused);
   cudaFree(m->d_occ);
   cudaFree(m->d_counter);
   for (auto& kv : m->ts_cache) cudaFree(kv.second.first);

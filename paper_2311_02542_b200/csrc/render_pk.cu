@@ -30,9 +30,13 @@ namespace pk {
 constexpr int kThreads = 128;  // UMMA M: 4 warps x 32 rows
 constexpr int kWarps = kThreads / 32;
 constexpr int kPW = 8, kPH = 4;  // packet: 8 x 4 pixels = one warp of rays
-constexpr uint32_t kTmemCols = 128;  // [0,64): fp32 accumulators, [64,104): fp16 A operand
-constexpr uint32_t kAcol = 64;       // hidden activations: K/2 columns from here
-constexpr uint32_t kOnesCol = 96;    // the constant [1 0 ... 0] bias block (K = 16, 8 columns)
+// TMEM columns: [0,80) fp32 accumulators (N <= 80), [80,112) hidden activations h (fp16 pairs,
+// the TS-form A operand), [112,120) the SH encoding (fused layer only), [120,128) the
+// constant [1 0 ... 0] bias block
+constexpr uint32_t kTmemCols = 128;
+constexpr uint32_t kAcol = 80;
+constexpr uint32_t kShCol = 112;
+constexpr uint32_t kOnesCol = 120;
 constexpr int kKb = 16;              // every layer's bias is one extra K = 16 step
 constexpr int kAch = (32 + kKb) / 8; // 8-element K chunks of the layer-1 A tile
 #ifndef LUMI_PK_PAIRS
@@ -52,8 +56,7 @@ struct __align__(16) Smem {
   // (bias in column K of B, a constant [1 0 ... 0] block in A), so epilogues add nothing
   uint8_t A[128 * (32 + kKb) * 2];  // layer-1 input: hash-grid features + ones block
   uint8_t W1[64 * (32 + kKb) * 2];  // density L1  N=64 K=32
-  uint8_t W2[32 * (64 + kKb) * 2];  // density L2  N=32 (17 used) K=64
-  uint8_t C1[64 * (32 + kKb) * 2];  // colour L1   N=64 K=32
+  uint8_t F[80 * (80 + kKb) * 2];   // density L2 folded into colour L1: N=80 (65 used) K=64+16
   uint8_t C2[64 * (64 + kKb) * 2];  // colour L2   N=64 K=64
   uint8_t C3[16 * (64 + kKb) * 2];  // colour L3   N=16 (3 used) K=64
   float4 res[kThreads];     // per row: sigma, r, g, b (row lane -> owner lane)
@@ -223,12 +226,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
   // ---- setup: weights, biases, mbarrier, TMEM ------------------------------------------
   const float* dp = p.mlp.dparams;
   const float* cp = p.mlp.cparams;
-  const float* d2 = dp + 64 * 32 + 64;
   const float* c2 = cp + 64 * 32 + 64;
   const float* c3 = c2 + 64 * 64 + 64;
   load_weight_tile(s.W1, dp, 64, 64, 32);
-  load_weight_tile(s.W2, d2, 1 + kBottleneck, 32, 64);
-  load_weight_tile(s.C1, cp, 64, 64, 32);
+  load_weight_tile(s.F, p.mlp.fused, kHidden + 1, 80, 80);
   load_weight_tile(s.C2, c2, 64, 64, 64);
   load_weight_tile(s.C3, c3, 3, 16, 64);
   // this row's constant ones block of the layer-1 A tile (never overwritten)
@@ -476,43 +477,31 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     phase ^= 1;
     ptx::tc_fence_after();
     relu64_to_tmem(t_lane, a_lane);
-    ptx::tc_fence_before();
-    __syncthreads();
-
-    if (issuer) {
-      ptx::tc_fence_after();
-      issue_layer_ts<32, 64>(a_tmem, ones_tmem, s.W2, tmem);
-      ptx::mma_commit(&s.mbar);
-    }
-    ptx::mbar_wait(&s.mbar, phase);
-    phase ^= 1;
-    ptx::tc_fence_after();
-    ptx::tmem_ld16(t_lane, v32);
-    ptx::tmem_ld16(t_lane + 16, v32 + 16);
-    ptx::tmem_ld_wait();
-    const float sigma = trunc_exp(v32[0]);
-    {
-      float cin[32];
+    {  // the colour network's direction input, SH degree 3 (network.h:17-37), next to h
+      float sh[16];
+      sh_encode(d3{(double)dx, (double)dy, (double)dz}, sh);
+      uint32_t wv[8];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) cin[j] = v32[1 + j];
-      sh_encode(d3{(double)dx, (double)dy, (double)dz}, cin + 16);
-      uint32_t wv[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) wv[j] = pack2(cin[2 * j], cin[2 * j + 1]);
-      ptx::tmem_st16(a_lane, wv);
+      for (int j = 0; j < 8; ++j) wv[j] = pack2(sh[2 * j], sh[2 * j + 1]);
+      ptx::tmem_st8(t_lane + kShCol, wv);
       ptx::tmem_st_wait();
     }
     ptx::tc_fence_before();
     __syncthreads();
 
+    // density L2 + colour L1 as one layer on [h, sh] (lumi_api.cu fuse_l2_c1): outputs 0..63
+    // are the colour hidden pre-activations, output 64 is sigma's
     if (issuer) {
       ptx::tc_fence_after();
-      issue_layer_ts<64, 32>(a_tmem, ones_tmem, s.C1, tmem);
+      issue_layer_ts<80, 80>(a_tmem, ones_tmem, s.F, tmem);
       ptx::mma_commit(&s.mbar);
     }
     ptx::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     ptx::tc_fence_after();
+    ptx::tmem_ld16(t_lane + 64, v32);
+    ptx::tmem_ld_wait();
+    const float sigma = trunc_exp(v32[0]);
     relu64_to_tmem(t_lane, a_lane);
     ptx::tc_fence_before();
     __syncthreads();
