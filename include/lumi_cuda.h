@@ -19,6 +19,14 @@
  *   lumi_bake_occupancy         OccupancyGrid::probe + prune proj/src/occupancy.cpp:97-154
  *   lumi_equal_assignment, lumi_assign_rows, lumi_next_assignment, lumi_aggregate_stats
  *                               the row scheduler            proj/src/scheduler.cpp:18-162
+ *   lumi_train_backward[_async] the training loop's per-ray body: march_ray(record) +
+ *                               ray_loss + backward_ray      proj/src/trainer.cpp:549-561,
+ *                               proj/include/lumi/train_step.h:16-154, renderer.h:110-120,
+ *                               field.h:141-179, network.h:115-136, grid.h:118-137
+ *   lumi_adam_step_async        simd::adam_step              proj/include/lumi/simd.h:106-121,
+ *                                                            proj/src/trainer.cpp:228-235
+ *   lumi_model_device_params, lumi_model_params_updated
+ *                               in-place parameter access for a device-side optimizer
  *
  * All device work is sm_100a CUDA (paper_2311_02542_b200/csrc); there is no CPU
  * fallback -- without a usable B200 the calls fail with LUMI_ERR_CUDA.
@@ -200,6 +208,71 @@ int lumi_checkpoint_read(const char* path, LumiCheckpointInfo* info, float* tabl
 int lumi_bake_occupancy(LumiModel* m, const LumiCameraDesc* cams, int ncams,
                         int samples_per_ray, int points_per_axis, int occ_res, float alpha,
                         uint8_t* occupancy_out, float* probe_max_out);
+
+/* ---- training reverse path (GPU) ------------------------------------------------ */
+/* TrainRay (trainer.h:90-97): the ray and its right-neighbour ray (generate_ray at
+   x + 0.5 / generate_ray_unchecked at x + 1.5), the model-space target, the ground-truth
+   depth (< 0: unavailable), the normalised vignetting radius and the camera index. */
+typedef struct LumiTrainRay {
+  double origin[3], dir[3];
+  double norigin[3], ndir[3];
+  float gt[3];
+  int32_t camera;
+  double gt_depth;
+  double vignette_r;
+} LumiTrainRay;
+
+/* The TrainConfig fields ray_loss reads (trainer.h:18-60) and the per-iteration inputs. */
+typedef struct LumiLossConfig {
+  double lambda_depth, lambda_dvar, lambda_dist;
+  double inv_batch;    /* 1 / batch size (trainer.cpp:544) */
+  int32_t depth_active; /* iteration < depth window (trainer.cpp:545) */
+  int32_t _pad;
+} LumiLossConfig;
+
+/* LossTerms (trainer.h:99-102), the ray-dependent part; total = image+depth+dvar+dist. */
+typedef struct LumiLossTerms {
+  double total, image, depth, dvar, dist;
+} LumiLossTerms;
+
+/* FieldGradients (field.h:48-62) + the per-camera vignetting gradient and loss sums.  All
+   are ACCUMULATED (zero them per iteration, as trainer.cpp:547 does).  grid:
+   [layout.total_floats], density: [layout.density_params], color: [layout.color_params]
+   (weights then bias per layer), alpha_v: [ncams], loss: one LumiLossTerms. */
+typedef struct LumiTrainGrads {
+  float* grid;
+  float* density;
+  float* color;
+  double* alpha_v;
+  LumiLossTerms* loss;
+} LumiTrainGrads;
+
+/* For every ray: march_ray(record = true) through the model's occupancy grid, ray_loss, and
+   backward_ray into `grads` -- the body of trainer.cpp:549-561.  cam_tnf ([ncams][2] t_near,
+   t_far) and alpha_v ([ncams]) are host arrays.  Async form: rays, grads and the optional
+   per-ray outputs (ray_evals = rec.t.size(), ray_contrib = rec.contributing) are device
+   pointers, work is enqueued on `stream`; it synchronises the stream twice internally to
+   size the per-sample buffers.  Sync form: the same with host buffers. */
+int lumi_train_backward_async(LumiModel* m, const LumiTrainRay* rays, int nrays,
+                              const double* cam_tnf, const double* alpha_v, int ncams,
+                              const LumiRenderOptions* opts, const LumiLossConfig* loss,
+                              const LumiTrainGrads* grads, int32_t* ray_evals,
+                              int32_t* ray_contrib, void* stream);
+int lumi_train_backward(LumiModel* m, const LumiTrainRay* rays, int nrays, const double* cam_tnf,
+                        const double* alpha_v, int ncams, const LumiRenderOptions* opts,
+                        const LumiLossConfig* loss, const LumiTrainGrads* grads,
+                        int32_t* ray_evals, int32_t* ray_contrib);
+/* simd::adam_step (simd.h:106-121) on device arrays of n floats: c1 = 1/(1-beta1^t),
+   c2 = 1/(1-beta2^t) precomputed by the caller (trainer.cpp:230-231). */
+int lumi_adam_step_async(float* params, const float* grads, float* mom, float* vel, uint64_t n,
+                         float lr, float beta1, float beta2, float eps, float c1, float c2,
+                         void* stream);
+/* The model's device-resident fp32 parameters (table in the grid.h:58-74 layout, density and
+   colour nets weights-then-bias), for an in-place device optimizer.  After changing them,
+   lumi_model_params_updated() rebuilds the derived copies the renderers read (fp16 table,
+   fused density-L2/colour-L1 layer).  Synchronous. */
+int lumi_model_device_params(LumiModel* m, float** table, float** density, float** color);
+int lumi_model_params_updated(LumiModel* m);
 
 /* ---- row scheduler (host) ------------------------------------------------------- */
 int lumi_equal_assignment(int height, int workers, int32_t* rows, double* shares);

@@ -1016,3 +1016,491 @@ int lo_aggregate_stats(const double* wall_ms, int n, double out[3]) { /* schedul
   free(t);
   return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Training reverse path: march_ray(record) + ray_loss + backward_ray         */
+/* (renderer.h:126-237, train_step.h:16-154, field.h:106-179, network.h:115-136, */
+/*  grid.h:118-137, simd.h:35-90 scalar order)                               */
+/* ------------------------------------------------------------------------- */
+
+/* FieldChunk (field.h:30-45) with feature-major activations of n <= LO_BATCH samples */
+typedef struct {
+  int n;
+  double (*pos)[3];
+  float *lodw, *feat, *h, *dout, *cin, *c1, *c2, *craw, *sigma_raw, *sigma, *color;
+} lo_chunk;
+
+static void lo_chunk_alloc(lo_chunk* c, int L, int F, int H, int B) {
+  c->n = 0;
+  c->pos = (double(*)[3])malloc(sizeof(double) * 3 * LO_BATCH);
+  c->lodw = (float*)malloc(sizeof(float) * (size_t)L * LO_BATCH);
+  c->feat = (float*)malloc(sizeof(float) * (size_t)F * LO_BATCH);
+  c->h = (float*)malloc(sizeof(float) * (size_t)H * LO_BATCH);
+  c->dout = (float*)malloc(sizeof(float) * (size_t)(1 + B) * LO_BATCH);
+  c->cin = (float*)malloc(sizeof(float) * (size_t)(B + 16) * LO_BATCH);
+  c->c1 = (float*)malloc(sizeof(float) * (size_t)H * LO_BATCH);
+  c->c2 = (float*)malloc(sizeof(float) * (size_t)H * LO_BATCH);
+  c->craw = (float*)malloc(sizeof(float) * 3 * LO_BATCH);
+  c->sigma_raw = (float*)malloc(sizeof(float) * LO_BATCH);
+  c->sigma = (float*)malloc(sizeof(float) * LO_BATCH);
+  c->color = (float*)malloc(sizeof(float) * 3 * LO_BATCH);
+}
+
+static void lo_chunk_free(lo_chunk* c) {
+  free(c->pos);
+  free(c->lodw);
+  free(c->feat);
+  free(c->h);
+  free(c->dout);
+  free(c->cin);
+  free(c->c1);
+  free(c->c2);
+  free(c->craw);
+  free(c->sigma_raw);
+  free(c->sigma);
+  free(c->color);
+}
+
+/* RadianceField::forward_chunk with every activation kept (field.h:106-137) */
+static void lo_chunk_forward(const lo_model* m, lo_chunk* ck, const float* sh) {
+  const lo_field_config* cfg = &m->cfg;
+  const int n = ck->n, L = cfg->levels, F = L * cfg->features_per_level, H = cfg->hidden_width,
+            B = cfg->bottleneck;
+  float one[LO_MAX_LEVELS * 8];
+  for (int i = 0; i < n; ++i) {
+    lo_encode(m, ck->pos[i], ck->lodw + (size_t)i * L, one);
+    for (int f = 0; f < F; ++f) ck->feat[(size_t)f * n + i] = one[f];
+  }
+  const float* dp = m->dparams;
+  lo_dense(m->mlp_mode, H, F, n, dp, dp + (size_t)H * F, ck->feat, ck->h, 1);
+  dp += (size_t)H * F + H;
+  lo_dense(m->mlp_mode, 1 + B, H, n, dp, dp + (size_t)(1 + B) * H, ck->h, ck->dout, 0);
+  for (int i = 0; i < n; ++i) {
+    ck->sigma_raw[i] = ck->dout[i];
+    ck->sigma[i] = lo_trunc_exp(ck->dout[i]);
+  }
+  memcpy(ck->cin, ck->dout + n, sizeof(float) * (size_t)B * n);
+  for (int s = 0; s < 16; ++s)
+    for (int i = 0; i < n; ++i) ck->cin[(size_t)(B + s) * n + i] = sh[s];
+  const float* cp = m->cparams;
+  lo_dense(m->mlp_mode, H, B + 16, n, cp, cp + (size_t)H * (B + 16), ck->cin, ck->c1, 1);
+  cp += (size_t)H * (B + 16) + H;
+  lo_dense(m->mlp_mode, H, H, n, cp, cp + (size_t)H * H, ck->c1, ck->c2, 1);
+  cp += (size_t)H * H + H;
+  lo_dense(m->mlp_mode, 3, H, n, cp, cp + (size_t)3 * H, ck->c2, ck->craw, 0);
+  for (int i = 0; i < 3 * n; ++i)
+    ck->color[i] = cfg->color_space == 0 ? lo_sigmoid(ck->craw[i]) : lo_trunc_exp(ck->craw[i]);
+}
+
+static inline float lo_trunc_exp_grad(float x) { /* network.h:48-52 */
+  return expf(x < 10.0f ? x : 10.0f);
+}
+
+/* simd::scalar::relu_backward / dense_backward_weights / dense_backward_data (simd.h:53-90) */
+static void lo_relu_bwd(size_t mm, const float* y, float* dy) {
+  for (size_t i = 0; i < mm; ++i)
+    if (y[i] <= 0.0f) dy[i] = 0.0f;
+}
+static void lo_dense_bwd_w(int rows, int cols, int n, const float* dy, const float* x, float* dW,
+                           float* db) {
+  for (int r = 0; r < rows; ++r) {
+    const float* dyr = dy + (size_t)r * n;
+    float acc = 0.0f;
+    for (int i = 0; i < n; ++i) acc += dyr[i];
+    db[r] += acc;
+    float* dwr = dW + (size_t)r * cols;
+    for (int c = 0; c < cols; ++c) {
+      const float* xc = x + (size_t)c * n;
+      float a = 0.0f;
+      for (int i = 0; i < n; ++i) a += dyr[i] * xc[i];
+      dwr[c] += a;
+    }
+  }
+}
+static void lo_dense_bwd_x(int rows, int cols, int n, const float* W, const float* dy, float* dx) {
+  for (int r = 0; r < rows; ++r) {
+    const float* wr = W + (size_t)r * cols;
+    const float* dyr = dy + (size_t)r * n;
+    for (int c = 0; c < cols; ++c) {
+      const float w = wr[c];
+      float* dxc = dx + (size_t)c * n;
+      for (int i = 0; i < n; ++i) dxc[i] += w * dyr[i];
+    }
+  }
+}
+
+/* Mlp::backward (network.h:115-136) for a stack of `nl` layers; acts[k] is layer k's output,
+   dy0 the output gradient [out x n], dx (zeroed by the caller) the input gradient.  dy and
+   scratch ping-pong like the reference's dy.swap(scratch); each holds maxdim x n floats. */
+static void lo_mlp_backward(int nl, const int* in, const int* out, const int* relu,
+                            const float* params, const float* x, const float* const* acts, int n,
+                            const float* dy0, float* dx, float* grads, float* dy, float* scratch) {
+  size_t off[4];
+  size_t o = 0;
+  for (int k = 0; k < nl; ++k) {
+    off[k] = o;
+    o += (size_t)out[k] * in[k] + out[k];
+  }
+  memcpy(dy, dy0, sizeof(float) * (size_t)out[nl - 1] * n);
+  for (int k = nl - 1; k >= 0; --k) {
+    if (relu[k]) lo_relu_bwd((size_t)out[k] * n, acts[k], dy);
+    const float* input = k == 0 ? x : acts[k - 1];
+    float* gw = grads + off[k];
+    lo_dense_bwd_w(out[k], in[k], n, dy, input, gw, gw + (size_t)out[k] * in[k]);
+    const float* W = params + off[k];
+    if (k == 0) {
+      lo_dense_bwd_x(out[k], in[k], n, W, dy, dx);
+    } else {
+      memset(scratch, 0, sizeof(float) * (size_t)in[k] * n);
+      lo_dense_bwd_x(out[k], in[k], n, W, dy, scratch);
+      float* t = dy;
+      dy = scratch;
+      scratch = t;
+    }
+  }
+}
+
+/* MultiResHashGrid::encode_backward (grid.h:118-137) for one sample */
+static void lo_encode_backward(const lo_model* m, const double c[3], const float* w,
+                               const float* dfeat, size_t stride, float* grad) {
+  const lo_grid_layout* L = &m->layout;
+  const int fpl = L->fpl;
+  double u = (c[0] + 2.0) * 0.25, v = (c[1] + 2.0) * 0.25, s = (c[2] + 2.0) * 0.25;
+  for (int l = 0; l < L->levels; ++l) {
+    if (w[l] <= 0.0f) continue;
+    const int res = L->resolution[l];
+    double pu = lo_clamp(u, 0.0, 1.0) * res, pv = lo_clamp(v, 0.0, 1.0) * res,
+           ps = lo_clamp(s, 0.0, 1.0) * res;
+    int iu = (int)pu, iv = (int)pv, is = (int)ps;
+    if (iu > res - 1) iu = res - 1;
+    if (iv > res - 1) iv = res - 1;
+    if (is > res - 1) is = res - 1;
+    double fu = pu - iu, fv = pv - iv, fs = ps - is;
+    const uint32_t verts = (uint32_t)res + 1;
+    const float* dl = dfeat + (size_t)l * fpl * stride;
+    float* base = grad + L->offset[l];
+    for (int k = 0; k < 8; ++k) {
+      uint32_t x = (uint32_t)iu + (k & 1), y = (uint32_t)iv + ((k >> 1) & 1),
+               z = (uint32_t)is + ((k >> 2) & 1);
+      uint32_t idx = L->dense[l] ? (z * verts + y) * verts + x
+                                 : lo_spatial_hash(x, y, z, L->entries[l]);
+      double wu = (k & 1) ? fu : 1.0 - fu;
+      double wv = ((k >> 1) & 1) ? fv : 1.0 - fv;
+      double ws = ((k >> 2) & 1) ? fs : 1.0 - fs;
+      float tri = (float)(wu * wv * ws);
+      float coeff = tri * w[l];
+      float* entry = base + (size_t)idx * fpl;
+      for (int f = 0; f < fpl; ++f) entry[f] += coeff * dl[(size_t)f * stride];
+    }
+  }
+}
+
+/* RadianceField::backward_chunk (field.h:141-179), colour evaluated */
+static void lo_chunk_backward(const lo_model* m, const lo_chunk* ck, const float* dsigma,
+                              const float* dcolor, float* g_grid, float* g_density,
+                              float* g_color, float* work) {
+  const lo_field_config* cfg = &m->cfg;
+  const int n = ck->n, L = cfg->levels, F = L * cfg->features_per_level, H = cfg->hidden_width,
+            B = cfg->bottleneck, CI = B + 16;
+  float* bwd_dout = work;                            /* (1+B) x n */
+  float* bwd_craw = bwd_dout + (size_t)(1 + B) * n;  /* 3 x n */
+  float* bwd_cin = bwd_craw + (size_t)3 * n;         /* CI x n */
+  float* bwd_feat = bwd_cin + (size_t)CI * n;        /* F x n */
+  const int MD = (H > F ? H : F) > CI ? (H > F ? H : F) : CI;
+  float* dyb = bwd_feat + (size_t)F * n;             /* MD x n */
+  float* scratch = dyb + (size_t)MD * n;             /* MD x n */
+  memset(bwd_dout, 0, sizeof(float) * (size_t)(1 + B) * n);
+  if (dcolor) {
+    for (int i = 0; i < 3 * n; ++i) {
+      float g;
+      if (cfg->color_space == 0) {
+        float c = ck->color[i];
+        g = c * (1.0f - c);
+      } else {
+        g = lo_trunc_exp_grad(ck->craw[i]);
+      }
+      bwd_craw[i] = dcolor[i] * g;
+    }
+    memset(bwd_cin, 0, sizeof(float) * (size_t)CI * n);
+    const int in[3] = {CI, H, H}, out[3] = {H, H, 3}, relu[3] = {1, 1, 0};
+    const float* acts[3] = {ck->c1, ck->c2, ck->craw};
+    lo_mlp_backward(3, in, out, relu, m->cparams, ck->cin, acts, n, bwd_craw, bwd_cin, g_color,
+                    dyb, scratch);
+    memcpy(bwd_dout + n, bwd_cin, sizeof(float) * (size_t)B * n);
+  }
+  for (int i = 0; i < n; ++i) bwd_dout[i] = dsigma[i] * lo_trunc_exp_grad(ck->sigma_raw[i]);
+  memset(bwd_feat, 0, sizeof(float) * (size_t)F * n);
+  {
+    const int in[2] = {F, H}, out[2] = {H, 1 + B}, relu[2] = {1, 0};
+    const float* acts[2] = {ck->h, ck->dout};
+    lo_mlp_backward(2, in, out, relu, m->dparams, ck->feat, acts, n, bwd_dout, bwd_feat,
+                    g_density, dyb, scratch);
+  }
+  for (int i = 0; i < n; ++i)
+    lo_encode_backward(m, ck->pos[i], ck->lodw + (size_t)i * L, bwd_feat + i, (size_t)n, g_grid);
+}
+
+static inline double lo_sgn(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0); }
+
+int lo_train_backward(const lo_model* m, const double* cam_tnf, const double* alpha_v, int ncams,
+                      const lo_train_ray* rays, int nrays, const lo_render_options* opts,
+                      const lo_loss_config* lc, float* g_grid, float* g_density, float* g_color,
+                      double* alpha_grad, lo_loss_terms* loss, int32_t* ray_evals,
+                      int32_t* ray_contrib) {
+  const lo_field_config* cfg = &m->cfg;
+  const int L = cfg->levels, F = L * cfg->features_per_level, H = cfg->hidden_width,
+            B = cfg->bottleneck;
+  const int spp = opts->samples_per_ray, cs = opts->chunk_size;
+  if (cfg->levels > LO_MAX_LEVELS || spp < 2 || cs < 1 || cs > LO_BATCH) return -2;
+  const int max_chunks = (spp + cs - 1) / cs;
+  lo_chunk* chunks = (lo_chunk*)malloc(sizeof(lo_chunk) * (size_t)max_chunks);
+  for (int k = 0; k < max_chunks; ++k) lo_chunk_alloc(&chunks[k], L, F, H, B);
+  double* ts = (double*)malloc(sizeof(double) * (size_t)spp);
+  /* RayMarchRecord (renderer.h:34-50) */
+  double *rt = (double*)malloc(sizeof(double) * spp), *rdelta = (double*)malloc(sizeof(double) * spp),
+         *ralpha = (double*)malloc(sizeof(double) * spp), *rtrans = (double*)malloc(sizeof(double) * spp),
+         *rweight = (double*)malloc(sizeof(double) * spp);
+  float *rcolor = (float*)malloc(sizeof(float) * 3 * spp);
+  uint8_t* rinner = (uint8_t*)malloc((size_t)spp);
+  /* RayLossGrad (trainer.h:106-111) */
+  double *g_w = (double*)malloc(sizeof(double) * spp), *g_col = (double*)malloc(sizeof(double) * 3 * spp);
+  float *dsig = (float*)malloc(sizeof(float) * spp), *dcol = (float*)malloc(sizeof(float) * 3 * LO_BATCH);
+  float* work = (float*)malloc(sizeof(float) * (size_t)(1 + 16 + 3 + 16 + 2 * LO_MAX_LEVELS * 8 + 256) *
+                               LO_BATCH * 2);
+  int rc = 0;
+
+  for (int ri = 0; ri < nrays; ++ri) {
+    const lo_train_ray* ray = &rays[ri];
+    if (ray->camera < 0 || ray->camera >= ncams) {
+      rc = -1;
+      break;
+    }
+    const double t_near = cam_tnf[2 * ray->camera], t_far = cam_tnf[2 * ray->camera + 1];
+    if (!(t_near > 0 && t_far > t_near)) { /* renderer.h:134 */
+      rc = -3;
+      break;
+    }
+    double ratio;
+    lo_sample_distances(t_near, t_far, spp, ts, &ratio);
+
+    /* ---- march_ray(record = true) (renderer.h:126-237) ---- */
+    float sh[16];
+    lo_sh_encode(ray->dir, sh);
+    int nchunks = 0, nt = 0, nsig = 0, contributing = 0, evals = 0, terminated = 0;
+    double trans = 1.0, pixel[3] = {0, 0, 0}, depth = 0, opacity = 0;
+    lo_chunk* ck = &chunks[nchunks++];
+    ck->n = 0;
+#define LO_REC_FLUSH(CK)                                                                  \
+  do {                                                                                    \
+    lo_chunk* fc = (CK);                                                                  \
+    if (fc->n > 0) {                                                                      \
+      lo_chunk_forward(m, fc, sh);                                                        \
+      evals += fc->n;                                                                     \
+      const int base = nsig;                                                              \
+      for (int i = 0; i < fc->n; ++i) {                                                   \
+        const int s = base + i;                                                           \
+        const double sigma = (double)fc->sigma[i];                                        \
+        const double a = 1.0 - exp(-sigma * rdelta[s]);                                   \
+        const double w = trans * a;                                                       \
+        for (int c = 0; c < 3; ++c) rcolor[3 * s + c] = fc->color[(size_t)c * fc->n + i]; \
+        ralpha[s] = a;                                                                    \
+        rtrans[s] = trans;                                                                \
+        rweight[s] = w;                                                                   \
+        ++nsig;                                                                           \
+        for (int c = 0; c < 3; ++c) pixel[c] += w * (double)fc->color[(size_t)c * fc->n + i]; \
+        depth += w * rt[s];                                                               \
+        opacity += w;                                                                     \
+        trans *= 1.0 - a;                                                                 \
+        ++contributing;                                                                   \
+        if (opts->termination_transmittance > 0 && trans < opts->termination_transmittance) { \
+          terminated = 1;                                                                 \
+          break;                                                                          \
+        }                                                                                 \
+      }                                                                                   \
+      while (nsig < nt) {                                                                 \
+        const int s = nsig, i = s - base;                                                 \
+        for (int c = 0; c < 3; ++c) rcolor[3 * s + c] = fc->color[(size_t)c * fc->n + i]; \
+        ralpha[s] = 0.0;                                                                  \
+        rtrans[s] = 0.0;                                                                  \
+        rweight[s] = 0.0;                                                                 \
+        ++nsig;                                                                           \
+      }                                                                                   \
+    }                                                                                     \
+  } while (0)
+    for (int i = 0; i < spp && !terminated; ++i) {
+      double pos[3], c[3];
+      lo_ray_at(ray->origin, ray->dir, ts[i], pos);
+      lo_contract(pos, opts->contraction, c);
+      if (!lo_occupied(m, c)) continue;
+      const double delta = (i + 1 < spp) ? ts[i + 1] - ts[i] : ts[i] * (ratio - 1.0);
+      float* w = ck->lodw + (size_t)ck->n * L;
+      if (opts->lod_enabled) {
+        double r_c = lo_contracted_footprint(ray->origin, ray->dir, ray->norigin, ray->ndir, ts[i],
+                                             opts->contraction);
+        double l_star = lo_lod_level(lo_max(r_c, 1e-12), cfg);
+        lo_lod_weights(l_star, opts->lod_bias, L, w);
+      } else {
+        for (int l = 0; l < L; ++l) w[l] = 1.0f;
+      }
+      ck->pos[ck->n][0] = c[0];
+      ck->pos[ck->n][1] = c[1];
+      ck->pos[ck->n][2] = c[2];
+      ck->n++;
+      rt[nt] = ts[i];
+      rdelta[nt] = delta;
+      rinner[nt] = lo_linf(c) <= 1.0 ? 1 : 0;
+      ++nt;
+      if (ck->n >= cs) {
+        LO_REC_FLUSH(ck);
+        if (!terminated) {
+          ck = &chunks[nchunks++];
+          ck->n = 0;
+        }
+      }
+    }
+    if (!terminated) LO_REC_FLUSH(ck);
+#undef LO_REC_FLUSH
+    if (nchunks > 0 && chunks[nchunks - 1].n == 0) --nchunks;
+    const double final_trans = trans;
+    for (int c = 0; c < 3; ++c) pixel[c] += trans * opts->background[c];
+    depth = depth / (opacity + 1e-10);
+    if (ray_evals) ray_evals[ri] = evals;
+    if (ray_contrib) ray_contrib[ri] = contributing;
+
+    /* ---- ray_loss (train_step.h:16-123) ---- */
+    const int n = nt;
+    const double v_raw = 1.0 - alpha_v[ray->camera] * ray->vignette_r;
+    const double v = lo_max(v_raw, 1e-3);
+    const double inv_batch = lc->inv_batch;
+    lo_loss_terms lt = {0, 0, 0, 0, 0};
+    double dpix[3] = {0, 0, 0}, dv_total = 0, d_alpha_v = 0;
+    for (int c = 0; c < 3; ++c) {
+      double pred = v * pixel[c];
+      double diff = pred - ray->gt[c];
+      lt.image += fabs(diff) / 3.0 * inv_batch;
+      double dpred = inv_batch * lo_sgn(diff) / 3.0;
+      dpix[c] = dpred * v;
+      dv_total += dpred * pixel[c];
+    }
+    if (v_raw > 1e-3) d_alpha_v += dv_total * (-ray->vignette_r);
+    for (int i = 0; i < n; ++i) {
+      double gw = 0;
+      for (int c = 0; c < 3; ++c) {
+        double ci = (double)rcolor[(size_t)i * 3 + c];
+        gw += dpix[c] * ci;
+        g_col[(size_t)i * 3 + c] = dpix[c] * rweight[i];
+      }
+      g_w[i] = gw;
+    }
+    const double W = opacity, D = depth, denom = W + 1e-10;
+    double ddepth = 0;
+    if (lc->depth_active && lc->lambda_depth > 0 && ray->gt_depth >= 0) {
+      double diff = D - ray->gt_depth;
+      lt.depth = lc->lambda_depth * fabs(diff) * inv_batch;
+      ddepth = lc->lambda_depth * inv_batch * lo_sgn(diff);
+    }
+    double dvar_dD = 0, Wi = 0, V = 0;
+    if (lc->lambda_dvar > 0) {
+      double S2 = 0;
+      for (int i = 0; i < n; ++i) {
+        if (!rinner[i]) continue;
+        Wi += rweight[i];
+        S2 += rweight[i] * (rt[i] - D) * (rt[i] - D);
+      }
+      if (Wi > 1e-10) {
+        V = S2 / Wi;
+        lt.dvar = lc->lambda_dvar * V * inv_batch;
+        for (int i = 0; i < n; ++i) {
+          if (!rinner[i]) continue;
+          g_w[i] += lc->lambda_dvar * inv_batch * ((rt[i] - D) * (rt[i] - D) - V) / Wi;
+          dvar_dD += -2.0 * rweight[i] * (rt[i] - D) / Wi;
+        }
+        dvar_dD *= lc->lambda_dvar * inv_batch;
+      }
+    }
+    if (lc->lambda_dist > 0) {
+      double A = 0, Bs = 0, val = 0;
+      for (int i = 0; i < n; ++i) {
+        val += rweight[i] * (rt[i] * A - Bs);
+        A += rweight[i];
+        Bs += rweight[i] * rt[i];
+      }
+      val *= 2.0;
+      lt.dist = lc->lambda_dist * val * inv_batch;
+      double A_pre = 0, B_pre = 0;
+      for (int i = 0; i < n; ++i) {
+        double A_suf = A - A_pre - rweight[i];
+        double B_suf = Bs - B_pre - rweight[i] * rt[i];
+        double d = 2.0 * (rt[i] * A_pre - B_pre + B_suf - rt[i] * A_suf);
+        g_w[i] += lc->lambda_dist * inv_batch * d;
+        A_pre += rweight[i];
+        B_pre += rweight[i] * rt[i];
+      }
+    }
+    if (ddepth != 0 || dvar_dD != 0) {
+      double dD_total = ddepth + dvar_dD;
+      for (int i = 0; i < n; ++i) g_w[i] += dD_total * (rt[i] - D) / denom;
+    }
+    lt.total = lt.image + lt.depth + lt.dvar + lt.dist;
+    loss->image += lt.image;
+    loss->depth += lt.depth;
+    loss->dvar += lt.dvar;
+    loss->dist += lt.dist;
+
+    /* ---- backward_ray (train_step.h:127-154) ---- */
+    if (n > 0) {
+      double d_final_trans = 0;
+      for (int c = 0; c < 3; ++c) d_final_trans += dpix[c] * opts->background[c];
+      double suffix = d_final_trans * final_trans; /* composite_backward_sigma, renderer.h:110-120 */
+      for (int i = n - 1; i >= 0; --i) {
+        double d = rdelta[i] * ((1.0 - ralpha[i]) * g_w[i] * rtrans[i] - suffix);
+        dsig[i] = (float)d;
+        suffix += g_w[i] * rweight[i];
+      }
+      int offset = 0;
+      for (int k = 0; k < nchunks; ++k) {
+        const lo_chunk* c = &chunks[k];
+        for (int i = 0; i < c->n; ++i)
+          for (int q = 0; q < 3; ++q)
+            dcol[(size_t)q * c->n + i] = (float)g_col[(size_t)(offset + i) * 3 + q];
+        lo_chunk_backward(m, c, dsig + offset, dcol, g_grid, g_density, g_color, work);
+        offset += c->n;
+      }
+    }
+    alpha_grad[ray->camera] += d_alpha_v;
+  }
+
+  /* trainer.cpp:606-607 (the ray-dependent terms) */
+  loss->total = loss->image + loss->depth + loss->dvar + loss->dist;
+  for (int k = 0; k < max_chunks; ++k) lo_chunk_free(&chunks[k]);
+  free(chunks);
+  free(ts);
+  free(rt);
+  free(rdelta);
+  free(ralpha);
+  free(rtrans);
+  free(rweight);
+  free(rcolor);
+  free(rinner);
+  free(g_w);
+  free(g_col);
+  free(dsig);
+  free(dcol);
+  free(work);
+  return rc;
+}
+
+/* simd::scalar::adam_step (simd.h:106-121) */
+void lo_adam_step(size_t n, float* p, const float* g, float* mom, float* vel, float lr, float beta1,
+                  float beta2, float eps, float c1, float c2) {
+  for (size_t i = 0; i < n; ++i) {
+    float gi = g[i];
+    float mi = beta1 * mom[i] + (1.0f - beta1) * gi;
+    float vi = beta2 * vel[i] + (1.0f - beta2) * gi * gi;
+    mom[i] = mi;
+    vel[i] = vi;
+    float mhat = mi * c1;
+    float vhat = vi * c2;
+    p[i] -= lr * mhat / (sqrtf(vhat) + eps);
+  }
+}

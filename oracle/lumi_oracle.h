@@ -147,6 +147,46 @@ int lo_probe(const lo_model* m, const lo_camera* cams, int ncams, int samples_pe
 void lo_prune(const float* probe_max, const float* history, const uint8_t* carved, size_t n,
               float alpha, uint8_t* occ_out);
 
+/* ---- training reverse path (trainer.cpp:549-569, train_step.h, field.h:141-179) ---- */
+/* TrainRay (trainer.h:90-97): the ray, its right-neighbour ray, target, depth, vignette */
+typedef struct {
+  double origin[3], dir[3];
+  double norigin[3], ndir[3];
+  float gt[3];
+  int32_t camera;
+  double gt_depth; /* < 0: unavailable */
+  double vignette_r;
+} lo_train_ray;
+
+/* the TrainConfig fields ray_loss reads (trainer.h:18-60) + the per-iteration flags */
+typedef struct {
+  double lambda_depth, lambda_dvar, lambda_dist;
+  double inv_batch;
+  int32_t depth_active;
+  int32_t _pad;
+} lo_loss_config;
+
+/* LossTerms (trainer.h:99-102), the ray-dependent part */
+typedef struct {
+  double total, image, depth, dvar, dist;
+} lo_loss_terms;
+
+/* For every ray: march_ray(record = true) + ray_loss + backward_ray, exactly as the
+   training loop (trainer.cpp:549-561).  cam_tnf: [ncams][2] (t_near, t_far); alpha_v:
+   [ncams].  Gradients are ACCUMULATED into g_grid [layout.total_floats], g_density,
+   g_color (FieldGradients, weights-then-bias order) and alpha_grad [ncams]; loss terms are
+   summed over the rays.  ray_evals / ray_contrib (optional, [nrays]) receive
+   rec.t.size() and rec.contributing.  The dense backward replays the scalar order
+   (simd.h:53-90), so it is bit-identical to the reference under LUMI_SIMD=scalar. */
+int lo_train_backward(const lo_model* m, const double* cam_tnf, const double* alpha_v, int ncams,
+                      const lo_train_ray* rays, int nrays, const lo_render_options* opts,
+                      const lo_loss_config* lc, float* g_grid, float* g_density, float* g_color,
+                      double* alpha_grad, lo_loss_terms* loss, int32_t* ray_evals,
+                      int32_t* ray_contrib);
+/* simd::scalar::adam_step (simd.h:106-121) */
+void lo_adam_step(size_t n, float* p, const float* g, float* mom, float* vel, float lr, float beta1,
+                  float beta2, float eps, float c1, float c2);
+
 /* ---- scheduler (scheduler.cpp:18-162) ---- */
 int lo_equal_assignment(int height, int workers, int32_t* rows, double* shares);
 int lo_assign_rows(int height, int n, const double* throughputs, const double* prev_shares,

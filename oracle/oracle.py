@@ -98,6 +98,46 @@ class Model(C.Structure):
     ]
 
 
+class TrainRay(C.Structure):
+    """proj/include/lumi/trainer.h:90-97 (lo_train_ray)."""
+
+    _fields_ = [
+        ("origin", C.c_double * 3),
+        ("dir", C.c_double * 3),
+        ("norigin", C.c_double * 3),
+        ("ndir", C.c_double * 3),
+        ("gt", C.c_float * 3),
+        ("camera", C.c_int32),
+        ("gt_depth", C.c_double),
+        ("vignette_r", C.c_double),
+    ]
+
+
+class LossConfig(C.Structure):
+    """The TrainConfig fields ray_loss reads (trainer.h:18-60) (lo_loss_config)."""
+
+    _fields_ = [
+        ("lambda_depth", C.c_double),
+        ("lambda_dvar", C.c_double),
+        ("lambda_dist", C.c_double),
+        ("inv_batch", C.c_double),
+        ("depth_active", C.c_int32),
+        ("_pad", C.c_int32),
+    ]
+
+
+class LossTerms(C.Structure):
+    """LossTerms (trainer.h:99-102), ray-dependent part."""
+
+    _fields_ = [(k, C.c_double) for k in ("total", "image", "depth", "dvar", "dist")]
+
+
+def loss_config(lambda_depth=0.1, lambda_dvar=0.01, lambda_dist=0.001, inv_batch=1.0,
+                depth_active=True) -> LossConfig:
+    return LossConfig(lambda_depth, lambda_dvar, lambda_dist, inv_batch,
+                      1 if depth_active else 0, 0)
+
+
 def field_config(levels=16, fpl=2, base=128, scale=1.4, table_size=1 << 19, hidden=64,
                  bottleneck=16, color_space=0) -> FieldConfig:
     return FieldConfig(levels, fpl, base, hidden, scale, table_size, bottleneck, color_space, 0)
@@ -184,6 +224,8 @@ class Oracle:
         L.lo_assign_rows.argtypes = [i32, i32, vp, vp, d, vp, vp]
         L.lo_next_assignment.argtypes = [i32, i32, vp, vp, vp, i32, d, vp, vp]
         L.lo_aggregate_stats.argtypes = [vp, i32, vp]
+        L.lo_train_backward.argtypes = [vp, vp, vp, i32, vp, i32, vp, vp] + [vp] * 7
+        L.lo_adam_step.argtypes = [C.c_size_t] + [vp] * 4 + [C.c_float] * 6
 
     # -- model -------------------------------------------------------------
     def layout(self, cfg: FieldConfig) -> GridLayout:
@@ -279,6 +321,43 @@ class Oracle:
         occ = np.zeros(probe_max.size, np.uint8)
         self.lib.lo_prune(_p(probe_max), None, None, probe_max.size, alpha, _p(occ))
         return occ
+
+    # -- training reverse path -------------------------------------------------
+    def _train_args(self, model, cam_tnf, alpha_v, rays, grads):
+        cam_tnf = np.ascontiguousarray(cam_tnf, np.float64).reshape(-1, 2)
+        alpha_v = np.ascontiguousarray(alpha_v, np.float64)
+        nc = cam_tnf.shape[0]
+        if isinstance(rays, np.ndarray):  # structured array with the lo_train_ray layout
+            assert rays.dtype.itemsize == C.sizeof(TrainRay)
+            rays = np.ascontiguousarray(rays)
+            arr = rays.ctypes.data_as(C.c_void_p)
+        else:
+            arr = (TrainRay * len(rays))(*rays)
+        if grads is None:
+            lay = self.layout(model.cfg)
+            nd, ncp = self.param_counts(model.cfg)
+            grads = dict(grid=np.zeros(lay.total_floats, np.float32),
+                         density=np.zeros(nd, np.float32), color=np.zeros(ncp, np.float32),
+                         alpha=np.zeros(nc, np.float64))
+        return cam_tnf, alpha_v, nc, arr, grads
+
+    def train_backward(self, model, cam_tnf, alpha_v, rays, opts, lc, grads=None):
+        """march_ray(record) + ray_loss + backward_ray per ray (trainer.cpp:549-561).
+        Returns (grads dict, LossTerms, evals[n], contributing[n]); grads accumulate."""
+        cam_tnf, alpha_v, nc, arr, grads = self._train_args(model, cam_tnf, alpha_v, rays, grads)
+        loss = LossTerms()
+        ev = np.zeros(len(rays), np.int32)
+        co = np.zeros(len(rays), np.int32)
+        rc = self.lib.lo_train_backward(C.byref(model), _p(cam_tnf), _p(alpha_v), nc, arr,
+                                        len(rays), C.byref(opts), C.byref(lc), _p(grads["grid"]),
+                                        _p(grads["density"]), _p(grads["color"]),
+                                        _p(grads["alpha"]), C.byref(loss), _p(ev), _p(co))
+        if rc:
+            raise ValueError(f"lo_train_backward failed ({rc})")
+        return grads, loss, ev, co
+
+    def adam_step(self, p, g, m, v, lr, beta1, beta2, eps, c1, c2):
+        self.lib.lo_adam_step(p.size, _p(p), _p(g), _p(m), _p(v), lr, beta1, beta2, eps, c1, c2)
 
     # -- scalar helpers ------------------------------------------------------
     def generate_ray(self, cam, px, py):
@@ -394,6 +473,8 @@ class Reference(Oracle):
         L.ref_equal_assignment.argtypes = [i32, i32, vp, vp]
         L.ref_assign_rows.argtypes = [i32, i32, vp, vp, vp, d, vp, vp]
         L.ref_aggregate_stats.argtypes = [vp, i32, vp]
+        L.ref_train_backward.argtypes = [vp, vp, vp, i32, vp, i32, vp, vp] + [vp] * 7
+        L.ref_adam_step.argtypes = [C.c_size_t] + [vp] * 4 + [C.c_float] * 6
 
     def _check(self, rc):
         if rc:
@@ -488,6 +569,21 @@ class Reference(Oracle):
         bg = np.ascontiguousarray(background, np.float64)
         self._check(self.lib.ref_save_checkpoint(model.h, str(path).encode(), spp, _p(bg),
                                                  contraction))
+
+    def train_backward(self, model, cam_tnf, alpha_v, rays, opts, lc, grads=None):
+        cam_tnf, alpha_v, nc, arr, grads = self._train_args(model, cam_tnf, alpha_v, rays, grads)
+        loss = LossTerms()
+        ev = np.zeros(len(rays), np.int32)
+        co = np.zeros(len(rays), np.int32)
+        self._check(self.lib.ref_train_backward(model.h, _p(cam_tnf), _p(alpha_v), nc, arr,
+                                                len(rays), C.byref(opts), C.byref(lc),
+                                                _p(grads["grid"]), _p(grads["density"]),
+                                                _p(grads["color"]), _p(grads["alpha"]),
+                                                C.byref(loss), _p(ev), _p(co)))
+        return grads, loss, ev, co
+
+    def adam_step(self, p, g, m, v, lr, beta1, beta2, eps, c1, c2):
+        self.lib.ref_adam_step(p.size, _p(p), _p(g), _p(m), _p(v), lr, beta1, beta2, eps, c1, c2)
 
     def generate_ray(self, cam, px, py):
         o = np.zeros(3)

@@ -23,6 +23,8 @@
 #include "lumi/scene.h"
 #include "lumi/scheduler.h"
 #include "lumi/simd.h"
+#include "lumi/train_step.h"
+#include "lumi/trainer.h"
 
 #include "lumi_oracle.h"
 
@@ -405,6 +407,74 @@ int ref_aggregate_stats(const double* ms, int n, double out[3]) {
     out[1] = s.std_fps;
     out[2] = s.p99_fps;
   });
+}
+
+// The training loop's per-ray body (trainer.cpp:549-561): march_ray(record = true),
+// ray_loss, backward_ray, accumulated into FieldGradients exactly as train() does.
+int ref_train_backward(void* h, const double* cam_tnf, const double* alpha_v, int ncams,
+                       const lo_train_ray* rays, int nrays, const lo_render_options* o,
+                       const lo_loss_config* lc, float* g_grid, float* g_density, float* g_color,
+                       double* alpha_grad, lo_loss_terms* loss, int32_t* ray_evals,
+                       int32_t* ray_contrib) {
+  return guarded([&] {
+    RefModel& m = *static_cast<RefModel*>(h);
+    RenderOptions opts = to_opts(o);
+    TrainConfig cfg;
+    cfg.lambda_depth = lc->lambda_depth;
+    cfg.lambda_dvar = lc->lambda_dvar;
+    cfg.lambda_dist = lc->lambda_dist;
+    FieldGradients<float> grads = m.field.make_gradients();
+    std::memcpy(grads.grid.data(), g_grid, grads.grid.size() * sizeof(float));
+    std::memcpy(grads.density.data(), g_density, grads.density.size() * sizeof(float));
+    std::memcpy(grads.color.data(), g_color, grads.color.size() * sizeof(float));
+    RayMarchRecord<float> rec;
+    RayLossGrad rg;
+    std::vector<float> scratch, dcol_scratch;
+    LossTerms losses;
+    losses.image = loss->image;
+    losses.depth = loss->depth;
+    losses.dvar = loss->dvar;
+    losses.dist = loss->dist;
+    for (int i = 0; i < nrays; ++i) {
+      const lo_train_ray& r = rays[i];
+      require(r.camera >= 0 && r.camera < ncams, "ref_train_backward: camera index");
+      TrainRay tr;
+      tr.camera = r.camera;
+      tr.ray.origin = {r.origin[0], r.origin[1], r.origin[2]};
+      tr.ray.dir = {r.dir[0], r.dir[1], r.dir[2]};
+      tr.neighbor.origin = {r.norigin[0], r.norigin[1], r.norigin[2]};
+      tr.neighbor.dir = {r.ndir[0], r.ndir[1], r.ndir[2]};
+      for (int c = 0; c < 3; ++c) tr.gt[c] = r.gt[c];
+      tr.gt_depth = r.gt_depth;
+      tr.vignette_r = r.vignette_r;
+      march_ray(m.field, m.grid, tr.ray, tr.neighbor, cam_tnf[2 * r.camera],
+                cam_tnf[2 * r.camera + 1], opts, true, rec);
+      LossTerms lt = ray_loss(rec, tr, alpha_v[r.camera], opts.contraction, cfg,
+                              lc->depth_active != 0, lc->inv_batch, &rg);
+      losses.image += lt.image;
+      losses.depth += lt.depth;
+      losses.dvar += lt.dvar;
+      losses.dist += lt.dist;
+      backward_ray(m.field, rec, rg, opts.background, grads, scratch, dcol_scratch);
+      alpha_grad[r.camera] += rg.d_alpha_v;
+      if (ray_evals) ray_evals[i] = static_cast<int32_t>(rec.t.size());
+      if (ray_contrib) ray_contrib[i] = rec.contributing;
+    }
+    loss->image = losses.image;
+    loss->depth = losses.depth;
+    loss->dvar = losses.dvar;
+    loss->dist = losses.dist;
+    loss->total = losses.image + losses.depth + losses.dvar + losses.dist;
+    std::memcpy(g_grid, grads.grid.data(), grads.grid.size() * sizeof(float));
+    std::memcpy(g_density, grads.density.data(), grads.density.size() * sizeof(float));
+    std::memcpy(g_color, grads.color.data(), grads.color.size() * sizeof(float));
+  });
+}
+
+// simd::adam_step through the active ISA table (simd.h:238-247)
+void ref_adam_step(size_t n, float* p, const float* g, float* mom, float* vel, float lr, float beta1,
+                   float beta2, float eps, float c1, float c2) {
+  simd::adam_step<float>(n, p, g, mom, vel, lr, beta1, beta2, eps, c1, c2);
 }
 
 }  // extern "C"

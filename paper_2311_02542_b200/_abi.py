@@ -73,6 +73,21 @@ class CheckpointInfo(C.Structure):
                 ("color_params", C.c_uint64)]
 
 
+class LossConfig(C.Structure):
+    _fields_ = [("lambda_depth", C.c_double), ("lambda_dvar", C.c_double),
+                ("lambda_dist", C.c_double), ("inv_batch", C.c_double),
+                ("depth_active", C.c_int32), ("_pad", C.c_int32)]
+
+
+class LossTermsDesc(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("total", "image", "depth", "dvar", "dist")]
+
+
+class TrainGrads(C.Structure):
+    _fields_ = [("grid", C.c_void_p), ("density", C.c_void_p), ("color", C.c_void_p),
+                ("alpha_v", C.c_void_p), ("loss", C.c_void_p)]
+
+
 # (name, argtypes) of every exported entry point, in include/lumi_cuda.h order.
 _vp, _i, _d, _u64, _f = C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.c_float
 SIGNATURES = {
@@ -93,6 +108,12 @@ SIGNATURES = {
     "lumi_march_kept_async": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp], C.c_int),
     "lumi_checkpoint_read": ([C.c_char_p, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "lumi_bake_occupancy": ([_vp, _vp, _i, _i, _i, _i, _f, _vp, _vp], C.c_int),
+    "lumi_train_backward_async": ([_vp, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp],
+                                  C.c_int),
+    "lumi_train_backward": ([_vp, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "lumi_adam_step_async": ([_vp, _vp, _vp, _vp, _u64] + [_f] * 6 + [_vp], C.c_int),
+    "lumi_model_device_params": ([_vp, _vp, _vp, _vp], C.c_int),
+    "lumi_model_params_updated": ([_vp], C.c_int),
     "lumi_equal_assignment": ([_i, _i, _vp, _vp], C.c_int),
     "lumi_assign_rows": ([_i, _i, _vp, _vp, _d, _vp, _vp], C.c_int),
     "lumi_next_assignment": ([_i, _i, _vp, _vp, _vp, _i, _d, _vp, _vp], C.c_int),

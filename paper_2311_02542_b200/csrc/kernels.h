@@ -20,6 +20,66 @@ struct BakeParams {
   uint8_t* occ;
 };
 
+// ---- training reverse path (train.cu) ----------------------------------------------------
+// LumiTrainRay (include/lumi_cuda.h), TrainRay (trainer.h:90-97)
+struct LumiTrainRayDev {
+  double origin[3], dir[3];
+  double norigin[3], ndir[3];
+  float gt[3];
+  int32_t camera;
+  double gt_depth;
+  double vignette_r;
+};
+static_assert(sizeof(LumiTrainRayDev) == 128, "LumiTrainRay layout");
+
+// One occupancy-kept sample of a training ray (RayMarchRecord t/delta/inner + FieldChunk
+// pos/lodw, renderer.h:34-50, field.h:30-35)
+struct TrainSample {
+  double c[3];  // contracted position
+  double t, delta;
+  int32_t ray;
+  int32_t lod_full;
+  float lod_frac;
+  uint8_t floor_only, inner, _pad[2];
+};
+
+struct TrainParams {
+  GridDev grid;
+  MlpDev mlp;
+  const uint8_t* occ;
+  int occ_res;
+  int n;  // samples_per_ray
+  int lod_enabled;
+  double lod_bias;
+  double t_cut;
+  double bg[3];
+  int contraction;
+  int chunk;
+  // batch
+  const LumiTrainRayDev* rays;
+  int nrays;
+  int ncams;
+  const double* cam_ts;     // [ncams][n] host-computed exponential distances
+  const double* cam_ratio;  // [ncams]
+  const double* alpha_v;    // [ncams]
+  // loss (TrainConfig, trainer.h:18-60)
+  double lambda_depth, lambda_dvar, lambda_dist, inv_batch;
+  int depth_active;
+  int total;  // kept samples (set by the launcher)
+  // outputs (device, accumulated)
+  float* g_grid;
+  float* g_density;
+  float* g_color;
+  double* alpha_grad;
+  double* loss;  // [total, image, depth, dvar, dist]
+  int32_t* ray_evals;
+  int32_t* ray_contrib;
+};
+
+struct AdamConsts {
+  float lr, beta1, beta2, eps, c1, c2;
+};
+
 }  // namespace lumi_dev
 
 cudaError_t launch_render_simt(const lumi_dev::RenderParams& p, cudaStream_t s);
@@ -37,3 +97,8 @@ cudaError_t launch_render_pk(lumi_dev::RenderParams p, cudaStream_t s, int num_s
                              cudaEvent_t* ev = nullptr);
 cudaError_t launch_to_half(const float* src, void* dst_half, uint64_t n, cudaStream_t s);
 cudaError_t launch_bake(const lumi_dev::BakeParams& p, cudaStream_t s);
+cudaError_t launch_train_backward(lumi_dev::TrainParams p, cudaStream_t s, int num_sms,
+                                  long long* kept_total, long long* eval_total);
+size_t train_backward_smem_bytes();
+cudaError_t launch_adam(float* p, const float* g, float* m, float* v, uint64_t n,
+                        lumi_dev::AdamConsts k, cudaStream_t s);

@@ -708,6 +708,176 @@ int lumi_bake_occupancy(LumiModel* m, const LumiCameraDesc* cams, int ncams, int
   return done(LUMI_OK);
 }
 
+// ---- training reverse path (trainer.cpp:549-561) ------------------------------------------
+
+static_assert(sizeof(LumiTrainRay) == sizeof(lumi_dev::LumiTrainRayDev), "LumiTrainRay layout");
+
+int lumi_train_backward_async(LumiModel* m, const LumiTrainRay* rays, int nrays,
+                              const double* cam_tnf, const double* alpha_v, int ncams,
+                              const LumiRenderOptions* o, const LumiLossConfig* lc,
+                              const LumiTrainGrads* g, int32_t* ray_evals, int32_t* ray_contrib,
+                              void* stream) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  if (!lc || !g || !g->grid || !g->density || !g->color || !g->alpha_v || !g->loss)
+    return fail(LUMI_ERR_INVALID, "train_backward: null loss config or gradient buffer");
+  if (nrays < 0 || (nrays > 0 && !rays)) return fail(LUMI_ERR_INVALID, "train_backward: bad rays");
+  if (ncams < 1 || !cam_tnf || !alpha_v) return fail(LUMI_ERR_INVALID, "train_backward: bad cameras");
+  int rc;
+  if ((rc = check_opts(o))) return rc;
+  for (int c = 0; c < ncams; ++c)  // renderer.h:134
+    if (!(cam_tnf[2 * c] > 0 && cam_tnf[2 * c + 1] > cam_tnf[2 * c]))
+      return fail(LUMI_ERR_INVALID, "march_ray: bad sampling interval");
+  DeviceGuard dg(m->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // grid / MLP / occupancy descriptors through the render parameter block
+  RenderParams rp;
+  LumiCameraDesc dummy{};
+  dummy.rot[0] = dummy.rot[4] = dummy.rot[8] = 1.0;
+  dummy.fx = dummy.fy = 1.0;
+  dummy.width = dummy.height = 1;
+  dummy.t_near = cam_tnf[0];
+  dummy.t_far = cam_tnf[1];
+  if ((rc = make_params(m, &dummy, o, 0, 0, &rp))) return rc;
+  // per-camera exponential distances and step ratios (renderer.h:135-142), host libm
+  const int n = o->samples_per_ray;
+  std::vector<double> host((size_t)ncams * n + 2 * (size_t)ncams);
+  for (int c = 0; c < ncams; ++c) {
+    const double tn = cam_tnf[2 * c], tf = cam_tnf[2 * c + 1];
+    double* ts = host.data() + (size_t)c * n;
+    const double log_ratio = std::log(tf / tn);
+    for (int i = 0; i < n; ++i) ts[i] = tn * std::exp(log_ratio * (static_cast<double>(i) / (n - 1)));
+    ts[0] = tn;
+    ts[n - 1] = tf;
+    host[(size_t)ncams * n + c] = std::pow(tf / tn, 1.0 / (n - 1));
+    host[(size_t)ncams * n + ncams + c] = alpha_v[c];
+  }
+  double* d_cam = nullptr;
+  LUMI_CUDA_TRY(cudaMallocAsync(&d_cam, host.size() * sizeof(double), s));
+  cudaError_t e = cudaMemcpyAsync(d_cam, host.data(), host.size() * sizeof(double),
+                                  cudaMemcpyHostToDevice, s);
+  lumi_dev::TrainParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.grid = rp.grid;
+  p.mlp = rp.mlp;
+  p.occ = rp.occ;
+  p.occ_res = rp.occ_res;
+  p.n = n;
+  p.lod_enabled = rp.lod_enabled;
+  p.lod_bias = rp.lod_bias;
+  p.t_cut = rp.t_cut;
+  for (int c = 0; c < 3; ++c) p.bg[c] = rp.bg[c];
+  p.contraction = rp.contraction;
+  p.chunk = rp.chunk;
+  p.rays = reinterpret_cast<const lumi_dev::LumiTrainRayDev*>(rays);
+  p.nrays = nrays;
+  p.ncams = ncams;
+  p.cam_ts = d_cam;
+  p.cam_ratio = d_cam + (size_t)ncams * n;
+  p.alpha_v = d_cam + (size_t)ncams * n + ncams;
+  p.lambda_depth = lc->lambda_depth;
+  p.lambda_dvar = lc->lambda_dvar;
+  p.lambda_dist = lc->lambda_dist;
+  p.inv_batch = lc->inv_batch;
+  p.depth_active = lc->depth_active;
+  p.g_grid = g->grid;
+  p.g_density = g->density;
+  p.g_color = g->color;
+  p.alpha_grad = g->alpha_v;
+  p.loss = reinterpret_cast<double*>(g->loss);
+  p.ray_evals = ray_evals;
+  p.ray_contrib = ray_contrib;
+  if (e == cudaSuccess) e = launch_train_backward(p, s, m->num_sms, nullptr, nullptr);
+  cudaFreeAsync(d_cam, s);
+  if (e != cudaSuccess) return fail(LUMI_ERR_CUDA, std::string("train_backward: ") + cudaGetErrorString(e));
+  return LUMI_OK;
+}
+
+int lumi_train_backward(LumiModel* m, const LumiTrainRay* rays, int nrays, const double* cam_tnf,
+                        const double* alpha_v, int ncams, const LumiRenderOptions* o,
+                        const LumiLossConfig* lc, const LumiTrainGrads* g, int32_t* ray_evals,
+                        int32_t* ray_contrib) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  if (!g || !g->grid || !g->density || !g->color || !g->alpha_v || !g->loss)
+    return fail(LUMI_ERR_INVALID, "train_backward: null gradient buffer");
+  if (ncams < 1) return fail(LUMI_ERR_INVALID, "train_backward: bad cameras");
+  DeviceGuard dg(m->device);
+  const size_t ng = m->layout.total_floats, nd = m->layout.density_params,
+               nc = m->layout.color_params, nr = (size_t)std::max(nrays, 0);
+  char* buf = nullptr;
+  const size_t bytes = nr * sizeof(LumiTrainRay) + (ng + nd + nc) * sizeof(float) +
+                       ncams * sizeof(double) + sizeof(LumiLossTerms) + 2 * nr * sizeof(int32_t) + 256;
+  LUMI_CUDA_TRY(cudaMalloc(&buf, bytes));
+  auto done = [&](int code) {
+    cudaFree(buf);
+    return code;
+  };
+  LumiTrainRay* d_rays = reinterpret_cast<LumiTrainRay*>(buf);
+  LumiTrainGrads dg_{};
+  dg_.grid = reinterpret_cast<float*>(d_rays + nr);
+  dg_.density = dg_.grid + ng;
+  dg_.color = dg_.density + nd;
+  dg_.alpha_v = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(dg_.color + nc) + 7) & ~static_cast<uintptr_t>(7));
+  dg_.loss = reinterpret_cast<LumiLossTerms*>(dg_.alpha_v + ncams);
+  int32_t* d_ev = reinterpret_cast<int32_t*>(dg_.loss + 1);
+  int32_t* d_co = d_ev + nr;
+  cudaError_t e;
+  if ((nr && (e = cudaMemcpy(d_rays, rays, nr * sizeof(LumiTrainRay), cudaMemcpyHostToDevice))) ||
+      (e = cudaMemcpy(dg_.grid, g->grid, ng * sizeof(float), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(dg_.density, g->density, nd * sizeof(float), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(dg_.color, g->color, nc * sizeof(float), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(dg_.alpha_v, g->alpha_v, ncams * sizeof(double), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(dg_.loss, g->loss, sizeof(LumiLossTerms), cudaMemcpyHostToDevice)))
+    return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(e)));
+  int rc = lumi_train_backward_async(m, d_rays, nrays, cam_tnf, alpha_v, ncams, o, lc, &dg_, d_ev,
+                                     d_co, nullptr);
+  if (rc) return done(rc);
+  if ((e = cudaMemcpy(g->grid, dg_.grid, ng * sizeof(float), cudaMemcpyDeviceToHost)) ||
+      (e = cudaMemcpy(g->density, dg_.density, nd * sizeof(float), cudaMemcpyDeviceToHost)) ||
+      (e = cudaMemcpy(g->color, dg_.color, nc * sizeof(float), cudaMemcpyDeviceToHost)) ||
+      (e = cudaMemcpy(g->alpha_v, dg_.alpha_v, ncams * sizeof(double), cudaMemcpyDeviceToHost)) ||
+      (e = cudaMemcpy(g->loss, dg_.loss, sizeof(LumiLossTerms), cudaMemcpyDeviceToHost)) ||
+      (ray_evals && nr && (e = cudaMemcpy(ray_evals, d_ev, nr * sizeof(int32_t), cudaMemcpyDeviceToHost))) ||
+      (ray_contrib && nr && (e = cudaMemcpy(ray_contrib, d_co, nr * sizeof(int32_t), cudaMemcpyDeviceToHost))))
+    return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(e)));
+  return done(LUMI_OK);
+}
+
+int lumi_adam_step_async(float* params, const float* grads, float* mom, float* vel, uint64_t n,
+                         float lr, float beta1, float beta2, float eps, float c1, float c2,
+                         void* stream) {
+  if (n && (!params || !grads || !mom || !vel)) return fail(LUMI_ERR_INVALID, "adam_step: null buffer");
+  const bool aligned = ((reinterpret_cast<uintptr_t>(params) | reinterpret_cast<uintptr_t>(grads) |
+                         reinterpret_cast<uintptr_t>(mom) | reinterpret_cast<uintptr_t>(vel)) & 15) == 0;
+  if (!aligned) return fail(LUMI_ERR_INVALID, "adam_step: buffers must be 16-byte aligned");
+  lumi_dev::AdamConsts k{lr, beta1, beta2, eps, c1, c2};
+  cudaError_t e = launch_adam(params, grads, mom, vel, n, k, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(LUMI_ERR_CUDA, std::string("adam_step: ") + cudaGetErrorString(e));
+  return LUMI_OK;
+}
+
+int lumi_model_device_params(LumiModel* m, float** table, float** density, float** color) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  if (table) *table = m->d_table;
+  if (density) *density = m->d_dparams;
+  if (color) *color = m->d_cparams;
+  return LUMI_OK;
+}
+
+int lumi_model_params_updated(LumiModel* m) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  DeviceGuard dg(m->device);
+  std::vector<float> dp(m->layout.density_params), cp(m->layout.color_params);
+  LUMI_CUDA_TRY(cudaDeviceSynchronize());
+  LUMI_CUDA_TRY(launch_to_half(m->d_table, m->d_table16, m->layout.total_floats, nullptr));
+  LUMI_CUDA_TRY(cudaMemcpy(dp.data(), m->d_dparams, dp.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  LUMI_CUDA_TRY(cudaMemcpy(cp.data(), m->d_cparams, cp.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  const std::vector<float> fused = fuse_l2_c1(dp.data(), cp.data());
+  LUMI_CUDA_TRY(cudaMemcpy(m->d_fused, fused.data(), fused.size() * sizeof(float), cudaMemcpyHostToDevice));
+  LUMI_CUDA_TRY(cudaDeviceSynchronize());
+  return LUMI_OK;
+}
+
 // ---- scheduler (scheduler.cpp:18-162) -----------------------------------------------------
 
 static void round_rows(const double* shares, int n, int height, int32_t* rows) {

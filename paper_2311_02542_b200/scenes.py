@@ -134,3 +134,51 @@ CONFIGS = {
                  frames=120),
     "C5": Config("C5", "stress: 4Kx4K per eye, dense occupancy", STRESS, 4096, 2),
 }
+
+
+# -- synthetic training batches (the reverse path) ----------------
+def _ray_dir(cam: CameraSpec, px: float, py: float):
+    """generate_ray (proj/src/camera.cpp:10-24): dir = normalize(R * ((px-cx)/fx, (py-cy)/fy, 1))."""
+    x, y = (px - cam.cx) / cam.fx, (py - cam.cy) / cam.fy
+    r = cam.rot
+    d = ((r[0] * x + r[1] * y) + r[2], (r[3] * x + r[4] * y) + r[5], (r[6] * x + r[7] * y) + r[8])
+    n = math.sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2])
+    return (d[0] / n, d[1] / n, d[2] / n)
+
+
+def train_cameras(size: int = 256, count: int = 4):
+    """Training views: `count` poses of the head path at eyebuffer size `size`."""
+    return [pinhole(size, size, *head_pose(i * 120 // max(count, 1))) for i in range(count)]
+
+
+def train_batch(cams, rays_per_camera: int, seed: int = 7, depth_fraction: float = 0.5):
+    """A seeded synthetic TrainRay batch (trainer.h:90-97) as a numpy structured array with
+    the LumiTrainRay / lo_train_ray layout: pixels uniform over each camera, the right
+    neighbour at x + 1.5 (renderer.h:264-265), PQ-space targets uniform in [0, 1), a
+    ground-truth depth on `depth_fraction` of the rays (else -1), vignette radius
+    |p - c| / |c| (the normalised radius trainer.cpp uses)."""
+    import numpy as np
+    from .train import TRAIN_RAY_DTYPE
+
+    rng = np.random.default_rng(seed)
+    out = np.zeros(len(cams) * rays_per_camera, TRAIN_RAY_DTYPE)
+    k = 0
+    for ci, cam in enumerate(cams):
+        px = rng.integers(0, cam.width, rays_per_camera)
+        py = rng.integers(0, cam.height, rays_per_camera)
+        for x, y in zip(px.tolist(), py.tolist()):
+            r = out[k]
+            r["origin"] = cam.origin
+            r["norigin"] = cam.origin
+            r["dir"] = _ray_dir(cam, x + 0.5, y + 0.5)
+            r["ndir"] = _ray_dir(cam, x + 1.5, y + 0.5)
+            r["camera"] = ci
+            k += 1
+        sl = slice(k - rays_per_camera, k)
+        out["gt"][sl] = rng.random((rays_per_camera, 3), dtype=np.float32)
+        has_d = rng.random(rays_per_camera) < depth_fraction
+        out["gt_depth"][sl] = np.where(has_d, rng.uniform(0.3, 3.0, rays_per_camera), -1.0)
+        rx = (px + 0.5 - cam.cx) / cam.cx
+        ry = (py + 0.5 - cam.cy) / cam.cy
+        out["vignette_r"][sl] = np.sqrt(rx * rx + ry * ry) / math.sqrt(2.0)
+    return out
