@@ -49,8 +49,12 @@ constexpr int oD1 = 0, oD2 = oD1 + kHidden * kFeat + kHidden,
 constexpr int oC1 = 0, oC2 = oC1 + kHidden * kIn + kHidden, oC3 = oC2 + kHidden * kHidden + kHidden,
               kColorParams = oC3 + 3 * kHidden + 3;
 
+constexpr int kDensityPad = (kDensityParams + 3) & ~3;  // colour weights start 16-B aligned
+constexpr int kColorPad = (kColorParams + 3) & ~3;
+
 struct Smem {
   float act[kRows * kS];
+  float wts[kDensityPad + kColorPad];  // fp32 parameters, density then colour (network.h:144-151)
   float dW[kDensityParams + kColorParams];  // density then colour
   float dsig[kTile];
   float dcol[3][kTile];
@@ -65,52 +69,69 @@ __device__ __forceinline__ bool occupied(const TrainParams& p, d3 c) {
 __device__ __forceinline__ d3 ld3(const double* v) { return d3{v[0], v[1], v[2]}; }
 
 // ---- march: counts and sample records (renderer.h:205-222) ---------------------------------
-__global__ void __launch_bounds__(128) k_train_count(TrainParams p, int* cnt) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= p.nrays) return;
-  const LumiTrainRayDev& ray = p.rays[r];
-  const double* ts = p.cam_ts + (size_t)ray.camera * p.n;
-  const d3 o = ld3(ray.origin), d = ld3(ray.dir);
-  int k = 0;
-  for (int i = 0; i < p.n; ++i)
-    if (occupied(p, contract(ray_at(o, d, ts[i]), p.contraction))) ++k;
-  cnt[r] = k;
+// One warp per (ray, 32-candidate word): each lane tests one candidate in the exact double
+// geometry, the ballot is the word's kept mask.  A training batch has only ~10^4 rays, so a
+// thread per ray would leave most SMs idle.
+__device__ __forceinline__ uint32_t kept_word(const TrainParams& p, const LumiTrainRayDev& ray,
+                                              const double* ts, int word, int lane) {
+  const int i = word * 32 + lane;
+  bool keep = false;
+  if (i < p.n) keep = occupied(p, contract(ray_at(ld3(ray.origin), ld3(ray.dir), ts[i]), p.contraction));
+  return __ballot_sync(0xffffffffu, keep);
 }
 
-__global__ void __launch_bounds__(128) k_train_samples(TrainParams p, const int* off, TrainSample* out) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= p.nrays) return;
+__global__ void __launch_bounds__(128) k_train_count(TrainParams p, int words, uint32_t* masks, int* cnt) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= (long long)p.nrays * words) return;
+  const int r = (int)(gw / words), word = (int)(gw % words);
+  const LumiTrainRayDev& ray = p.rays[r];
+  const uint32_t m = kept_word(p, ray, p.cam_ts + (size_t)ray.camera * p.n, word, lane);
+  if (lane == 0) {
+    masks[gw] = m;
+    if (m) atomicAdd(cnt + r, __popc(m));
+  }
+}
+
+// one warp per (ray, word): the word's kept candidates get consecutive records after the
+// popcounts of the ray's earlier words
+__global__ void __launch_bounds__(128) k_train_samples(TrainParams p, int words, const uint32_t* masks,
+                                                       const int* off, TrainSample* out) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= (long long)p.nrays * words) return;
+  const int r = (int)(gw / words), word = (int)(gw % words);
+  const uint32_t m = masks[gw];
+  if (!((m >> lane) & 1u)) return;
+  int k = off[r] + __popc(m & ((1u << lane) - 1u));
+  for (int w = 0; w < word; ++w) k += __popc(masks[(long long)r * words + w]);
   const LumiTrainRayDev& ray = p.rays[r];
   const double* ts = p.cam_ts + (size_t)ray.camera * p.n;
   const double ratio = p.cam_ratio[ray.camera];
   const d3 o = ld3(ray.origin), d = ld3(ray.dir), no = ld3(ray.norigin), nd = ld3(ray.ndir);
-  int k = off[r];
-  for (int i = 0; i < p.n; ++i) {
-    const double t = ts[i];
-    const d3 c = contract(ray_at(o, d, t), p.contraction);
-    if (!occupied(p, c)) continue;
-    TrainSample s;
-    s.c[0] = c.x;
-    s.c[1] = c.y;
-    s.c[2] = c.z;
-    s.t = t;
-    s.delta = (i + 1 < p.n) ? dsub(ts[i + 1], t) : dmul(t, dsub(ratio, 1.0));
-    LodW lw{p.grid.levels, 0.f, false};
-    if (p.lod_enabled) {
-      // contracted_footprint (camera.cpp:68-73) with the neighbour's own origin
-      const d3 a = contract(ray_at(o, d, t), p.contraction);
-      const d3 b = contract(ray_at(no, nd, t), p.contraction);
-      const double rc = dmul(0.5, dnorm(d3{dsub(a.x, b.x), dsub(a.y, b.y), dsub(a.z, b.z)}));
-      lw = lod_weights(lod_level(dmax(rc, 1e-12), p.grid.two_base, p.grid.log_scale, p.grid.levels),
-                       p.lod_bias, p.grid.levels);
-    }
-    s.ray = r;
-    s.lod_full = lw.full;
-    s.lod_frac = lw.frac;
-    s.floor_only = lw.floor_only ? 1 : 0;
-    s.inner = dlinf(c) <= 1.0 ? 1 : 0;  // renderer.h:224
-    out[k++] = s;
+  const int i = word * 32 + lane;
+  const double t = ts[i];
+  const d3 c = contract(ray_at(o, d, t), p.contraction);
+  TrainSample s;
+  s.c[0] = c.x;
+  s.c[1] = c.y;
+  s.c[2] = c.z;
+  s.t = t;
+  s.delta = (i + 1 < p.n) ? dsub(ts[i + 1], t) : dmul(t, dsub(ratio, 1.0));
+  LodW lw{p.grid.levels, 0.f, false};
+  if (p.lod_enabled) {
+    // contracted_footprint (camera.cpp:68-73) with the neighbour's own origin
+    const d3 b = contract(ray_at(no, nd, t), p.contraction);
+    const double rc = dmul(0.5, dnorm(d3{dsub(c.x, b.x), dsub(c.y, b.y), dsub(c.z, b.z)}));
+    lw = lod_weights(lod_level(dmax(rc, 1e-12), p.grid.two_base, p.grid.log_scale, p.grid.levels),
+                     p.lod_bias, p.grid.levels);
   }
+  s.ray = r;
+  s.lod_full = lw.full;
+  s.lod_frac = lw.frac;
+  s.floor_only = lw.floor_only ? 1 : 0;
+  s.inner = dlinf(c) <= 1.0 ? 1 : 0;  // renderer.h:224
+  out[k] = s;
 }
 
 __device__ __forceinline__ LodW lodw_of(const TrainSample& s) {
@@ -120,19 +141,62 @@ __device__ __forceinline__ LodW lodw_of(const TrainSample& s) {
 __device__ __forceinline__ d3 ray_dir_of(const TrainParams& p, int r) { return ld3(p.rays[r].dir); }
 
 // ---- forward: sigma and colour of every kept sample (field.h:106-137) ------------------
-__global__ void __launch_bounds__(128) k_train_forward(TrainParams p, const TrainSample* smp, int total,
+// Thread per sample, activations in registers, the fp32 weights staged once per CTA in shared
+// memory (16-B broadcast loads); per output the four-chain fmaf order of mlp_simt.cuh dense().
+template <int OUT, int IN, bool RELU>
+__device__ __forceinline__ void dense_s(const float* W, const float* x, float* y) {
+  const float* b = W + OUT * IN;
+#pragma unroll
+  for (int r = 0; r < OUT; ++r) {
+    const float4* w4 = reinterpret_cast<const float4*>(W + r * IN);
+    float a0 = b[r], a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+    for (int c = 0; c < IN / 4; ++c) {
+      const float4 w = w4[c];
+      a0 = fmaf(w.x, x[4 * c + 0], a0);
+      a1 = fmaf(w.y, x[4 * c + 1], a1);
+      a2 = fmaf(w.z, x[4 * c + 2], a2);
+      a3 = fmaf(w.w, x[4 * c + 3], a3);
+    }
+    const float v = (a0 + a1) + (a2 + a3);
+    y[r] = RELU ? fmaxf(v, 0.f) : v;
+  }
+}
+
+
+__global__ void __launch_bounds__(128, 3) k_train_forward(TrainParams p, const TrainSample* smp, int total,
                                                        float* sig, float* col) {
+  __shared__ __align__(16) float w[kDensityPad + kColorPad];
+  for (int e = threadIdx.x; e < kDensityParams; e += blockDim.x) w[e] = __ldg(p.mlp.dparams + e);
+  for (int e = threadIdx.x; e < kColorParams; e += blockDim.x) w[kDensityPad + e] = __ldg(p.mlp.cparams + e);
+  __syncthreads();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= total) return;
   const TrainSample q = smp[s];
-  float feat[kFeat], sh[16], sigma, rgb[3];
+  float feat[kFeat], h[kHidden], h2[kHidden], dout[1 + kBottleneck], cin[kBottleneck + 16];
   encode(p.grid, d3{q.c[0], q.c[1], q.c[2]}, lodw_of(q), feat);
-  sh_encode(ray_dir_of(p, q.ray), sh);
-  field_mlp(p.mlp, feat, sh, sigma, rgb);
+  const float* dp = w;
+  dense_s<kHidden, kFeat, true>(dp, feat, h);
+  dense_s<1 + kBottleneck, kHidden, false>(dp + kHidden * kFeat + kHidden, h, dout);
+  const float sigma = trunc_exp(dout[0]);
+#pragma unroll
+  for (int i = 0; i < kBottleneck; ++i) cin[i] = dout[1 + i];
+  {
+    float sh[16];
+    sh_encode(ray_dir_of(p, q.ray), sh);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cin[kBottleneck + i] = sh[i];
+  }
+  const float* cp = w + kDensityPad;
+  dense_s<kHidden, kBottleneck + 16, true>(cp, cin, h);
+  cp += kHidden * (kBottleneck + 16) + kHidden;
+  dense_s<kHidden, kHidden, true>(cp, h, h2);
+  cp += kHidden * kHidden + kHidden;
+  float raw[3];
+  dense_s<3, kHidden, false>(cp, h2, raw);
   sig[s] = sigma;
-  col[3 * s + 0] = rgb[0];
-  col[3 * s + 1] = rgb[1];
-  col[3 * s + 2] = rgb[2];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) col[3 * s + k] = p.mlp.color_space == 0 ? sigmoid(raw[k]) : trunc_exp(raw[k]);
 }
 
 __device__ __forceinline__ double sgn(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0); }
@@ -294,42 +358,73 @@ __global__ void __launch_bounds__(128) k_train_compact(TrainParams p, const int*
 
 // ---- backward over 128-sample tiles ------------------------------------------------------
 
-// y[o][s] for o = h, h + 2, ... (the thread pair of sample s splits the rows): the same
-// four-chain fmaf order as mlp_simt.cuh dense(), so activations match k_train_forward.
+// y[o][s] for the output blocks o = 4b .. 4b+3, b = h, h + 2, ... (the thread pair of sample s
+// splits the rows): per output the same four-chain fmaf order as mlp_simt.cuh dense(), so
+// activations match k_train_forward bit for bit; four outputs share every activation load.
+// W: the layer's weights [OUT x IN] then bias [OUT], in shared memory (16-B aligned rows).
 template <int OUT, int IN, bool RELU>
-__device__ __forceinline__ void fwd_layer(const float* __restrict__ W, const float* x, float* y,
-                                          int s, int h) {
-  const float* __restrict__ bias = W + OUT * IN;
+__device__ __forceinline__ void fwd_layer(const float* W, const float* x, float* y, int s, int h) {
+  const float* bias = W + OUT * IN;
+  constexpr int NB = (OUT + 3) / 4;
 #pragma unroll 1
-  for (int o = h; o < OUT; o += 2) {
-    const float4* w4 = reinterpret_cast<const float4*>(W + o * IN);
-    float a0 = __ldg(bias + o), a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 8
-    for (int c = 0; c < IN / 4; ++c) {
-      const float4 w = __ldg(w4 + c);
-      a0 = fmaf(w.x, x[(4 * c + 0) * kS + s], a0);
-      a1 = fmaf(w.y, x[(4 * c + 1) * kS + s], a1);
-      a2 = fmaf(w.z, x[(4 * c + 2) * kS + s], a2);
-      a3 = fmaf(w.w, x[(4 * c + 3) * kS + s], a3);
+  for (int b = h; b < NB; b += 2) {
+    float a[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      a[q][0] = (4 * b + q < OUT) ? bias[4 * b + q] : 0.f;
+      a[q][1] = a[q][2] = a[q][3] = 0.f;
     }
-    const float v = (a0 + a1) + (a2 + a3);
-    y[o * kS + s] = RELU ? fmaxf(v, 0.f) : v;
+#pragma unroll 4
+    for (int c = 0; c < IN / 4; ++c) {
+      const float x0 = x[(4 * c + 0) * kS + s], x1 = x[(4 * c + 1) * kS + s],
+                  x2 = x[(4 * c + 2) * kS + s], x3 = x[(4 * c + 3) * kS + s];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (4 * b + q < OUT) {
+          const float4 w = *reinterpret_cast<const float4*>(W + (4 * b + q) * IN + 4 * c);
+          a[q][0] = fmaf(w.x, x0, a[q][0]);
+          a[q][1] = fmaf(w.y, x1, a[q][1]);
+          a[q][2] = fmaf(w.z, x2, a[q][2]);
+          a[q][3] = fmaf(w.w, x3, a[q][3]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (4 * b + q < OUT) {
+        const float v = (a[q][0] + a[q][1]) + (a[q][2] + a[q][3]);
+        y[(4 * b + q) * kS + s] = RELU ? fmaxf(v, 0.f) : v;
+      }
+    }
   }
 }
 
-// dx[i][s] = sum_o W[o][i] dy[o][s] (dense_backward_data, simd.h:53-64), optionally masked
-// by the ReLU of the layer below (relu_backward, simd.h:85-90: dy = 0 where y <= 0), written
-// over x (each thread owns its sample's column).  Rows i in [0, NI).
+// dx[i][s] = sum_o W[o][i] dy[o][s] (dense_backward_data, simd.h:53-64) for the input blocks
+// i = 4b .. 4b+3 < NI, b = h, h + 2, ..., optionally masked by the ReLU of the layer below
+// (relu_backward, simd.h:85-90: dy = 0 where y <= 0), written over x (each thread owns its
+// sample's column).  One dy load and one 16-B weight load feed four FMAs.
 template <int OUT, int IN, int NI, bool MASK>
-__device__ __forceinline__ void bwd_data(const float* __restrict__ W, const float* dy, float* x,
-                                         float* dx, int s, int h) {
+__device__ __forceinline__ void bwd_data(const float* W, const float* dy, const float* x, float* dx,
+                                         int s, int h) {
 #pragma unroll 1
-  for (int i = h; i < NI; i += 2) {
-    float acc = 0.f;
-#pragma unroll 4
-    for (int o = 0; o < OUT; ++o) acc = fmaf(__ldg(W + o * IN + i), dy[o * kS + s], acc);
-    if (MASK && !(x[i * kS + s] > 0.f)) acc = 0.f;
-    dx[i * kS + s] = acc;
+  for (int b = h; b < NI / 4; b += 2) {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 8
+    for (int o = 0; o < OUT; ++o) {
+      const float d = dy[o * kS + s];
+      const float4 w = *reinterpret_cast<const float4*>(W + o * IN + 4 * b);
+      a0 = fmaf(w.x, d, a0);
+      a1 = fmaf(w.y, d, a1);
+      a2 = fmaf(w.z, d, a2);
+      a3 = fmaf(w.w, d, a3);
+    }
+    float r[4] = {a0, a1, a2, a3};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = 4 * b + q;
+      if (MASK && !(x[i * kS + s] > 0.f)) r[q] = 0.f;
+      dx[i * kS + s] = r[q];
+    }
   }
 }
 
@@ -407,48 +502,60 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_backward(TrainParams p, c
   float* dWd = S.dW;
   float* dWc = S.dW + kDensityParams;
   for (int e = tid; e < kDensityParams + kColorParams; e += kThreads) S.dW[e] = 0.f;
-  const float* dp = p.mlp.dparams;
-  const float* cp = p.mlp.cparams;
+  for (int e = tid; e < kDensityParams; e += kThreads) S.wts[e] = __ldg(p.mlp.dparams + e);
+  for (int e = tid; e < kColorParams; e += kThreads) S.wts[kDensityPad + e] = __ldg(p.mlp.cparams + e);
+  const float* dp = S.wts;
+  const float* cp = S.wts + kDensityPad;
   const int ntiles = (nact + kTile - 1) / kTile;
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int nvalid = min(kTile, nact - tile * kTile);
     __syncthreads();  // previous tile's scatter reads FEAT; dW updates are owner-only
-    // ---- 1. inputs: features (pair thread 0), SH + output gradients (pair thread 1) ----
-    if (h == 0) {
-      float feat[kFeat];
-      if (s < nvalid) {
-        const int si = act[tile * kTile + s];
-        S.sample[s] = si;
+    // ---- 1. inputs: features (levels split over the thread pair), SH and the output
+    //      gradients (pair thread 1) ----
+    {
+      const int si = s < nvalid ? act[tile * kTile + s] : -1;
+      if (h == 0) S.sample[s] = si;
+      if (si >= 0) {
         const TrainSample q = smp[si];
-        encode(p.grid, d3{q.c[0], q.c[1], q.c[2]}, lodw_of(q), feat);
+        const LodW lw = lodw_of(q);
+        const double u = dmul(dadd(q.c[0], 2.0), 0.25), v = dmul(dadd(q.c[1], 2.0), 0.25),
+                     w = dmul(dadd(q.c[2], 2.0), 0.25);
+        for (int l = h; l < kMaxLevels; l += 2) {  // encode (grid.h:90-114), bit-exact
+          float2 f = make_float2(0.f, 0.f);
+          if (l < p.grid.levels) {
+            const float wl = lod_weight_at(lw, l);
+            if (wl > 0.f) f = encode_level(p.grid, l, u, v, w, wl);
+          }
+          X[(rFEAT + 2 * l) * kS + s] = f.x;
+          X[(rFEAT + 2 * l + 1) * kS + s] = f.y;
+        }
       } else {
-        S.sample[s] = -1;
-#pragma unroll
-        for (int f = 0; f < kFeat; ++f) feat[f] = 0.f;
+        for (int l = h; l < kMaxLevels; l += 2) {
+          X[(rFEAT + 2 * l) * kS + s] = 0.f;
+          X[(rFEAT + 2 * l + 1) * kS + s] = 0.f;
+        }
       }
+      if (h == 1) {
+        float sh[16];
+        float ds = 0.f, dc[3] = {0.f, 0.f, 0.f};
+        if (si >= 0) {
+          sh_encode(ray_dir_of(p, smp[si].ray), sh);
+          ds = dsig_g[si];
+          dc[0] = dcol_g[3 * si + 0];
+          dc[1] = dcol_g[3 * si + 1];
+          dc[2] = dcol_g[3 * si + 2];
+        } else {
 #pragma unroll
-      for (int f = 0; f < kFeat; ++f) X[(rFEAT + f) * kS + s] = feat[f];
-    } else {
-      float sh[16];
-      float ds = 0.f, dc[3] = {0.f, 0.f, 0.f};
-      if (s < nvalid) {
-        const int si = act[tile * kTile + s];
-        sh_encode(ray_dir_of(p, smp[si].ray), sh);
-        ds = dsig_g[si];
-        dc[0] = dcol_g[3 * si + 0];
-        dc[1] = dcol_g[3 * si + 1];
-        dc[2] = dcol_g[3 * si + 2];
-      } else {
+          for (int k = 0; k < 16; ++k) sh[k] = 0.f;
+        }
 #pragma unroll
-        for (int k = 0; k < 16; ++k) sh[k] = 0.f;
+        for (int k = 0; k < 16; ++k) X[(rCIN + kBottleneck + k) * kS + s] = sh[k];
+        S.dsig[s] = ds;
+        S.dcol[0][s] = dc[0];
+        S.dcol[1][s] = dc[1];
+        S.dcol[2][s] = dc[2];
       }
-#pragma unroll
-      for (int k = 0; k < 16; ++k) X[(rCIN + kBottleneck + k) * kS + s] = sh[k];
-      S.dsig[s] = ds;
-      S.dcol[0][s] = dc[0];
-      S.dcol[1][s] = dc[1];
-      S.dcol[2][s] = dc[2];
     }
     __syncthreads();
     // ---- 2. forward, activations kept (field.h:106-137) ---------------------------------
@@ -523,29 +630,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_backward(TrainParams p, c
   for (int e = tid; e < kColorParams; e += kThreads) atomicAdd(p.g_color + e, dWc[e]);
 }
 
-// Deterministic sums over rays: loss terms (trainer.cpp:556-559) and the per-camera
-// vignetting gradients (trainer.cpp:562).  One block.
+// Deterministic sums over rays: block 0 the loss terms (trainer.cpp:556-559), block 1 + c the
+// vignetting gradient of camera c (trainer.cpp:562).  Fixed-shape tree reductions.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
 __global__ void __launch_bounds__(256) k_train_reduce(TrainParams p, const double* ray_terms) {
   __shared__ double red[256];
-  for (int k = 0; k < 4; ++k) {
-    double acc = 0;
-    for (int r = threadIdx.x; r < p.nrays; r += 256) acc += ray_terms[5 * (size_t)r + k];
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-      __syncthreads();
+  if (blockIdx.x == 0) {
+    double sums[4];
+    for (int k = 0; k < 4; ++k) {
+      double acc = 0;
+      for (int r = threadIdx.x; r < p.nrays; r += 256) acc += ray_terms[5 * (size_t)r + k];
+      sums[k] = block_sum(acc, red);
     }
-    if (threadIdx.x == 0) p.loss[1 + k] += red[0];
-    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < 4; ++k) p.loss[1 + k] += sums[k];
+      p.loss[0] = ((p.loss[1] + p.loss[2]) + p.loss[3]) + p.loss[4];
+    }
+    return;
   }
-  if (threadIdx.x == 0) p.loss[0] = ((p.loss[1] + p.loss[2]) + p.loss[3]) + p.loss[4];
-  for (int c = threadIdx.x; c < p.ncams; c += 256) {
-    double acc = 0;
-    for (int r = 0; r < p.nrays; ++r)
-      if (p.rays[r].camera == c) acc += ray_terms[5 * (size_t)r + 4];
-    p.alpha_grad[c] += acc;
-  }
+  const int c = blockIdx.x - 1;
+  double acc = 0;
+  for (int r = threadIdx.x; r < p.nrays; r += 256)
+    if (p.rays[r].camera == c) acc += ray_terms[5 * (size_t)r + 4];
+  const double tot = block_sum(acc, red);
+  if (threadIdx.x == 0) p.alpha_grad[c] += tot;
 }
 
 // simd::adam_step (simd.h:106-121), elementwise, float4 body + scalar tail
@@ -607,15 +726,19 @@ cudaError_t launch_train_backward(TrainParams p, cudaStream_t s, int num_sms, lo
   if (p.nrays <= 0) return cudaSuccess;
   const unsigned rb = (unsigned)((p.nrays + 127) / 128);
   Scratch<int> cnt(s), off(s), evals(s), aoff(s);
+  Scratch<uint32_t> masks(s);
+  const int words = (p.n + 31) / 32;
+  const long long march_threads = (long long)p.nrays * words * 32;
+  const unsigned mb = (unsigned)((march_threads + 127) / 128);
   Scratch<uint8_t> tmp(s);
   if ((e = cnt.alloc(p.nrays + 1)) || (e = off.alloc(p.nrays + 1)) || (e = evals.alloc(p.nrays + 1)) ||
-      (e = aoff.alloc(p.nrays + 1)))
+      (e = aoff.alloc(p.nrays + 1)) || (e = masks.alloc((size_t)p.nrays * words)))
     return e;
   size_t tmp_bytes = 0;
   if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt.p, off.p, p.nrays + 1, s))) return e;
   if ((e = tmp.alloc(tmp_bytes))) return e;
-  if ((e = cudaMemsetAsync(cnt.p + p.nrays, 0, sizeof(int), s))) return e;
-  tr::k_train_count<<<rb, 128, 0, s>>>(p, cnt.p);
+  if ((e = cudaMemsetAsync(cnt.p, 0, sizeof(int) * (p.nrays + 1), s))) return e;
+  tr::k_train_count<<<mb, 128, 0, s>>>(p, words, masks.p, cnt.p);
   if ((e = cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, cnt.p, off.p, p.nrays + 1, s))) return e;
   int total = 0;
   if ((e = cudaMemcpyAsync(&total, off.p + p.nrays, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
@@ -632,7 +755,7 @@ cudaError_t launch_train_backward(TrainParams p, cudaStream_t s, int num_sms, lo
       (e = dcol.alloc(3 * T)) || (e = wbuf.alloc(4 * T)) || (e = terms.alloc(5 * (size_t)p.nrays)) ||
       (e = act.alloc(T)))
     return e;
-  tr::k_train_samples<<<rb, 128, 0, s>>>(p, off.p, smp.p);
+  tr::k_train_samples<<<mb, 128, 0, s>>>(p, words, masks.p, off.p, smp.p);
   if (total > 0) tr::k_train_forward<<<(unsigned)((total + 127) / 128), 128, 0, s>>>(p, smp.p, total, sig.p, col.p);
   if ((e = cudaMemsetAsync(evals.p + p.nrays, 0, sizeof(int), s))) return e;
   tr::k_train_loss<<<rb, 128, 0, s>>>(p, off.p, cnt.p, smp.p, sig.p, col.p, wbuf.p, evals.p, dsig.p,
@@ -657,7 +780,7 @@ cudaError_t launch_train_backward(TrainParams p, cudaStream_t s, int num_sms, lo
     tr::k_train_backward<<<std::min(tiles, num_sms), tr::kThreads, smem, s>>>(p, smp.p, act.p, nact,
                                                                               dsig.p, dcol.p);
   }
-  tr::k_train_reduce<<<1, 256, 0, s>>>(p, terms.p);
+  tr::k_train_reduce<<<1 + p.ncams, 256, 0, s>>>(p, terms.p);
   return cudaGetLastError();
 }
 
