@@ -16,6 +16,7 @@
 #include <cstring>
 #include <atomic>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -152,6 +153,21 @@ int check_opts(const LumiRenderOptions* o) {
 
 constexpr unsigned kCounterSlots = 64;
 
+// One host-buffer render_rows call's device resources (reused across calls).
+struct Staging {
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  void* buf = nullptr;
+  size_t bytes = 0;
+  ~Staging() {
+    if (s) cudaStreamSynchronize(s);
+    cudaFree(buf);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
 struct LumiModel {
   int device = 0;
   LumiFieldDesc desc{};
@@ -172,6 +188,7 @@ struct LumiModel {
   bool timing = false;
   std::vector<std::array<cudaEvent_t, 3>> ev_pool;  // [march start, render start, render end]
   size_t ev_used = 0;
+  std::vector<std::unique_ptr<Staging>> staging;  // lumi_render_rows slots
 };
 
 namespace {
@@ -471,6 +488,7 @@ int lumi_model_destroy(LumiModel* m) {
   for (auto& kv : m->ts_cache) cudaFree(kv.second.first);
   for (auto& a : m->ev_pool)
     for (auto x : a) cudaEventDestroy(x);
+  m->staging.clear();
   delete m;
   return LUMI_OK;
 }
@@ -577,60 +595,79 @@ int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOp
   DeviceGuard dg(m->device);
   const int W = cam->width, rows = e - b;
   const size_t plane = static_cast<size_t>(W) * rows;
-  cudaStream_t s;
-  LUMI_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  float* d_buf = nullptr;
-  int64_t* d_rows = nullptr;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
+  const int nplanes = 3 + (depth ? 1 : 0) + (opacity ? 1 : 0);
+  // a staging slot (stream, events, device planes) from the model's pool: concurrent
+  // run_frame workers each take their own; slots are reused across calls
+  std::unique_ptr<Staging> st;
+  {
+    std::lock_guard<std::mutex> lk(m->mu);
+    if (!m->staging.empty()) {
+      st = std::move(m->staging.back());
+      m->staging.pop_back();
+    }
+  }
+  if (!st) {
+    st.reset(new Staging());
+    LUMI_CUDA_TRY(cudaStreamCreateWithFlags(&st->s, cudaStreamNonBlocking));
+    LUMI_CUDA_TRY(cudaEventCreate(&st->e0));
+    LUMI_CUDA_TRY(cudaEventCreate(&st->e1));
+  }
   auto done = [&](int code) {
-    cudaStreamSynchronize(s);
-    cudaFree(d_buf);
-    cudaFree(d_rows);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaStreamDestroy(s);
+    cudaStreamSynchronize(st->s);
+    std::lock_guard<std::mutex> lk(m->mu);
+    m->staging.push_back(std::move(st));
     return code;
   };
+  const size_t need = plane * nplanes * sizeof(float) + rows * sizeof(int64_t) + 256;
   cudaError_t ce;
-  if ((ce = cudaMallocAsync(&d_buf, plane * 5 * sizeof(float), s)) != cudaSuccess ||
-      (ce = cudaMallocAsync(&d_rows, rows * sizeof(int64_t), s)) != cudaSuccess ||
-      (ce = cudaMemsetAsync(d_rows, 0, rows * sizeof(int64_t), s)) != cudaSuccess)
+  if (st->bytes < need) {
+    cudaFree(st->buf);
+    st->buf = nullptr;
+    st->bytes = 0;
+    if ((ce = cudaMalloc(&st->buf, need)) != cudaSuccess)
+      return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+    st->bytes = need;
+  }
+  cudaStream_t s = st->s;
+  float* d_buf = static_cast<float*>(st->buf);
+  int64_t* d_rows = reinterpret_cast<int64_t*>(d_buf + plane * nplanes + 64);
+  if ((ce = cudaMemsetAsync(d_rows, 0, rows * sizeof(int64_t), s)) != cudaSuccess)
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+  float* d_depth = depth ? d_buf + 3 * plane : nullptr;
+  float* d_opac = opacity ? d_buf + (3 + (depth ? 1 : 0)) * plane : nullptr;
   LumiFrameTarget t{};
   t.rgb = d_buf;
-  t.depth = d_buf + 3 * plane;
-  t.opacity = d_buf + 4 * plane;
+  t.depth = d_depth;
+  t.opacity = d_opac;
   t.row_evals = d_rows - b;  // indexed by camera row
   t.width = W;
   t.height = rows;
   t.row_offset = -b;
-  cudaEventRecord(e0, s);
+  cudaEventRecord(st->e0, s);
   if ((rc = lumi_render_rows_async(m, cam, o, b, e, &t, s))) return done(rc);
-  cudaEventRecord(e1, s);
+  cudaEventRecord(st->e1, s);
   const size_t full = static_cast<size_t>(W) * cam->height;
   for (int c = 0; c < 3; ++c)
     if ((ce = cudaMemcpyAsync(out + c * full + static_cast<size_t>(b) * W, d_buf + c * plane,
                               plane * sizeof(float), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
       return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
   if (depth &&
-      (ce = cudaMemcpyAsync(depth + static_cast<size_t>(b) * W, d_buf + 3 * plane,
-                            plane * sizeof(float), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      (ce = cudaMemcpyAsync(depth + static_cast<size_t>(b) * W, d_depth, plane * sizeof(float),
+                            cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
   if (opacity &&
-      (ce = cudaMemcpyAsync(opacity + static_cast<size_t>(b) * W, d_buf + 4 * plane,
-                            plane * sizeof(float), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-    return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
-  std::vector<int64_t> row_ev(rows);
-  if ((ce = cudaMemcpyAsync(row_ev.data(), d_rows, rows * sizeof(int64_t),
+      (ce = cudaMemcpyAsync(opacity + static_cast<size_t>(b) * W, d_opac, plane * sizeof(float),
                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+  std::vector<int64_t> row_ev(stats ? rows : 0);
+  if (stats && (ce = cudaMemcpyAsync(row_ev.data(), d_rows, rows * sizeof(int64_t),
+                                     cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
   if ((ce = cudaStreamSynchronize(s)) != cudaSuccess)
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
   if (stats) {
     float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventElapsedTime(&ms, st->e0, st->e1);
     for (int y = b; y < e; ++y) {
       // The device renders all rows in one launch; the row share of the launch time is
       // reported (renderer.h:272-276 measures each row on the CPU).

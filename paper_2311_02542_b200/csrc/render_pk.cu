@@ -47,6 +47,7 @@ constexpr int kPairs = LUMI_PK_PAIRS;  // (sample, level) pairs per lane per gat
 // per-phase warp-cycles (instrumented builds only): fill, geometry, gather, CTA sync, MLP,
 // composite, round barrier
 __device__ unsigned long long g_phase_cycles_pk[7];
+__device__ unsigned long long g_counts_pk[4];  // warp-rounds, rows, gather passes, pairs
 #endif
 
 // UMMA no-swizzle operands need 16-byte alignment only; the struct is used straight from
@@ -62,6 +63,8 @@ struct __align__(16) Smem {
   float4 res[kThreads];     // per row: sigma, r, g, b (row lane -> owner lane)
   uint32_t ballot[kWarps][32];   // per warp: lanes with candidate bit i of the current word
   uint16_t prefix[kWarps][33];   // exclusive prefix of popc(ballot[i])
+  uint32_t own[kWarps][32];      // per ray lane: the rows of this round holding its samples
+  uint16_t rowcand[kWarps][32];  // per row: its candidate index
   uint64_t mbar;
   uint32_t tmem_base;
   uint4 lvl[kMaxLevels];         // per level: res, hash mask (0 = dense), pair offset, (float)res
@@ -207,7 +210,6 @@ struct Ray {
   bool valid, alive;  // pixel inside the range / still compositing
   int x, y, id;
   float3 d, nd;       // fp32 directions for the network-input geometry
-  uint32_t todo;      // kept candidates of the current word not yet composited
   int kept_total, contributing;
   bool term;
   double trans, px, py, pz, depth, opac;
@@ -293,10 +295,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
 #endif
 
   for (;;) {
-    // ---- A: this warp's 32 rows: the next samples of its packet stream --------------------
-    int take = 0, g0 = 0;
-    while (!no_more) {
+    // ---- A: this warp's 32 rows: the next samples of its packet stream, across as many
+    //      mask words as it takes to fill the round (a round never mixes packets) ---------
+    int take = 0;     // rows filled this round
+    int ci = 0, rl = lane, cand = 0;  // this row lane's candidate slot / ray lane / candidate
+    while (take < 32 && !no_more) {
       if (!packet_live) {
+        if (take > 0) break;
         long long pkt = 0;
         if (lane == 0) pkt = (long long)atomicAdd(p.work_counter, 1u);
         pkt = __shfl_sync(FULL, pkt, 0);
@@ -323,19 +328,29 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
         r.term = false;
         r.trans = 1.0;
         r.px = r.py = r.pz = r.depth = r.opac = 0.0;
-        r.todo = 0;
         packet_live = true;
         word = -1;
         g_next = word_total = 0;
       }
       if (g_next < word_total) {
-        take = min(32, word_total - g_next);
-        g0 = g_next;
-        g_next += take;
-        break;
+        // rows [take, take + n) <- stream positions [g_next, g_next + n) of the current word
+        const int n = min(32 - take, word_total - g_next);
+        if (lane >= take && lane < take + n) {
+          const int g = g_next + (lane - take);
+          int lo = 0;  // largest i with prefix[i] <= g
+#pragma unroll
+          for (int st = 16; st > 0; st >>= 1)
+            if (s.prefix[warp][lo + st] <= g) lo += st;
+          ci = lo;
+          rl = nth_set_bit(s.ballot[warp][ci], g - s.prefix[warp][ci]);
+          cand = word * 32 + ci;
+        }
+        take += n;
+        g_next += n;
+        continue;
       }
-      // next word: the alive rays' kept candidates, candidate-major prefix sums
       if (word + 1 >= p.mask_words) {
+        if (take > 0) break;  // composite this round first; the pixels are stored next round
         // packet exhausted: owners store their pixels (renderer.h:233-236, 267-276)
         if (r.valid) {
           RayResult res{r.px, r.py, r.pz, r.depth, r.opac,
@@ -348,7 +363,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
       }
       ++word;
       const uint32_t bits = r.alive ? __ldg(p.kept_mask + (size_t)word * p.total_rays + r.id) : 0u;
-      r.todo = bits;
       int run = 0;
       for (int i = 0; i < 32; ++i) {
         const uint32_t b = __ballot_sync(FULL, (bits >> i) & 1u);
@@ -365,23 +379,22 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     }
     PT_MARK(0);
 
-    // row lane: its (candidate, ray lane) and network-input geometry
+    // row lane: its ray and network-input geometry
     const bool have = lane < take;
-    int ci = 0, rl = lane;
-    if (have) {
-      const int g = g0 + lane;
-      int lo = 0;  // largest i with prefix[i] <= g
-#pragma unroll
-      for (int st = 16; st > 0; st >>= 1)
-        if (s.prefix[warp][lo + st] <= g) lo += st;
-      ci = lo;
-      rl = nth_set_bit(s.ballot[warp][ci], g - s.prefix[warp][ci]);
+    {  // owner lanes learn which rows of the round hold their ray's samples
+      s.own[warp][lane] = 0u;
+      __syncwarp();
+      const unsigned same = __match_any_sync(FULL, have ? rl : 32 + lane);
+      if (have) {
+        s.own[warp][rl] = same;
+        s.rowcand[warp][lane] = (uint16_t)cand;
+      }
+      __syncwarp();
     }
     const float dx = __shfl_sync(FULL, r.d.x, rl), dy = __shfl_sync(FULL, r.d.y, rl),
                 dz = __shfl_sync(FULL, r.d.z, rl);
     const float nx = __shfl_sync(FULL, r.nd.x, rl), ny = __shfl_sync(FULL, r.nd.y, rl),
                 nz = __shfl_sync(FULL, r.nd.z, rl);
-    const int cand = word * 32 + ci;
     float u = 0.f, v = 0.f, w = 0.f;
     LodW lw{0, 0.f, false};
     int na = 0;
@@ -425,6 +438,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
       }
       __syncwarp();
       uint8_t* Abase = s.A + (warp * 32 / 8) * (kAch * 128);
+#ifdef LUMI_PHASE_TIMING
+      if (lane == 0) {
+        atomicAdd(&g_counts_pk[2], (unsigned long long)((npairs + 32 * kPairs - 1) / (32 * kPairs)));
+        atomicAdd(&g_counts_pk[3], (unsigned long long)npairs);
+      }
+#endif
 #pragma unroll 1
       for (int base = 0; base < npairs; base += 32 * kPairs) {
         uint32_t code[kPairs];
@@ -455,6 +474,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     }
     ptx::fence_async_smem();
     PT_MARK(2);
+#ifdef LUMI_PHASE_TIMING
+    if (lane == 0) {
+      atomicAdd(&g_counts_pk[0], 1ull);
+      atomicAdd(&g_counts_pk[1], (unsigned long long)take);
+    }
+#endif
     if (!__syncthreads_or(have)) {
       if (__syncthreads_and(no_more)) break;  // every warp's stream is exhausted
       continue;
@@ -542,15 +567,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
 
     PT_MARK(4);
     // ---- C: owners composite their samples of this round, in order (renderer.h:170-190) ---
-    if (r.alive && take > 0) {
-      const unsigned lt = (1u << lane) - 1u;
-      while (r.todo) {
-        const int i = __ffs(r.todo) - 1;
-        const int g = s.prefix[warp][i] + __popc(s.ballot[warp][i] & lt);
-        if (g >= g0 + take) break;  // later rounds
-        r.todo &= r.todo - 1;
-        const float4 e = s.res[warp * 32 + (g - g0)];
-        const int cnd = word * 32 + i;
+    {
+      uint32_t mine = s.own[warp][lane];
+      while (mine && r.alive) {
+        const int j = __ffs(mine) - 1;  // rows are in stream order: increasing candidate
+        mine &= mine - 1;
+        const float4 e = s.res[warp * 32 + j];
+        const int cnd = s.rowcand[warp][j];
         const double t = __ldg(p.ts + cnd);
         const double delta = (cnd + 1 < p.n) ? dsub(__ldg(p.ts + cnd + 1), t) : dmul(t, dsub(p.ratio, 1.0));
         const double a = dsub(1.0, exp(dmul(-(double)e.x, delta)));
@@ -565,8 +588,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
         if (p.t_cut > 0 && r.trans < p.t_cut) {
           r.term = true;
           r.alive = false;
-          r.todo = 0;
-          break;
         }
       }
     }
@@ -645,6 +666,7 @@ cudaError_t launch_render_pk(RenderParams p, cudaStream_t s, int num_sms, cudaEv
 #ifdef LUMI_PHASE_TIMING
   unsigned long long zero7[7] = {0, 0, 0, 0, 0, 0, 0};
   cudaMemcpyToSymbolAsync(pk::g_phase_cycles_pk, zero7, sizeof(zero7), 0, cudaMemcpyHostToDevice, s);
+  cudaMemcpyToSymbolAsync(pk::g_counts_pk, zero7, 4 * sizeof(unsigned long long), 0, cudaMemcpyHostToDevice, s);
 #endif
   pk::k_render_pk<<<(unsigned)grid, pk::kThreads, smem, s>>>(p);
   if (ev) cudaEventRecord(ev[2], s);
@@ -659,6 +681,12 @@ cudaError_t launch_render_pk(RenderParams p, cudaStream_t s, int num_sms, cudaEv
                  "composite %.1f roundbar %.1f\n", 100 * pc[0] / tot, 100 * pc[1] / tot,
                  100 * pc[2] / tot, 100 * pc[3] / tot, 100 * pc[4] / tot, 100 * pc[5] / tot,
                  100 * pc[6] / tot);
+    unsigned long long cn[4];
+    cudaMemcpyFromSymbolAsync(cn, pk::g_counts_pk, sizeof(cn), 0, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "[lumi] pk counts: warp-rounds %llu rows %llu (fill %.3f) gather passes %llu "
+                 "pairs %llu (lane use %.3f)\n", cn[0], cn[1], cn[1] / (32.0 * cn[0]), cn[2], cn[3],
+                 cn[3] / (64.0 * cn[2]));
   }
 #endif
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
