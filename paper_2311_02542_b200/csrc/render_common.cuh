@@ -132,4 +132,66 @@ __device__ __forceinline__ void add_work_stats(const RenderParams& p, unsigned l
   }
 }
 
+// OccupancyGrid::is_occupied of a contracted point (occupancy.h:50-53), exact double.
+__device__ __forceinline__ bool occupied_exact(const RenderParams& p, d3 c) {
+  const int64_t vi = voxel_index(c, p.occ_res);
+  return vi >= 0 && __ldg(p.occ + vi) != 0;
+}
+
+// The occupancy test of one candidate decided in fp32 with a certified error bound:
+//
+// x = o + d t in fp32 differs from the exact value by at most ex = 8 * 2^-24 * (|o| + t)
+// (o, d, t rounded to fp32 plus one FMA rounding, 2x slack).  The contraction
+// (camera.cpp:34-49) is 1-Lipschitz up to 2/max(1, m), so the contracted point is off by at
+// most ec = 2 ex / max(1, m) + 2^-21 (reciprocal and product roundings), and the voxel
+// coordinate g = (c + 2) * res / 4 by eg = res/4 * ec + res * 2^-23.  If every axis of g is
+// further than 4 eg from an integer, floor(g) -- hence the voxel and its occupancy bit, and
+// the domain test for the uncontracted mode -- equals the double computation's.  The
+// contraction's max-axis choice is discontinuous at ties (|x_i| == |x_j| == m), so a second
+// axis within 4 ex of the max is also undecided.  ~1e-3 of candidates are undecided; the
+// warp re-tests them cooperatively in double (below), so a rare fallback never serialises
+// a whole warp behind one lane.
+// Returns 0 (empty), 1 (occupied) or 2 (undecided in fp32).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ int occupied_filtered(const RenderParams& p, float3 of, float3 df,
+                                                 float onorm, float tf) {
+  const float x = fmaf(df.x, tf, of.x), y = fmaf(df.y, tf, of.y), z = fmaf(df.z, tf, of.z);
+  const float ax = fabsf(x), ay = fabsf(y), az = fabsf(z);
+  const float m = fmaxf(ax, fmaxf(ay, az));
+  const float ex = 4.76837158e-07f * (onorm + tf);  // 8 * 2^-24 * (|o| + t)
+  const bool contract = p.contraction != 0 && m > 1.f;
+  const float inv = contract ? rcp_approx(m) : 1.f;  // ~1 ulp, inside the 2^-21 term
+  const float mapped = 2.f - inv;
+  // the reference maps the FIRST axis with |x_i| == m (camera.cpp:42-47)
+  const bool isx = ax == m, isy = !isx && ay == m, isz = !isx && !isy;
+  const float cx = contract && isx ? copysignf(mapped, x) : x * inv;
+  const float cy = contract && isy ? copysignf(mapped, y) : y * inv;
+  const float cz = contract && isz ? copysignf(mapped, z) : z * inv;
+  const float m2 = isx ? fmaxf(ay, az) : (isy ? fmaxf(ax, az) : fmaxf(ax, ay));
+  const float res = (float)p.occ_res, q = 0.25f * res;
+  const float ec = 2.f * ex * inv + 4.76837158e-07f;
+  const float eps = 4.f * (q * ec + res * 1.1920929e-07f);
+  const float gx = fmaf(cx, q, 2.f * q), gy = fmaf(cy, q, 2.f * q), gz = fmaf(cz, q, 2.f * q);
+  // Rounding by the 1.5 * 2^23 magic constant keeps the whole test on the FMA/ALU pipes
+  // (no FRND/F2I on the narrow XU pipe): |g - rint(g)| is the distance to the nearest voxel
+  // boundary, and rint(g - 1/2) = floor(g) for every certified g.
+  constexpr float kMagic = 12582912.f;
+  const float rx = __fsub_rn(__fadd_rn(gx, kMagic), kMagic), ry = __fsub_rn(__fadd_rn(gy, kMagic), kMagic),
+              rz = __fsub_rn(__fadd_rn(gz, kMagic), kMagic);
+  const float dmin = fminf(fabsf(gx - rx), fminf(fabsf(gy - ry), fabsf(gz - rz)));
+  if (dmin <= eps || (contract && m - m2 <= 4.f * ex)) return 2;
+  if (fminf(gx, fminf(gy, gz)) < 0.f || fmaxf(gx, fmaxf(gy, gz)) > res) return 0;
+  const uint32_t r = (uint32_t)p.occ_res;  // res^3 < 2^32 (checked on the host)
+  const uint32_t ix = (uint32_t)(__float_as_int(__fadd_rn(gx - 0.5f, kMagic)) - 0x4B400000),
+                 iy = (uint32_t)(__float_as_int(__fadd_rn(gy - 0.5f, kMagic)) - 0x4B400000),
+                 iz = (uint32_t)(__float_as_int(__fadd_rn(gz - 0.5f, kMagic)) - 0x4B400000);
+  return __ldg(p.occ + ((iz * r + iy) * r + ix)) != 0 ? 1 : 0;
+}
+
+
 }  // namespace lumi_dev
