@@ -67,7 +67,7 @@ struct __align__(16) Smem {
   uint16_t rowcand[kWarps][32];  // per row: its candidate index
   uint64_t mbar;
   uint32_t tmem_base;
-  uint4 lvl[kMaxLevels];         // per level: res, hash mask (0 = dense), pair offset, (float)res
+  uint4 lvl[kMaxLevels];         // per level: res, hash mask (0 = dense), level base address (lo, hi)
   float4 samp[kWarps][32];       // per row: grid coordinates u, v, w and the LOD fraction
   uint16_t pairs[kWarps][32 * kMaxLevels];  // (sample, level) gather list: row | l<<5 | class<<9
 };
@@ -161,19 +161,20 @@ __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane)
 }
 
 // One hash-grid level of one sample from the fp16 table (grid.h:96-113, 144-167): fp32 grid
-// coordinates, 32-bit entry indices off the level's pair offset, fp16 trilinear weights
+// coordinates, 32-bit entry indices off the level's base address, fp16 trilinear weights
 // (HMUL2) accumulated in fp32 by FHFMA in two interleaved chains per feature.
-__device__ __forceinline__ float2 gather_level(const __half2* __restrict__ t16, uint4 L, float u,
-                                               float v, float s, float wl) {
+__device__ __forceinline__ float2 gather_level(uint4 L, float u, float v, float s, float wl) {
   const int res = (int)L.x;
-  const float r = __uint_as_float(L.w);
+  const float r = (float)res;
+  const __half2* __restrict__ base =
+      reinterpret_cast<const __half2*>(((unsigned long long)L.w << 32) | L.z);  // level's first pair
   const float pu = u * r, pv = v * r, ps = s * r;
   const int iu = min((int)pu, res - 1), iv = min((int)pv, res - 1), is = min((int)ps, res - 1);
   uint32_t idx[8];
   corner_indices(L.y == 0u, iu, iv, is, (uint32_t)res + 1u, L.y, idx);
   __half2 e[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) e[k] = __ldg(t16 + (L.z + idx[k]));
+  for (int k = 0; k < 8; ++k) e[k] = __ldg(base + idx[k]);  // one IMAD.WIDE per corner
   const float fu = pu - (float)iu, fv = pv - (float)iv, fs = ps - (float)is;
   const __half2 hu = __floats2half2_rn(1.f - fu, fu);
   const __half2 w0 = __hmul2(hu, __float2half2_rn(1.f - fv));
@@ -189,6 +190,13 @@ __device__ __forceinline__ float2 gather_level(const __half2* __restrict__ t16, 
   }
   return make_float2((a[0] + a[1]) * wl, (b[0] + b[1]) * wl);
 }
+
+// trunc_exp / sigmoid (network.h:41-57) with the MUFU exp2 / reciprocal: ~2 ulp, far below the
+// fp16 MLP operands' 1.6e-4 (oracle-measured)
+__device__ __forceinline__ float trunc_exp_fast(float x) {
+  return x <= 10.f ? __expf(x) : 22026.4657948f * (1.f + (x - 10.f));
+}
+__device__ __forceinline__ float sigmoid_fast(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
 
 // position of the (k+1)-th set bit of m (k < popc(m))
 __device__ __forceinline__ int nth_set_bit(uint32_t m, int k) {
@@ -240,8 +248,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
   for (int l = tid; l < kMaxLevels; l += kThreads) {
     const int res = l < p.grid.levels ? p.grid.res[l] : 1;
     const bool dense = (p.grid.dense_mask >> l) & 1u;
-    s.lvl[l] = make_uint4((uint32_t)res, dense ? 0u : p.grid.hash_mask[l],
-                          (uint32_t)p.grid.offset2[l], __float_as_uint((float)res));
+    const unsigned long long base =
+        reinterpret_cast<unsigned long long>(p.grid.table16 + (l < p.grid.levels ? p.grid.offset2[l] : 0));
+    s.lvl[l] = make_uint4((uint32_t)res, dense ? 0u : p.grid.hash_mask[l], (uint32_t)base,
+                          (uint32_t)(base >> 32));
   }
   if (tid == 0) {
     ptx::mbar_init(&s.mbar, 1);
@@ -460,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
             const float4 P = s.samp[warp][code[q] & 31u];
             const uint32_t cls = code[q] >> 9;
             const float wl = cls == 0u ? 1.f : (cls == 1u ? P.w : 1e-4f);
-            f[q] = gather_level(p.grid.table16, s.lvl[(code[q] >> 5) & 15u], P.x, P.y, P.z, wl);
+            f[q] = gather_level(s.lvl[(code[q] >> 5) & 15u], P.x, P.y, P.z, wl);
           }
         }
 #pragma unroll
@@ -526,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     ptx::tc_fence_after();
     ptx::tmem_ld16(t_lane + 64, v32);
     ptx::tmem_ld_wait();
-    const float sigma = trunc_exp(v32[0]);
+    const float sigma = trunc_exp_fast(v32[0]);
     relu64_to_tmem(t_lane, a_lane);
     ptx::tc_fence_before();
     __syncthreads();
@@ -559,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const float raw = v32[k];
-        rgb[k] = p.mlp.color_space == 0 ? sigmoid(raw) : trunc_exp(raw);
+        rgb[k] = p.mlp.color_space == 0 ? sigmoid_fast(raw) : trunc_exp_fast(raw);
       }
       s.res[tid] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
     }
