@@ -86,17 +86,20 @@ __device__ __forceinline__ void corner_indices(bool dense, int iu, int iv, int i
     idx[6] = b + vv + verts;
     idx[7] = b + vv + verts + 1u;
   } else {
+    // (x ^ hy ^ hz) & mask == (x & mask) ^ (hy & mask) ^ (hz & mask): mask the six terms once,
+    // then one three-input LOP3 per corner
     const uint32_t hy0 = y0 * 2654435761u, hy1 = hy0 + 2654435761u;
     const uint32_t hz0 = z0 * 805459861u, hz1 = hz0 + 805459861u;
-    const uint32_t x1 = x0 + 1u;
-    idx[0] = (x0 ^ hy0 ^ hz0) & mask;
-    idx[1] = (x1 ^ hy0 ^ hz0) & mask;
-    idx[2] = (x0 ^ hy1 ^ hz0) & mask;
-    idx[3] = (x1 ^ hy1 ^ hz0) & mask;
-    idx[4] = (x0 ^ hy0 ^ hz1) & mask;
-    idx[5] = (x1 ^ hy0 ^ hz1) & mask;
-    idx[6] = (x0 ^ hy1 ^ hz1) & mask;
-    idx[7] = (x1 ^ hy1 ^ hz1) & mask;
+    const uint32_t xa = x0 & mask, xb = (x0 + 1u) & mask, ya = hy0 & mask, yb = hy1 & mask,
+                   za = hz0 & mask, zb = hz1 & mask;
+    idx[0] = xa ^ ya ^ za;
+    idx[1] = xb ^ ya ^ za;
+    idx[2] = xa ^ yb ^ za;
+    idx[3] = xb ^ yb ^ za;
+    idx[4] = xa ^ ya ^ zb;
+    idx[5] = xb ^ ya ^ zb;
+    idx[6] = xa ^ yb ^ zb;
+    idx[7] = xb ^ yb ^ zb;
   }
 }
 

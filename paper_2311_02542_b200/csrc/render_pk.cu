@@ -69,12 +69,23 @@ struct __align__(16) Smem {
   uint32_t tmem_base;
   uint4 lvl[kMaxLevels];         // per level: res, hash mask (0 = dense), level base address (lo, hi)
   float4 samp[kWarps][32];       // per row: grid coordinates u, v, w and the LOD fraction
-  uint16_t pairs[kWarps][32 * kMaxLevels];  // (sample, level) gather list: row | l<<5 | class<<9
+  uint16_t pairs[kWarps][32 * kMaxLevels];  // (sample, level) gather list: row | l<<5
 };
 
 __device__ __forceinline__ uint32_t core_off(int row, int chunk, int kchunks) {
   return (uint32_t)((row >> 3) * (kchunks * 128) + chunk * 128 + (row & 7) * 16);
 }
+
+// The layer-1 A tile is chunk-major (all 128 rows of an 8-element K chunk contiguous; core
+// matrices LBO = 2048 B along K, SBO = 128 B along M), so row r, chunk c starts at c*2048 + r*16
+// and a (sample, level) feature pair lands at a byte offset that IS its gather-list code:
+// src*16 | (l & 3)*4 | (l >> 2)*2048 within the warp's 32 rows.
+constexpr uint32_t kALbo = 2048;
+__device__ __forceinline__ uint32_t a_off(int row, int chunk) { return (uint32_t)(chunk * kALbo + row * 16); }
+__device__ __forceinline__ uint32_t pair_code(int src, int l) {
+  return (uint32_t)((src << 4) | ((l & 3) << 2) | ((l >> 2) << 11));
+}
+__device__ __forceinline__ int pair_level(uint32_t code) { return (int)(((code >> 2) & 3u) | ((code >> 9) & 12u)); }
 
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
@@ -105,7 +116,8 @@ __device__ void load_weight_tile(uint8_t* dst, const float* __restrict__ W, int 
   }
 }
 
-// layer 1 (SS form): A = features + ones block in shared memory
+// layer 1 (SS form): A = features + ones block in shared memory (chunk-major, a_off), B the
+// row-group-major weight tile
 template <int N, int K>
 __device__ __forceinline__ void issue_layer(const uint8_t* A, const uint8_t* B, uint32_t d_tmem) {
   constexpr uint32_t idesc = ptx::idesc_f16_f32<128, N>();
@@ -113,7 +125,7 @@ __device__ __forceinline__ void issue_layer(const uint8_t* A, const uint8_t* B, 
   const uint32_t a = ptx::smem_addr(A), b = ptx::smem_addr(B);
 #pragma unroll
   for (int kk = 0; kk < (K + kKb) / 16; ++kk)
-    ptx::mma_f16(d_tmem, ptx::make_smem_desc(a + kk * 256, 128, sbo),
+    ptx::mma_f16(d_tmem, ptx::make_smem_desc(a + kk * 2 * kALbo, kALbo, 128),
                  ptx::make_smem_desc(b + kk * 256, 128, sbo), idesc, kk > 0 ? 1u : 0u);
 }
 
@@ -243,8 +255,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
   load_weight_tile(s.C2, c2, 64, 64, 64);
   load_weight_tile(s.C3, c3, 3, 16, 64);
   // this row's constant ones block of the layer-1 A tile (never overwritten)
-  st16(s.A, core_off(tid, 4, kAch), make_uint4(0x3C00u, 0u, 0u, 0u));  // fp16 1.0
-  st16(s.A, core_off(tid, 5, kAch), make_uint4(0u, 0u, 0u, 0u));
+  st16(s.A, a_off(tid, 4), make_uint4(0x3C00u, 0u, 0u, 0u));  // fp16 1.0
+  st16(s.A, a_off(tid, 5), make_uint4(0u, 0u, 0u, 0u));
   for (int l = tid; l < kMaxLevels; l += kThreads) {
     const int res = l < p.grid.levels ? p.grid.res[l] : 1;
     const bool dense = (p.grid.dense_mask >> l) & 1u;
@@ -432,8 +444,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     {
       const uint4 zero = make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) st16(s.A, core_off(tid, j, kAch), zero);
-      if (have) s.samp[warp][lane] = make_float4(u, v, w, lw.frac);
+      for (int j = 0; j < 4; ++j) st16(s.A, a_off(tid, j), zero);
+      // LOD weights as one number: w_l = saturate(fl - l) with fl = full + frac (grid.cpp:15-37;
+      // 1e-4 for the floor-only case, levels for all-on)
+      const float fl = lw.floor_only ? 1e-4f : (float)lw.full + lw.frac;
+      if (have) s.samp[warp][lane] = make_float4(u, v, w, fl);
       uint16_t* pc = s.pairs[warp];
       const unsigned lt = (1u << lane) - 1u;
       int npairs = 0;
@@ -441,13 +456,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
         const unsigned m = __ballot_sync(FULL, na > l);
         if (m == 0u) break;  // active levels are a prefix [0, na)
         if (na > l) {
-          const uint32_t cls = lw.floor_only ? 2u : (l < lw.full ? 0u : 1u);
-          pc[npairs + __popc(m & lt)] = (uint16_t)(lane | (l << 5) | (cls << 9));
+          pc[npairs + __popc(m & lt)] = (uint16_t)pair_code(lane, l);
         }
         npairs += __popc(m);
       }
       __syncwarp();
-      uint8_t* Abase = s.A + (warp * 32 / 8) * (kAch * 128);
+      uint8_t* Abase = s.A + a_off(warp * 32, 0);
+      const uint8_t* Pbase = reinterpret_cast<const uint8_t*>(s.samp[warp]);
 #ifdef LUMI_PHASE_TIMING
       if (lane == 0) {
         atomicAdd(&g_counts_pk[2], (unsigned long long)((npairs + 32 * kPairs - 1) / (32 * kPairs)));
@@ -467,19 +482,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
         for (int q = 0; q < kPairs; ++q) {
           f[q] = make_float2(0.f, 0.f);
           if (code[q] != 0xffffu) {
-            const float4 P = s.samp[warp][code[q] & 31u];
-            const uint32_t cls = code[q] >> 9;
-            const float wl = cls == 0u ? 1.f : (cls == 1u ? P.w : 1e-4f);
-            f[q] = gather_level(s.lvl[(code[q] >> 5) & 15u], P.x, P.y, P.z, wl);
+            const float4 P = *reinterpret_cast<const float4*>(Pbase + (code[q] & 0x1F0u));
+            const int lv = pair_level(code[q]);
+            const float wl = __saturatef(P.w - (float)lv);
+            f[q] = gather_level(s.lvl[lv], P.x, P.y, P.z, wl);
           }
         }
 #pragma unroll
         for (int q = 0; q < kPairs; ++q)
-          if (code[q] != 0xffffu) {
-            const int src = code[q] & 31u, lv = (code[q] >> 5) & 15u;
-            *reinterpret_cast<__half2*>(Abase + core_off(src, lv >> 2, kAch) + (lv & 3) * 4) =
-                __floats2half2_rn(f[q].x, f[q].y);
-          }
+          if (code[q] != 0xffffu)
+            *reinterpret_cast<__half2*>(Abase + code[q]) = __floats2half2_rn(f[q].x, f[q].y);
       }
     }
     ptx::fence_async_smem();
