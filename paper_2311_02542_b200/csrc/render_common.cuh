@@ -194,4 +194,49 @@ __device__ __forceinline__ int occupied_filtered(const RenderParams& p, float3 o
 }
 
 
+// Fast path of the certified test for candidates strictly inside the unit cube, where the
+// contraction is the identity: the voxel coordinate is one FMA in t per axis,
+//   g = (o + d t + 2) q = G0 + G1 t,  G1 = fl(d_f q), G0 = fl(fl(o_f q) + 2q),  q = res / 4.
+// Against the exact g (double o, d, t): |o_f - o| <= 2^-24 |o|, |d_f - d| <= 2^-24 |d|
+// (|d| <= 1), |t_f - t| <= 2^-24 t; G1 and G0 add one rounding each and the FMA one more, so
+// |g_f - g| <= 2^-24 (3 q t + 2 q |o|_inf + |G0| + |g_f|) <= 2^-24 q (3 t + 3 |o|_inf + 5)
+// inside the cube (|G0|, |g| <= 3q + q|o|).  eps = E0 + E1 t takes 4x that.  The candidate is
+// decided here only if every axis is more than eps inside (q, 3q) -- so the exact point is
+// strictly inside too and contract() is the identity for both -- and more than eps from a
+// voxel boundary; anything else returns -1 for the general test.
+struct InsideMarch {
+  float3 g0, g1;
+  float e0, e1, qlo, qhi;
+};
+
+__device__ __forceinline__ InsideMarch inside_march_setup(const RenderParams& p, float3 of, float3 df) {
+  const float q = 0.25f * (float)p.occ_res;
+  InsideMarch m;
+  m.g1 = make_float3(df.x * q, df.y * q, df.z * q);
+  m.g0 = make_float3(of.x * q + 2.f * q, of.y * q + 2.f * q, of.z * q + 2.f * q);
+  const float om = fmaxf(fabsf(of.x), fmaxf(fabsf(of.y), fabsf(of.z)));
+  m.e0 = 2.384185791e-07f * q * (3.f * om + 5.f);  // 4 * 2^-24 * q * (3|o| + 5)
+  m.e1 = 2.384185791e-07f * q * 3.f;
+  m.qlo = q;
+  m.qhi = 3.f * q;
+  return m;
+}
+
+// 0 / 1: decided (empty / occupied); -1: use occupied_filtered
+__device__ __forceinline__ int occupied_inside(const RenderParams& p, const InsideMarch& m, float tf) {
+  const float gx = fmaf(m.g1.x, tf, m.g0.x), gy = fmaf(m.g1.y, tf, m.g0.y), gz = fmaf(m.g1.z, tf, m.g0.z);
+  const float eps = fmaf(m.e1, tf, m.e0);
+  constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: rint on the FMA pipe
+  const float rx = __fsub_rn(__fadd_rn(gx, kMagic), kMagic), ry = __fsub_rn(__fadd_rn(gy, kMagic), kMagic),
+              rz = __fsub_rn(__fadd_rn(gz, kMagic), kMagic);
+  const float dmin = fminf(fabsf(gx - rx), fminf(fabsf(gy - ry), fabsf(gz - rz)));
+  const float gmin = fminf(gx, fminf(gy, gz)), gmax = fmaxf(gx, fmaxf(gy, gz));
+  if (!(dmin > eps && gmin - eps > m.qlo && gmax + eps < m.qhi)) return -1;
+  const uint32_t r = (uint32_t)p.occ_res;
+  const uint32_t ix = (uint32_t)(__float_as_int(__fadd_rn(gx - 0.5f, kMagic)) - 0x4B400000),
+                 iy = (uint32_t)(__float_as_int(__fadd_rn(gy - 0.5f, kMagic)) - 0x4B400000),
+                 iz = (uint32_t)(__float_as_int(__fadd_rn(gz - 0.5f, kMagic)) - 0x4B400000);
+  return __ldg(p.occ + ((iz * r + iy) * r + ix)) != 0 ? 1 : 0;
+}
+
 }  // namespace lumi_dev

@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(128) k_march_mask_fast(RenderParams p) {
   const float3 of = make_float3((float)o.x, (float)o.y, (float)o.z);
   const float3 df = make_float3((float)d.x, (float)d.y, (float)d.z);
   const float onorm = fabsf(of.x) + fabsf(of.y) + fabsf(of.z);
+  const InsideMarch im = inside_march_setup(p, of, df);
   int count = 0;
   for (int w0 = 0; w0 < p.mask_words; ++w0) {
     uint32_t bits = 0, unsure = 0;
@@ -298,7 +299,9 @@ __global__ void __launch_bounds__(128) k_march_mask_fast(RenderParams p) {
       const int hi = min(32, p.n - w0 * 32);
 #pragma unroll 4
       for (int b = 0; b < hi; ++b) {
-        const int r = occupied_filtered(p, of, df, onorm, s_tf[w0 * 32 + b]);
+        const float tf = s_tf[w0 * 32 + b];
+        int r = occupied_inside(p, im, tf);  // -1: not certified inside the unit cube
+        if (r < 0) r = occupied_filtered(p, of, df, onorm, tf);
         bits |= (uint32_t)(r & 1) << b;
         unsure |= (uint32_t)(r >> 1) << b;
       }
