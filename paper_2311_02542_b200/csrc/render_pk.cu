@@ -40,7 +40,7 @@ constexpr uint32_t kOnesCol = 120;
 constexpr int kKb = 16;              // every layer's bias is one extra K = 16 step
 constexpr int kAch = (32 + kKb) / 8; // 8-element K chunks of the layer-1 A tile
 #ifndef LUMI_PK_PAIRS
-#define LUMI_PK_PAIRS 2
+#define LUMI_PK_PAIRS 3
 #endif
 constexpr int kPairs = LUMI_PK_PAIRS;  // (sample, level) pairs per lane per gather step
 #ifdef LUMI_PHASE_TIMING
