@@ -293,14 +293,15 @@ def run_ours(args):
     d2h = 3 * rays_frame * 4
     h2d = 2 * (C.sizeof(_abi.CameraDesc) + C.sizeof(_abi.RenderOptionsDesc))
     if world == 1:
-        host = torch.empty((cfg.eyes, 3, cfg.eye_size, cfg.eye_size), dtype=torch.float32).pin_memory()
+        # the frame driver renders the stacked eye pair (rays_frame), so does the e2e leg
+        host = torch.empty((2, 3, cfg.eye_size, cfg.eye_size), dtype=torch.float32).pin_memory()
         host_np = host.numpy()
         cams = drv.cameras(0)
         dm.render_rows(cams[0], opts, 0, cfg.eye_size, host_np[0])  # warm
         t0 = time.perf_counter()
         for k in range(e2e_steps):
             cams = drv.cameras(args.warmup + k)  # the timed region's first frames
-            for eye in range(cfg.eyes):
+            for eye in range(2):
                 dm.render_rows(cams[eye], opts, 0, cfg.eye_size, host_np[eye])
         e2e_s = time.perf_counter() - t0
     else:
@@ -363,9 +364,11 @@ def run_ours(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64 geometry / f32 field", "data": "synthetic (seeded init_random + reference-baked occupancy)",
         "config": {"workload": f"{args.config}: {cfg.description}", "eye_size": cfg.eye_size,
-                   "eyes": cfg.eyes, "table_size": spec.table_size, "rays_per_frame": rays_frame,
+                   "eyes": 2, "table_size": spec.table_size, "rays_per_frame": rays_frame,
                    "samples_per_ray": opts.samples_per_ray, "parallelism": f"rows{world}",
-                   "l2": "inputs larger than L2 (hash table %.0f MB fp32)" % (field.grid_params.nbytes / 1e6),
+                   "l2": ("inputs larger than L2 (hash table %.0f MB fp32)" if field.grid_params.nbytes > 126e6
+                          else "hash table %.0f MB fp32 fits in L2 (no flush between frames)")
+                         % (field.grid_params.nbytes / 1e6),
                    "kernel": kname},
         "fps": round(fps, 3),
         "render_ms_per_step": round(kernel_ms / args.steps, 3),  # rank-0 march+render span
