@@ -320,3 +320,39 @@ def test_stress_dense_occupancy_4k_rows(lumi, torch_cuda, small, oracle):
     band = slice(2040, 2048)
     assert np.abs(out[:, band] - ref["out"][:, band]).max() <= PIX_TOL
     assert sum(s.evals for s in stats) == pytest.approx(int(ref["row_evals"].sum()), rel=0.01)
+
+
+def test_concurrent_workers_and_optional_planes(lumi, torch_cuda, small):
+    """run_frame's contract (scheduler.cpp:124-142): concurrent render_rows calls on disjoint
+    bands of one image from worker threads (pooled staging slots, one stream each) give the
+    single-call image bit for bit; requesting depth/opacity planes does not change rgb."""
+    import threading
+    cam = lumi.CameraModel.from_spec(scenes.pinhole(256, 192))
+    opts = lumi.RenderOptions()
+    dm = small["dm"]
+    full = np.zeros((3, 192, 256), np.float32)
+    depth = np.zeros((192, 256), np.float32)
+    opac = np.zeros((192, 256), np.float32)
+    dm.render_rows(cam, opts, 0, 192, full, depth, opac)
+    assert depth.any() and opac.any()
+    rgb_only = np.zeros_like(full)
+    dm.render_rows(cam, opts, 0, 192, rgb_only)
+    assert np.array_equal(full, rgb_only)
+    for rep in range(3):
+        par = np.zeros_like(full)
+        bands = [(0, 61), (61, 130), (130, 192)]
+        errs = []
+
+        def work(b, e):
+            try:
+                dm.render_rows(cam, opts, b, e, par)
+            except Exception as ex:  # noqa: BLE001
+                errs.append(ex)
+
+        ts = [threading.Thread(target=work, args=be) for be in bands]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        assert not errs
+        assert np.array_equal(par, full), f"rep {rep}"
