@@ -23,26 +23,11 @@
 #include "kernels.h"
 #include "render_common.cuh"
 #include "tc_ptx.cuh"
+#include "pk_parts.cuh"
 
 namespace lumi_dev {
 namespace pk {
 
-constexpr int kThreads = 128;  // UMMA M: 4 warps x 32 rows
-constexpr int kWarps = kThreads / 32;
-constexpr int kPW = 8, kPH = 4;  // packet: 8 x 4 pixels = one warp of rays
-// TMEM columns: [0,80) fp32 accumulators (N <= 80), [80,112) hidden activations h (fp16 pairs,
-// the TS-form A operand), [112,120) the SH encoding (fused layer only), [120,128) the
-// constant [1 0 ... 0] bias block
-constexpr uint32_t kTmemCols = 128;
-constexpr uint32_t kAcol = 80;
-constexpr uint32_t kShCol = 112;
-constexpr uint32_t kOnesCol = 120;
-constexpr int kKb = 16;              // every layer's bias is one extra K = 16 step
-constexpr int kAch = (32 + kKb) / 8; // 8-element K chunks of the layer-1 A tile
-#ifndef LUMI_PK_PAIRS
-#define LUMI_PK_PAIRS 3
-#endif
-constexpr int kPairs = LUMI_PK_PAIRS;  // (sample, level) pairs per lane per gather step
 #ifdef LUMI_PHASE_TIMING
 // per-phase warp-cycles (instrumented builds only): fill, geometry, gather, CTA sync, MLP,
 // composite, round barrier
@@ -70,173 +55,6 @@ struct __align__(16) Smem {
   uint4 lvl[kMaxLevels];         // per level: res, hash mask (0 = dense), level base address (lo, hi)
   float4 samp[kWarps][32];       // per row: grid coordinates u, v, w and the LOD fraction
   uint16_t pairs[kWarps][32 * kMaxLevels];  // (sample, level) gather list: row | l<<5
-};
-
-__device__ __forceinline__ uint32_t core_off(int row, int chunk, int kchunks) {
-  return (uint32_t)((row >> 3) * (kchunks * 128) + chunk * 128 + (row & 7) * 16);
-}
-
-// The layer-1 A tile is chunk-major (all 128 rows of an 8-element K chunk contiguous; core
-// matrices LBO = 2048 B along K, SBO = 128 B along M), so row r, chunk c starts at c*2048 + r*16
-// and a (sample, level) feature pair lands at a byte offset that IS its gather-list code:
-// src*16 | (l & 3)*4 | (l >> 2)*2048 within the warp's 32 rows.
-constexpr uint32_t kALbo = 2048;
-__device__ __forceinline__ uint32_t a_off(int row, int chunk) { return (uint32_t)(chunk * kALbo + row * 16); }
-__device__ __forceinline__ uint32_t pair_code(int src, int l) {
-  return (uint32_t)((src << 4) | ((l & 3) << 2) | ((l >> 2) << 11));
-}
-__device__ __forceinline__ int pair_level(uint32_t code) { return (int)(((code >> 2) & 3u) | ((code >> 9) & 12u)); }
-
-__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
-
-__device__ __forceinline__ void st16(uint8_t* base, uint32_t off, uint4 v) {
-  *reinterpret_cast<uint4*>(base + off) = v;
-}
-
-__device__ __forceinline__ uint4 pack8(const float* v) {
-  return make_uint4(h2u(__floats2half2_rn(v[0], v[1])), h2u(__floats2half2_rn(v[2], v[3])),
-                    h2u(__floats2half2_rn(v[4], v[5])), h2u(__floats2half2_rn(v[6], v[7])));
-}
-
-// weights [n_real x K] fp32 row-major + bias [n_real] (network.h:64, 144-151) -> fp16 UMMA
-// tile [n_pad][K + 16] with the bias in column K
-__device__ void load_weight_tile(uint8_t* dst, const float* __restrict__ W, int n_real, int n_pad,
-                                 int K) {
-  const float* bias = W + (size_t)n_real * K;
-  const int kch = (K + kKb) / 8;
-  for (int it = threadIdx.x; it < n_pad * kch; it += blockDim.x) {
-    const int n = it / kch, j = it % kch;
-    float v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int k = 8 * j + q;
-      v[q] = n >= n_real ? 0.f : k < K ? __ldg(W + (size_t)n * K + k) : k == K ? __ldg(bias + n) : 0.f;
-    }
-    st16(dst, core_off(n, j, kch), pack8(v));
-  }
-}
-
-// layer 1 (SS form): A = features + ones block in shared memory (chunk-major, a_off), B the
-// row-group-major weight tile
-template <int N, int K>
-__device__ __forceinline__ void issue_layer(const uint8_t* A, const uint8_t* B, uint32_t d_tmem) {
-  constexpr uint32_t idesc = ptx::idesc_f16_f32<128, N>();
-  constexpr uint32_t sbo = ((K + kKb) / 8) * 128;
-  const uint32_t a = ptx::smem_addr(A), b = ptx::smem_addr(B);
-#pragma unroll
-  for (int kk = 0; kk < (K + kKb) / 16; ++kk)
-    ptx::mma_f16(d_tmem, ptx::make_smem_desc(a + kk * 2 * kALbo, kALbo, 128),
-                 ptx::make_smem_desc(b + kk * 256, 128, sbo), idesc, kk > 0 ? 1u : 0u);
-}
-
-// hidden layers (TS form): A = activations in TMEM columns [a_tmem, a_tmem + K/2), then the
-// TMEM ones block against the bias column of B
-template <int N, int K>
-__device__ __forceinline__ void issue_layer_ts(uint32_t a_tmem, uint32_t ones_tmem, const uint8_t* B,
-                                               uint32_t d_tmem) {
-  constexpr uint32_t idesc = ptx::idesc_f16_f32<128, N>();
-  constexpr uint32_t sbo = ((K + kKb) / 8) * 128;
-  const uint32_t b = ptx::smem_addr(B);
-#pragma unroll
-  for (int kk = 0; kk < K / 16; ++kk)  // 16 fp16 of K = 8 TMEM columns per step
-    ptx::mma_f16_ts(d_tmem, a_tmem + kk * 8, ptx::make_smem_desc(b + kk * 256, 128, sbo), idesc,
-                    kk > 0 ? 1u : 0u);
-  ptx::mma_f16_ts(d_tmem, ones_tmem, ptx::make_smem_desc(b + (K / 16) * 256, 128, sbo), idesc, 1u);
-}
-
-// two fp32 -> packed fp16 (lo, hi), optionally clamped at 0, in one F2FP
-__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
-  uint32_t d;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
-  return d;
-}
-__device__ __forceinline__ uint32_t pack2_relu(float lo, float hi) {
-  uint32_t d;
-  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
-  return d;
-}
-
-// hidden-layer epilogue into TMEM: D row (64 fp32, bias included), ReLU, fp16 pairs -> the A
-// columns of this thread's lane for the next layer
-__device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane) {
-#pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    float v[16];
-    ptx::tmem_ld16(t_lane + 16 * h, v);
-    ptx::tmem_ld_wait();
-    uint32_t w[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) w[j] = pack2_relu(v[2 * j], v[2 * j + 1]);
-    ptx::tmem_st8(a_lane + 8 * h, w);
-  }
-  ptx::tmem_st_wait();
-}
-
-// One hash-grid level of one sample from the fp16 table (grid.h:96-113, 144-167): fp32 grid
-// coordinates, 32-bit entry indices off the level's base address, fp16 trilinear weights
-// (HMUL2) accumulated in fp32 by FHFMA in two interleaved chains per feature.
-__device__ __forceinline__ float2 gather_level(uint4 L, float u, float v, float s, float wl) {
-  const int res = (int)L.x;
-  const float r = (float)res;
-  const __half2* __restrict__ base =
-      reinterpret_cast<const __half2*>(((unsigned long long)L.w << 32) | L.z);  // level's first pair
-  const float pu = u * r, pv = v * r, ps = s * r;
-  const int iu = min((int)pu, res - 1), iv = min((int)pv, res - 1), is = min((int)ps, res - 1);
-  uint32_t idx[8];
-  corner_indices(L.y == 0u, iu, iv, is, (uint32_t)res + 1u, L.y, idx);
-  __half2 e[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) e[k] = __ldg(base + idx[k]);  // one IMAD.WIDE per corner
-  const float fu = pu - (float)iu, fv = pv - (float)iv, fs = ps - (float)is;
-  const __half2 hu = __floats2half2_rn(1.f - fu, fu);
-  const __half2 w0 = __hmul2(hu, __float2half2_rn(1.f - fv));
-  const __half2 w1 = __hmul2(hu, __float2half2_rn(fv));
-  const __half2 gs2 = __float2half2_rn(1.f - fs), fs2 = __float2half2_rn(fs);
-  const __half2 t[4] = {__hmul2(w0, gs2), __hmul2(w1, gs2), __hmul2(w0, fs2), __hmul2(w1, fs2)};
-  float a[2] = {0.f, 0.f}, b[2] = {0.f, 0.f};
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const __half tri = (k & 1) ? __high2half(t[k >> 1]) : __low2half(t[k >> 1]);
-    a[k & 1] = fma_f32_f16(tri, __low2half(e[k]), a[k & 1]);
-    b[k & 1] = fma_f32_f16(tri, __high2half(e[k]), b[k & 1]);
-  }
-  return make_float2((a[0] + a[1]) * wl, (b[0] + b[1]) * wl);
-}
-
-// trunc_exp / sigmoid (network.h:41-57) with the MUFU exp2 / reciprocal: ~2 ulp, far below the
-// fp16 MLP operands' 1.6e-4 (oracle-measured)
-__device__ __forceinline__ float trunc_exp_fast(float x) {
-  return x <= 10.f ? __expf(x) : 22026.4657948f * (1.f + (x - 10.f));
-}
-__device__ __forceinline__ float sigmoid_fast(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
-
-// position of the (k+1)-th set bit of m (k < popc(m))
-__device__ __forceinline__ int nth_set_bit(uint32_t m, int k) {
-  int pos = 0;
-#pragma unroll
-  for (int w = 16; w > 0; w >>= 1) {
-    const int c = __popc(m & ((1u << w) - 1u));
-    if (k >= c) {
-      k -= c;
-      m >>= w;
-      pos += w;
-    }
-  }
-  return pos;
-}
-
-// The owner-lane state of one ray of the packet.
-struct Ray {
-  bool valid, alive;  // pixel inside the range / still compositing
-  int x, y, id;
-  float3 d, nd;       // fp32 directions for the network-input geometry
-  int kept_total, contributing;
-  bool term;
-  double trans, px, py, pz, depth, opac;
-};
-
-struct Counters {
-  unsigned evals, level_samples, marched, rays;
 };
 
 __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
