@@ -331,7 +331,8 @@ def run_ours(args):
     # the tensor-core kernel gathers the fp16 copy of the table (32 B per level-sample), the
     # SIMT cross-check the reference fp32 layout (64 B)
     bytes_per_ls = GATHER_BYTES_PER_LEVEL_SAMPLE // (1 if dm.kernel == "simt" else 2)
-    kname = {"tc": "k_render_tc", "packet": "k_render_pk", "simt": "k_render_simt"}[dm.kernel]
+    kname = {"tc": "k_render_tc", "packet": "k_render_pk", "simt": "k_render_simt",
+             "ws": "k_render_ws"}[dm.kernel]
     gather_bytes = level_samples * bytes_per_ls
     # the render kernel's own launches on rank 0 (CUDA events on the launch stream around
     # each launch, march pass excluded); counters are summed over ranks, so scale by 1/world

@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("LUMI_CUDA_LIB") or os.path.join(HERE, "lib", "liblumi
 
 LUMI_MAX_LEVELS = 16
 LUMI_OK, LUMI_ERR_INVALID, LUMI_ERR_CUDA, LUMI_ERR_UNSUPPORTED = 0, 1, 2, 3
-LUMI_KERNEL_TC, LUMI_KERNEL_SIMT, LUMI_KERNEL_PACKET = 0, 1, 2
+LUMI_KERNEL_TC, LUMI_KERNEL_SIMT, LUMI_KERNEL_PACKET, LUMI_KERNEL_WS = 0, 1, 2, 3
 
 
 class Error(RuntimeError):

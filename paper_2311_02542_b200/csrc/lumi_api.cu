@@ -181,7 +181,7 @@ struct LumiModel {
   int occ_res = 0;
   unsigned int* d_counter = nullptr;  // kCounterSlots per-launch tile counters
   std::atomic<unsigned> counter_slot{0};
-  int kernel = LUMI_KERNEL_PACKET;
+  int kernel = LUMI_KERNEL_WS;
   int num_sms = 148;
   std::mutex mu;
   std::map<std::tuple<double, double, int>, std::pair<double*, double>> ts_cache;
@@ -453,7 +453,10 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
   if ((rc = lumi_model_set_occupancy(m, occ, occ_res))) return cleanup(rc);
   if (const char* k = std::getenv("LUMI_KERNEL")) {
     const std::string ks(k);
-    m->kernel = ks == "simt" ? LUMI_KERNEL_SIMT : ks == "tc" ? LUMI_KERNEL_TC : LUMI_KERNEL_PACKET;
+    m->kernel = ks == "simt"     ? LUMI_KERNEL_SIMT
+                : ks == "tc"     ? LUMI_KERNEL_TC
+                : ks == "packet" ? LUMI_KERNEL_PACKET
+                                 : LUMI_KERNEL_WS;
   }
   *out = m;
   return LUMI_OK;
@@ -495,7 +498,8 @@ int lumi_model_destroy(LumiModel* m) {
 
 int lumi_model_set_kernel(LumiModel* m, int kernel) {
   if (!m) return fail(LUMI_ERR_INVALID, "null model");
-  if (kernel != LUMI_KERNEL_TC && kernel != LUMI_KERNEL_SIMT && kernel != LUMI_KERNEL_PACKET)
+  if (kernel != LUMI_KERNEL_TC && kernel != LUMI_KERNEL_SIMT && kernel != LUMI_KERNEL_PACKET &&
+      kernel != LUMI_KERNEL_WS)
     return fail(LUMI_ERR_INVALID, "unknown kernel variant");
   m->kernel = kernel;
   return LUMI_OK;
@@ -534,6 +538,8 @@ int lumi_render_rows_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRe
     if (ev) LUMI_CUDA_TRY(cudaEventRecord(ev[2], st));
   } else if (m->kernel == LUMI_KERNEL_PACKET) {
     LUMI_CUDA_TRY(launch_render_pk(p, st, m->num_sms, ev));
+  } else if (m->kernel == LUMI_KERNEL_WS) {
+    LUMI_CUDA_TRY(launch_render_ws(p, st, m->num_sms, ev));
   } else {
     LUMI_CUDA_TRY(launch_render_tc(p, st, m->num_sms, ev));
   }

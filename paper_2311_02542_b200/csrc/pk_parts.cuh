@@ -56,7 +56,7 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
 
 // weights [n_real x K] fp32 row-major + bias [n_real] (network.h:64, 144-151) -> fp16 UMMA
 // tile [n_pad][K + 16] with the bias in column K
-__device__ void load_weight_tile(uint8_t* dst, const float* __restrict__ W, int n_real, int n_pad,
+static __device__ void load_weight_tile(uint8_t* dst, const float* __restrict__ W, int n_real, int n_pad,
                                  int K) {
   const float* bias = W + (size_t)n_real * K;
   const int kch = (K + kKb) / 8;

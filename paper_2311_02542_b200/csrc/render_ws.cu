@@ -1,0 +1,532 @@
+// render_ws.cu -- warp-specialised packet renderer.
+//
+// The packet kernel (render_pk.cu) is latency bound with 16 warps per SM, and every resource
+// that would admit more row-owning warps is full (TMEM 4 x 128 columns, 128 registers x 512
+// threads, 57 KB of shared memory x 4).  Here each CTA pairs a CONSUMER warpgroup -- the four
+// row-owning warps: packet streams, geometry, gather lists, the tcgen05 MLP and compositing --
+// with a PRODUCER warpgroup of four warps that only runs the hash-grid gather (half the
+// instructions).  The two are pipelined one round apart through double-buffered layer-1 A
+// tiles and gather lists, synchronised with named barriers (one pair per buffer), so a CTA of
+// 8 warps fits 3 times per SM: 24 warps instead of 16.  The math of every stage is the packet
+// kernel's (pk_parts.cuh); only the schedule differs:
+//
+//   consumers, iteration j:  fill/geometry/list of round j into buffer j&1
+//                            -> arrive LIST_READY[j&1]
+//                            -> wait GATHER_DONE[(j-1)&1] -> MLP + composite of round j-1
+//   producers, iteration j:  wait LIST_READY[j&1] -> gather round j (all four warps' lists,
+//                            dealt over 128 threads) -> arrive GATHER_DONE[j&1]
+//
+// Because round j is filled before round j-1 is composited, a packet whose stream ends is
+// stored only after the last round holding its rows is composited (one idle round per packet
+// for that warp), and rows of rays that terminate in round j-1 may still be evaluated in round
+// j (they are skipped by the compositing, exactly as in the packet kernel).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <algorithm>
+
+#include "kernels.h"
+#include "pk_parts.cuh"
+
+namespace lumi_dev {
+namespace ws {
+
+using namespace pk;
+
+constexpr int kCtaThreads = 256;  // consumers [0, 128), producers [128, 256)
+#ifndef WS_PROD_PAIRS
+#define WS_PROD_PAIRS 3
+#endif
+constexpr int kProdPairs = WS_PROD_PAIRS;  // pairs per producer thread per gather step
+// named barriers: 0 = __syncthreads (setup / teardown), LIST_READY 1 + b, GATHER_DONE 3 + b,
+// 5 = consumer warpgroup only
+constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5;
+
+struct __align__(16) Smem {
+  uint8_t A[2][128 * (32 + kKb) * 2];  // double-buffered layer-1 A tiles (chunk-major, a_off)
+  uint8_t W1[64 * (32 + kKb) * 2];
+  uint8_t F[80 * (80 + kKb) * 2];
+  uint8_t C2[64 * (64 + kKb) * 2];
+  uint8_t C3[16 * (64 + kKb) * 2];
+  float4 res[128];
+  uint32_t ballot[kWarps][32];
+  uint16_t prefix[kWarps][33];
+  uint32_t own[2][kWarps][32];
+  uint16_t rowcand[2][kWarps][32];
+  uint8_t rowlane[2][128];
+  uint64_t mbar;
+  uint32_t tmem_base;
+  int stop[2];
+  uint4 lvl[kMaxLevels];
+  float4 samp[2][128];
+  uint16_t pairs[2][kWarps][32 * kMaxLevels];
+  int npairs[2][kWarps];
+};
+
+// named barriers with immediate ids, so ptxas reserves only the barriers used (a register id
+// would reserve all 16, which caps residency at one CTA per SM)
+template <int ID, int N>
+__device__ __forceinline__ void bar_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory");
+}
+template <int ID, int N>
+__device__ __forceinline__ void bar_arrive() {
+  asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(N) : "memory");
+}
+template <int ID, int N>
+__device__ __forceinline__ bool bar_and(bool v) {
+  uint32_t r;
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n bar.red.and.pred q, %2, %3, p;\n"
+      " selp.u32 %0, 1, 0, q;\n}"
+      : "=r"(r)
+      : "r"((uint32_t)v), "n"(ID), "n"(N)
+      : "memory");
+  return r != 0;
+}
+// buffer-indexed barriers: b is 0 or 1
+__device__ __forceinline__ void list_ready_sync(int b) {
+  if (b) bar_sync<kBarList + 1, kCtaThreads>(); else bar_sync<kBarList, kCtaThreads>();
+}
+__device__ __forceinline__ void list_ready_arrive(int b) {
+  if (b) bar_arrive<kBarList + 1, kCtaThreads>(); else bar_arrive<kBarList, kCtaThreads>();
+}
+__device__ __forceinline__ void gather_done_sync(int b) {
+  if (b) bar_sync<kBarGather + 1, kCtaThreads>(); else bar_sync<kBarGather, kCtaThreads>();
+}
+__device__ __forceinline__ void gather_done_arrive(int b) {
+  if (b) bar_arrive<kBarGather + 1, kCtaThreads>(); else bar_arrive<kBarGather, kCtaThreads>();
+}
+
+__global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x, wg = tid >> 7, ctid = tid & 127, warp = ctid >> 5, lane = tid & 31;
+  const unsigned FULL = 0xffffffffu;
+
+  // ---- setup (all 256 threads) -------------------------------------------------------------
+  const float* dp = p.mlp.dparams;
+  const float* cp = p.mlp.cparams;
+  const float* c2 = cp + 64 * 32 + 64;
+  const float* c3 = c2 + 64 * 64 + 64;
+  load_weight_tile(s.W1, dp, 64, 64, 32);
+  load_weight_tile(s.F, p.mlp.fused, kHidden + 1, 80, 80);
+  load_weight_tile(s.C2, c2, 64, 64, 64);
+  load_weight_tile(s.C3, c3, 3, 16, 64);
+  // constant ones block of both A buffers (never overwritten)
+  st16(s.A[wg], a_off(ctid, 4), make_uint4(0x3C00u, 0u, 0u, 0u));
+  st16(s.A[wg], a_off(ctid, 5), make_uint4(0u, 0u, 0u, 0u));
+  for (int l = tid; l < kMaxLevels; l += kCtaThreads) {
+    const int res = l < p.grid.levels ? p.grid.res[l] : 1;
+    const bool dense = (p.grid.dense_mask >> l) & 1u;
+    const unsigned long long base =
+        reinterpret_cast<unsigned long long>(p.grid.table16 + (l < p.grid.levels ? p.grid.offset2[l] : 0));
+    s.lvl[l] = make_uint4((uint32_t)res, dense ? 0u : p.grid.hash_mask[l], (uint32_t)base,
+                          (uint32_t)(base >> 32));
+  }
+  if (tid == 0) {
+    ptx::mbar_init(&s.mbar, 1);
+    ptx::fence_mbar_init();
+  }
+  if (tid < 32) ptx::tmem_alloc<kTmemCols>(&s.tmem_base);
+  ptx::fence_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+
+  if (wg == 1) {
+    // ================================ producers ==============================================
+#pragma unroll 1
+    for (int j = 0;; ++j) {
+      const int b = j & 1;
+      list_ready_sync(b);
+      if (s.stop[b]) break;
+      int pre[kWarps + 1];
+      pre[0] = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) pre[w + 1] = pre[w] + s.npairs[b][w];
+      const int total = pre[kWarps];
+      const uint8_t* Pb = reinterpret_cast<const uint8_t*>(s.samp[b]);
+#pragma unroll 1
+      for (int base = 0; base < total; base += 128 * kProdPairs) {
+        uint32_t code[kProdPairs], woff[kProdPairs];
+        float2 f[kProdPairs];
+#pragma unroll
+        for (int q = 0; q < kProdPairs; ++q) {
+          const int pi = base + 128 * q + ctid;
+          code[q] = 0xffffu;
+          woff[q] = 0;
+          if (pi < total) {
+            const int w = (pi >= pre[1]) + (pi >= pre[2]) + (pi >= pre[3]);
+            code[q] = s.pairs[b][w][pi - pre[w]];
+            woff[q] = (uint32_t)w * 32u * 16u;  // the warp's rows in A (a_off) and samp
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kProdPairs; ++q) {
+          f[q] = make_float2(0.f, 0.f);
+          if (code[q] != 0xffffu) {
+            const float4 P = *reinterpret_cast<const float4*>(Pb + woff[q] + (code[q] & 0x1F0u));
+            const int lv = pair_level(code[q]);
+            const float wl = __saturatef(P.w - (float)lv);
+            f[q] = gather_level(s.lvl[lv], P.x, P.y, P.z, wl);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kProdPairs; ++q)
+          if (code[q] != 0xffffu)
+            *reinterpret_cast<__half2*>(s.A[b] + woff[q] + code[q]) = __floats2half2_rn(f[q].x, f[q].y);
+      }
+      ptx::fence_async_smem();
+      gather_done_arrive(b);
+    }
+  } else {
+    // ================================ consumers ==============================================
+    const uint32_t t_lane = tmem + ((uint32_t)(warp * 32) << 16);
+    {
+      const uint32_t ones[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      ptx::tmem_st8(t_lane + kOnesCol, ones);
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      bar_sync<kBarCons, 128>();
+      ptx::tc_fence_after();
+    }
+    const float3 o = make_float3((float)p.cam.origin[0], (float)p.cam.origin[1], (float)p.cam.origin[2]);
+    const float two_base = (float)p.grid.two_base, inv_log = (float)(1.0 / p.grid.log_scale);
+    const int levels = p.grid.levels;
+    const long long packets_x = p.tiles_x;
+    const long long total_packets = p.total_rays / 32;
+    const uint32_t a_tmem = tmem + kAcol, ones_tmem = tmem + kOnesCol;
+    const uint32_t a_lane = t_lane + kAcol;
+    const bool issuer = (ctid == 0);
+
+    Counters cnt{0, 0, 0, 0};
+    Ray r;
+    r.valid = r.alive = false;
+    bool packet_live = false, no_more = false, pending = false;
+    int last_round = -1;  // the last round holding rows of the pending packet
+    int word = 0, g_next = 0, word_total = 0;
+    uint32_t phase = 0;
+
+#pragma unroll 1
+    for (int j = 0;; ++j) {
+      const int b = j & 1;
+      // ---- F(j): this warp's rows of round j from its packet stream -----------------------
+      int take = 0, rl = lane, cand = 0;
+      while (take < 32 && !no_more && !pending) {
+        if (!packet_live) {
+          long long pkt = 0;
+          if (lane == 0) pkt = (long long)atomicAdd(p.work_counter, 1u);
+          pkt = __shfl_sync(FULL, pkt, 0);
+          if (pkt >= total_packets) {
+            no_more = true;
+            break;
+          }
+          const long long rid = pkt * 32 + lane;
+          r.x = (int)(pkt % packets_x) * kPW + (lane % kPW);
+          r.y = p.row_begin + (int)(pkt / packets_x) * kPH + lane / kPW;
+          r.id = (int)rid;
+          r.valid = r.x < p.cam.width && r.y < p.row_end;
+          r.alive = r.valid;
+          if (r.valid) {
+            const d3 dd = ray_dir(p.cam, (double)r.x + 0.5, (double)r.y + 0.5);
+            const d3 nn = ray_dir(p.cam, (double)r.x + 1.5, (double)r.y + 0.5);
+            r.d = make_float3((float)dd.x, (float)dd.y, (float)dd.z);
+            r.nd = make_float3((float)nn.x, (float)nn.y, (float)nn.z);
+            r.kept_total = __ldg(p.kept_count + rid);
+            ++cnt.rays;
+            cnt.marched += p.n;
+          }
+          r.contributing = 0;
+          r.term = false;
+          r.trans = 1.0;
+          r.px = r.py = r.pz = r.depth = r.opac = 0.0;
+          packet_live = true;
+          word = -1;
+          g_next = word_total = 0;
+        }
+        if (g_next < word_total) {
+          const int n = min(32 - take, word_total - g_next);
+          if (lane >= take && lane < take + n) {
+            const int g = g_next + (lane - take);
+            int lo = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1)
+              if (s.prefix[warp][lo + st] <= g) lo += st;
+            rl = nth_set_bit(s.ballot[warp][lo], g - s.prefix[warp][lo]);
+            cand = word * 32 + lo;
+          }
+          take += n;
+          g_next += n;
+          continue;
+        }
+        if (word + 1 >= p.mask_words) {
+          // stream exhausted: store the pixels once the last round with its rows is composited
+          pending = true;
+          last_round = take > 0 ? j : j - 1;
+          break;
+        }
+        ++word;
+        const uint32_t bits = r.alive ? __ldg(p.kept_mask + (size_t)word * p.total_rays + r.id) : 0u;
+        int run = 0;
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t bb = __ballot_sync(FULL, (bits >> i) & 1u);
+          if (lane == 0) {
+            s.ballot[warp][i] = bb;
+            s.prefix[warp][i] = (uint16_t)run;
+          }
+          run += __popc(bb);
+        }
+        if (lane == 0) s.prefix[warp][32] = (uint16_t)run;
+        __syncwarp();
+        g_next = 0;
+        word_total = run;
+      }
+      const bool have = lane < take;
+      {
+        s.own[b][warp][lane] = 0u;
+        __syncwarp();
+        const unsigned same = __match_any_sync(FULL, have ? rl : 32 + lane);
+        if (have) {
+          s.own[b][warp][rl] = same;
+          s.rowcand[b][warp][lane] = (uint16_t)cand;
+        }
+        s.rowlane[b][ctid] = (uint8_t)rl;
+        __syncwarp();
+      }
+      const float dx = __shfl_sync(FULL, r.d.x, rl), dy = __shfl_sync(FULL, r.d.y, rl),
+                  dz = __shfl_sync(FULL, r.d.z, rl);
+      const float nx = __shfl_sync(FULL, r.nd.x, rl), ny = __shfl_sync(FULL, r.nd.y, rl),
+                  nz = __shfl_sync(FULL, r.nd.z, rl);
+      float u = 0.f, v = 0.f, w = 0.f;
+      LodW lw{0, 0.f, false};
+      int na = 0;
+      if (have) {
+        const float t = (float)__ldg(p.ts + cand);
+        const float3 c = contract_f(make_float3(o.x + dx * t, o.y + dy * t, o.z + dz * t), p.contraction);
+        u = __saturatef((c.x + 2.f) * 0.25f);
+        v = __saturatef((c.y + 2.f) * 0.25f);
+        w = __saturatef((c.z + 2.f) * 0.25f);
+        if (p.lod_enabled) {
+          const float3 bq = contract_f(make_float3(o.x + nx * t, o.y + ny * t, o.z + nz * t), p.contraction);
+          const float ex = c.x - bq.x, ey = c.y - bq.y, ez = c.z - bq.z;
+          const float rc = fmaxf(0.5f * sqrtf(ex * ex + ey * ey + ez * ez), 1e-12f);
+          const float l = fminf(-__logf(two_base * rc) * inv_log, (float)(levels - 1));
+          lw = lod_weights_f(l + (float)p.lod_bias, levels);
+        } else {
+          lw = LodW{levels, 0.f, false};
+        }
+        na = active_levels(lw, levels);
+        cnt.level_samples += na;
+        ++cnt.evals;
+      }
+      {  // this row's A features (buffer b; its last reader, the MMA of round j-2, is done)
+        const uint4 zero = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) st16(s.A[b], a_off(ctid, q), zero);
+        const float fl = lw.floor_only ? 1e-4f : (float)lw.full + lw.frac;
+        if (have) s.samp[b][ctid] = make_float4(u, v, w, fl);
+        uint16_t* pc = s.pairs[b][warp];
+        const unsigned lt = (1u << lane) - 1u;
+        int npairs = 0;
+        for (int l = 0; l < levels; ++l) {
+          const unsigned m = __ballot_sync(FULL, na > l);
+          if (m == 0u) break;
+          if (na > l) pc[npairs + __popc(m & lt)] = (uint16_t)pair_code(lane, l);
+          npairs += __popc(m);
+        }
+        if (lane == 0) s.npairs[b][warp] = npairs;
+      }
+      // all consumer warps finished (every packet stored) -> the producers stop after round j
+      const bool stop = bar_and<kBarCons, 128>(no_more && !packet_live);
+      if (ctid == 0) s.stop[b] = stop ? 1 : 0;
+      ptx::fence_async_smem();
+      list_ready_arrive(b);
+
+      if (j > 0) {
+        // ---- M(j-1): the tcgen05 MLP over round j-1's 128 rows (field.h:106-137) ----------
+        const int bp = (j - 1) & 1;
+        gather_done_sync(bp);
+        const int rlp = s.rowlane[bp][ctid];
+        const float pdx = __shfl_sync(FULL, r.d.x, rlp), pdy = __shfl_sync(FULL, r.d.y, rlp),
+                    pdz = __shfl_sync(FULL, r.d.z, rlp);
+        float v32[32];
+        if (issuer) {
+          ptx::tc_fence_after();
+          issue_layer<64, 32>(s.A[bp], s.W1, tmem);
+          ptx::mma_commit(&s.mbar);
+        }
+        ptx::mbar_wait(&s.mbar, phase);
+        phase ^= 1;
+        ptx::tc_fence_after();
+        relu64_to_tmem(t_lane, a_lane);
+        {
+          float sh[16];
+          sh_encode(d3{(double)pdx, (double)pdy, (double)pdz}, sh);
+          uint32_t wv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) wv[q] = pack2(sh[2 * q], sh[2 * q + 1]);
+          ptx::tmem_st8(t_lane + kShCol, wv);
+          ptx::tmem_st_wait();
+        }
+        ptx::tc_fence_before();
+        bar_sync<kBarCons, 128>();
+        if (issuer) {
+          ptx::tc_fence_after();
+          issue_layer_ts<80, 80>(a_tmem, ones_tmem, s.F, tmem);
+          ptx::mma_commit(&s.mbar);
+        }
+        ptx::mbar_wait(&s.mbar, phase);
+        phase ^= 1;
+        ptx::tc_fence_after();
+        ptx::tmem_ld16(t_lane + 64, v32);
+        ptx::tmem_ld_wait();
+        const float sigma = trunc_exp_fast(v32[0]);
+        relu64_to_tmem(t_lane, a_lane);
+        ptx::tc_fence_before();
+        bar_sync<kBarCons, 128>();
+        if (issuer) {
+          ptx::tc_fence_after();
+          issue_layer_ts<64, 64>(a_tmem, ones_tmem, s.C2, tmem);
+          ptx::mma_commit(&s.mbar);
+        }
+        ptx::mbar_wait(&s.mbar, phase);
+        phase ^= 1;
+        ptx::tc_fence_after();
+        relu64_to_tmem(t_lane, a_lane);
+        ptx::tc_fence_before();
+        bar_sync<kBarCons, 128>();
+        if (issuer) {
+          ptx::tc_fence_after();
+          issue_layer_ts<16, 64>(a_tmem, ones_tmem, s.C3, tmem);
+          ptx::mma_commit(&s.mbar);
+        }
+        ptx::mbar_wait(&s.mbar, phase);
+        phase ^= 1;
+        ptx::tc_fence_after();
+        ptx::tmem_ld16(t_lane, v32);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        {
+          float rgb[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const float raw = v32[k];
+            rgb[k] = p.mlp.color_space == 0 ? sigmoid_fast(raw) : trunc_exp_fast(raw);
+          }
+          s.res[ctid] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
+        }
+        __syncwarp();
+        // ---- C(j-1): owners composite their samples of round j-1 in order ----------------
+        uint32_t mine = s.own[bp][warp][lane];
+        while (mine && r.alive) {
+          const int jj = __ffs(mine) - 1;
+          mine &= mine - 1;
+          const float4 e = s.res[warp * 32 + jj];
+          const int cnd = s.rowcand[bp][warp][jj];
+          const double t = __ldg(p.ts + cnd);
+          const double delta = (cnd + 1 < p.n) ? dsub(__ldg(p.ts + cnd + 1), t) : dmul(t, dsub(p.ratio, 1.0));
+          const double a = dsub(1.0, exp(dmul(-(double)e.x, delta)));
+          const double wgt = dmul(r.trans, a);
+          r.px = dadd(r.px, dmul(wgt, (double)e.y));
+          r.py = dadd(r.py, dmul(wgt, (double)e.z));
+          r.pz = dadd(r.pz, dmul(wgt, (double)e.w));
+          r.depth = dadd(r.depth, dmul(wgt, t));
+          r.opac = dadd(r.opac, wgt);
+          r.trans = dmul(r.trans, dsub(1.0, a));
+          ++r.contributing;
+          if (p.t_cut > 0 && r.trans < p.t_cut) {
+            r.term = true;
+            r.alive = false;
+          }
+        }
+      }
+      // a finished packet is stored once its last round is composited (renderer.h:233-236)
+      if (pending && j - 1 >= last_round) {
+        if (r.valid) {
+          RayResult res{r.px, r.py, r.pz, r.depth, r.opac,
+                        chunk_evals(r.term, r.contributing, r.kept_total, p.chunk), r.contributing};
+          store_ray(p, r.x, r.y, res, r.trans);
+        }
+        pending = false;
+        packet_live = false;
+      }
+      if (stop) break;
+    }
+    ptx::tc_fence_before();
+    bar_sync<kBarCons, 128>();
+    ptx::tc_fence_after();
+    if (warp == 0) ptx::tmem_dealloc<kTmemCols>(tmem);
+    add_work_stats(p, cnt.evals, cnt.level_samples, cnt.marched, cnt.rays);
+  }
+}
+
+}  // namespace ws
+}  // namespace lumi_dev
+
+using namespace lumi_dev;
+
+size_t render_ws_smem_bytes() { return sizeof(ws::Smem); }
+
+// march pass over packet-ordered ray ids + the warp-specialised kernel
+cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEvent_t* ev) {
+  const long long rays = (long long)(p.row_end - p.row_begin) * p.cam.width;
+  if (rays <= 0) return cudaSuccess;
+  static int blocks_per_sm = -1;
+  const size_t smem = render_ws_smem_bytes();
+  cudaError_t e;
+  if (blocks_per_sm < 0) {
+    if ((e = cudaFuncSetAttribute(ws::k_render_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem)) != cudaSuccess)
+      return e;
+    if ((e = cudaFuncSetAttribute(ws::k_render_ws, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  100)) != cudaSuccess)
+      return e;
+    int n = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ws::k_render_ws, ws::kCtaThreads, smem)) !=
+        cudaSuccess)
+      return e;
+    cudaFuncAttributes fa;
+    if ((e = cudaFuncGetAttributes(&fa, ws::k_render_ws)) != cudaSuccess) return e;
+    int dev = 0, smem_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    const int by_regs = 65536 / (((fa.numRegs * 32 + 255) / 256) * 256 * (ws::kCtaThreads / 32));
+    const int by_smem = smem_sm / (int)(smem + 1024);
+    blocks_per_sm = std::max(1, std::min({by_regs, by_smem, 4}));  // TMEM: 128 columns per CTA
+    if (std::getenv("LUMI_MAX_CTAS"))
+      blocks_per_sm = std::max(1, std::min(blocks_per_sm, std::atoi(std::getenv("LUMI_MAX_CTAS"))));
+    if (std::getenv("LUMI_DEBUG"))
+      std::fprintf(stderr, "[lumi] k_render_ws: %zu B smem (SM %d), %d regs, occupancy API %d, "
+                   "by regs %d, by smem %d -> %d CTAs/SM\n", smem, smem_sm, fa.numRegs, n, by_regs,
+                   by_smem, blocks_per_sm);
+  }
+  p.tile_w = pk::kPW;
+  p.tile_h = pk::kPH;
+  p.tiles_x = (p.cam.width + pk::kPW - 1) / pk::kPW;
+  const long long packets =
+      (long long)p.tiles_x * ((p.row_end - p.row_begin + pk::kPH - 1) / pk::kPH);
+  p.total_rays = packets * 32;
+  if (p.total_rays >= (1ll << 31)) return cudaErrorInvalidValue;
+  p.mask_words = (p.n + 31) / 32;
+  if ((e = cudaMallocAsync(&p.kept_mask, (size_t)p.total_rays * p.mask_words * 4, s)) != cudaSuccess)
+    return e;
+  if ((e = cudaMallocAsync(&p.kept_count, (size_t)p.total_rays * 2, s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(p.work_counter, 0, sizeof(unsigned int), s)) != cudaSuccess) return e;
+  RenderParams pm = p;
+  pm.work_stats = nullptr;
+  if (ev) cudaEventRecord(ev[0], s);
+  if ((e = launch_march_mask(pm, s)) != cudaSuccess) return e;
+  if (ev) cudaEventRecord(ev[1], s);
+  const long long grid = std::min<long long>((long long)blocks_per_sm * num_sms, (packets + 3) / 4);
+  ws::k_render_ws<<<(unsigned)grid, ws::kCtaThreads, smem, s>>>(p);
+  if (ev) cudaEventRecord(ev[2], s);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  cudaFreeAsync(p.kept_mask, s);
+  cudaFreeAsync(p.kept_count, s);
+  return cudaGetLastError();
+}

@@ -279,14 +279,15 @@ class DeviceModel:
         self.h = h
         self.field_version = field.version
         self.grid_version = grid.version
-        self.kernel = os.environ.get("LUMI_KERNEL", "packet")
+        self.kernel = os.environ.get("LUMI_KERNEL", "ws")
         self._lock = threading.Lock()
 
     def set_kernel(self, kernel: str) -> None:
-        """'packet' (packet-coherent tcgen05 kernel, default), 'tc' (one ray per thread
-        tcgen05 kernel) or 'simt' (fp32 CUDA-core cross-check)."""
+        """'ws' (warp-specialised packet kernel, default), 'packet' (packet-coherent tcgen05
+        kernel), 'tc' (one ray per thread tcgen05 kernel) or 'simt' (fp32 CUDA-core
+        cross-check)."""
         k = {"tc": _abi.LUMI_KERNEL_TC, "simt": _abi.LUMI_KERNEL_SIMT,
-             "packet": _abi.LUMI_KERNEL_PACKET}[kernel]
+             "packet": _abi.LUMI_KERNEL_PACKET, "ws": _abi.LUMI_KERNEL_WS}[kernel]
         check(_abi.lib().lumi_model_set_kernel(self.h, k))
         self.kernel = kernel
 

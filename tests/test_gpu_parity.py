@@ -120,7 +120,7 @@ def test_filtered_march_equals_exact_full_eye(lumi, torch_cuda, small, frame, co
     try:
         em, ec = march_kept_gpu(torch_cuda, lumi, dm, cam, opts, 0, 2048)
     finally:
-        dm.set_kernel("packet")
+        dm.set_kernel("ws")
     fm, fc = march_kept_gpu(torch_cuda, lumi, dm, cam, opts, 0, 2048)
     assert ec.sum() > 0
     assert np.array_equal(fc, ec)
@@ -169,15 +169,16 @@ def test_render_counts_vs_reference(lumi, torch_cuda, small, golden_c1):
     assert ev_match > 0.99 and co_match > 0.99
 
 
-@pytest.mark.parametrize("kernel", ["packet", "tc", "simt"])
+@pytest.mark.parametrize("kernel", ["ws", "packet", "tc", "simt"])
 def test_both_kernels_vs_reference_golden(lumi, torch_cuda, small, golden_c1, kernel):
-    """The tcgen05 production kernel and the fp32 CUDA-core cross-check kernel."""
+    """The tcgen05 kernels (warp-specialised production, packet, ray-per-thread) and the fp32
+    CUDA-core cross-check kernel, each with exact per-pixel evaluated / contributing counts."""
     cam = lumi.CameraModel.from_spec(scenes.pinhole(256, 256))
     small["dm"].set_kernel(kernel)
     try:
         out, _, opac, stats = _render(lumi, small["dm"], cam, lumi.RenderOptions())
     finally:
-        small["dm"].set_kernel("packet")
+        small["dm"].set_kernel("ws")
     err = np.abs(out - golden_c1["out"]).max()
     print(f"{kernel}: C1 max|dPQ|={err:.3e} PSNR={psnr(out, golden_c1['out']):.1f} dB")
     assert err <= (1e-6 if kernel == "simt" else PIX_TOL)
