@@ -42,8 +42,24 @@ constexpr int kCtaThreads = 256;  // consumers [0, 128), producers [128, 256)
 #endif
 constexpr int kProdPairs = WS_PROD_PAIRS;  // pairs per producer thread per gather step
 // named barriers: 0 = __syncthreads (setup / teardown), LIST_READY 1 + b, GATHER_DONE 3 + b,
-// 5 = consumer warpgroup only
-constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5;
+// 5 = consumer warpgroup only, 6 = producer warpgroup only
+constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5, kBarProd = 6;
+
+#ifdef LUMI_PHASE_TIMING
+// warp-cycles: producers [wait list, gather], consumers [fill+geometry+list, wait gather, MLP,
+// composite]
+__device__ unsigned long long g_ws_cycles[6];
+#define WS_T(k)                                                    \
+  do {                                                             \
+    const long long _t = clock64();                                \
+    if (lane == 0) atomicAdd(&g_ws_cycles[k], (unsigned long long)(_t - t_last)); \
+    t_last = _t;                                                   \
+  } while (0)
+#else
+#define WS_T(k) \
+  do {          \
+  } while (0)
+#endif
 
 struct __align__(16) Smem {
   uint8_t A[2][128 * (32 + kKb) * 2];  // double-buffered layer-1 A tiles (chunk-major, a_off)
@@ -62,8 +78,9 @@ struct __align__(16) Smem {
   int stop[2];
   uint4 lvl[kMaxLevels];
   float4 samp[2][128];
-  uint16_t pairs[2][kWarps][32 * kMaxLevels];
-  int npairs[2][kWarps];
+  uint8_t na[2][128];                        // per row: active LOD levels (0 = no sample)
+  uint16_t pairs[kWarps][32 * kMaxLevels];   // producers' gather lists of the current round
+  int npairs[kWarps];
 };
 
 // named barriers with immediate ids, so ptxas reserves only the barriers used (a register id
@@ -137,6 +154,9 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = s.tmem_base;
+#ifdef LUMI_PHASE_TIMING
+  long long t_last = clock64();
+#endif
 
   if (wg == 1) {
     // ================================ producers ==============================================
@@ -144,11 +164,31 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
     for (int j = 0;; ++j) {
       const int b = j & 1;
       list_ready_sync(b);
+      WS_T(0);
       if (s.stop[b]) break;
+      {
+        // clear this row's features (buffer b's last reader, the MMA of round j-2, is done)
+        // and list the (row, level) pairs of producer warp w's 32 rows, level-major
+        const uint4 zero = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) st16(s.A[b], a_off(ctid, q), zero);
+        const int na = s.na[b][ctid];
+        uint16_t* pc = s.pairs[warp];
+        const unsigned lt = (1u << lane) - 1u;
+        int npairs = 0;
+        for (int l = 0; l < kMaxLevels; ++l) {
+          const unsigned m = __ballot_sync(FULL, na > l);
+          if (m == 0u) break;
+          if (na > l) pc[npairs + __popc(m & lt)] = (uint16_t)pair_code(lane, l);
+          npairs += __popc(m);
+        }
+        if (lane == 0) s.npairs[warp] = npairs;
+      }
+      bar_sync<kBarProd, 128>();
       int pre[kWarps + 1];
       pre[0] = 0;
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) pre[w + 1] = pre[w] + s.npairs[b][w];
+      for (int w = 0; w < kWarps; ++w) pre[w + 1] = pre[w] + s.npairs[w];
       const int total = pre[kWarps];
       const uint8_t* Pb = reinterpret_cast<const uint8_t*>(s.samp[b]);
 #pragma unroll 1
@@ -162,7 +202,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
           woff[q] = 0;
           if (pi < total) {
             const int w = (pi >= pre[1]) + (pi >= pre[2]) + (pi >= pre[3]);
-            code[q] = s.pairs[b][w][pi - pre[w]];
+            code[q] = s.pairs[w][pi - pre[w]];
             woff[q] = (uint32_t)w * 32u * 16u;  // the warp's rows in A (a_off) and samp
           }
         }
@@ -182,7 +222,9 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
             *reinterpret_cast<__half2*>(s.A[b] + woff[q] + code[q]) = __floats2half2_rn(f[q].x, f[q].y);
       }
       ptx::fence_async_smem();
+      bar_sync<kBarProd, 128>();  // every producer is done with this round's lists
       gather_done_arrive(b);
+      WS_T(1);
     }
   } else {
     // ================================ consumers ==============================================
@@ -324,33 +366,22 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
         cnt.level_samples += na;
         ++cnt.evals;
       }
-      {  // this row's A features (buffer b; its last reader, the MMA of round j-2, is done)
-        const uint4 zero = make_uint4(0, 0, 0, 0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) st16(s.A[b], a_off(ctid, q), zero);
+      {  // the row's gather input for the producers: grid coordinates, LOD, active levels
         const float fl = lw.floor_only ? 1e-4f : (float)lw.full + lw.frac;
         if (have) s.samp[b][ctid] = make_float4(u, v, w, fl);
-        uint16_t* pc = s.pairs[b][warp];
-        const unsigned lt = (1u << lane) - 1u;
-        int npairs = 0;
-        for (int l = 0; l < levels; ++l) {
-          const unsigned m = __ballot_sync(FULL, na > l);
-          if (m == 0u) break;
-          if (na > l) pc[npairs + __popc(m & lt)] = (uint16_t)pair_code(lane, l);
-          npairs += __popc(m);
-        }
-        if (lane == 0) s.npairs[b][warp] = npairs;
+        s.na[b][ctid] = (uint8_t)na;
       }
       // all consumer warps finished (every packet stored) -> the producers stop after round j
       const bool stop = bar_and<kBarCons, 128>(no_more && !packet_live);
       if (ctid == 0) s.stop[b] = stop ? 1 : 0;
-      ptx::fence_async_smem();
       list_ready_arrive(b);
+      WS_T(2);
 
       if (j > 0) {
         // ---- M(j-1): the tcgen05 MLP over round j-1's 128 rows (field.h:106-137) ----------
         const int bp = (j - 1) & 1;
         gather_done_sync(bp);
+        WS_T(3);
         const int rlp = s.rowlane[bp][ctid];
         const float pdx = __shfl_sync(FULL, r.d.x, rlp), pdy = __shfl_sync(FULL, r.d.y, rlp),
                     pdz = __shfl_sync(FULL, r.d.z, rlp);
@@ -421,6 +452,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
           s.res[ctid] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
         }
         __syncwarp();
+        WS_T(4);
         // ---- C(j-1): owners composite their samples of round j-1 in order ----------------
         uint32_t mine = s.own[bp][warp][lane];
         while (mine && r.alive) {
@@ -445,6 +477,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
           }
         }
       }
+      WS_T(5);
       // a finished packet is stored once its last round is composited (renderer.h:233-236)
       if (pending && j - 1 >= last_round) {
         if (r.valid) {
@@ -523,7 +556,22 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
   if ((e = launch_march_mask(pm, s)) != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[1], s);
   const long long grid = std::min<long long>((long long)blocks_per_sm * num_sms, (packets + 3) / 4);
+#ifdef LUMI_PHASE_TIMING
+  unsigned long long z6[6] = {0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbolAsync(ws::g_ws_cycles, z6, sizeof(z6), 0, cudaMemcpyHostToDevice, s);
+#endif
   ws::k_render_ws<<<(unsigned)grid, ws::kCtaThreads, smem, s>>>(p);
+#ifdef LUMI_PHASE_TIMING
+  {
+    unsigned long long c[6];
+    cudaMemcpyFromSymbolAsync(c, ws::g_ws_cycles, sizeof(c), 0, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const double tp = (double)(c[0] + c[1]), tc = (double)(c[2] + c[3] + c[4] + c[5]);
+    std::fprintf(stderr, "[lumi] ws producers: wait list %.1f%% gather %.1f%% | consumers: fill %.1f%% "
+                 "wait gather %.1f%% mlp %.1f%% composite %.1f%%\n", 100 * c[0] / tp, 100 * c[1] / tp,
+                 100 * c[2] / tc, 100 * c[3] / tc, 100 * c[4] / tc, 100 * c[5] / tc);
+  }
+#endif
   if (ev) cudaEventRecord(ev[2], s);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   cudaFreeAsync(p.kept_mask, s);
