@@ -44,6 +44,10 @@ constexpr int kProdPairs = WS_PROD_PAIRS;  // pairs per producer thread per gath
 // named barriers: 0 = __syncthreads (setup / teardown), LIST_READY 1 + b, GATHER_DONE 3 + b,
 // 5 = consumer warpgroup only, 6 = producer warpgroup only
 constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5, kBarProd = 6;
+#ifndef WS_CONS_LEVELS
+#define WS_CONS_LEVELS 1
+#endif
+constexpr int kConsLevels = WS_CONS_LEVELS;  // LOD levels gathered by the consumers (<= 4)
 
 #ifdef LUMI_PHASE_TIMING
 // warp-cycles: producers [wait list, gather], consumers [fill+geometry+list, wait gather, MLP,
@@ -171,12 +175,12 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
         // and list the (row, level) pairs of producer warp w's 32 rows, level-major
         const uint4 zero = make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) st16(s.A[b], a_off(ctid, q), zero);
+        for (int q = 1; q < 4; ++q) st16(s.A[b], a_off(ctid, q), zero);  // chunk 0: consumers
         const int na = s.na[b][ctid];
         uint16_t* pc = s.pairs[warp];
         const unsigned lt = (1u << lane) - 1u;
         int npairs = 0;
-        for (int l = 0; l < kMaxLevels; ++l) {
+        for (int l = kConsLevels; l < kMaxLevels; ++l) {
           const unsigned m = __ballot_sync(FULL, na > l);
           if (m == 0u) break;
           if (na > l) pc[npairs + __popc(m & lt)] = (uint16_t)pair_code(lane, l);
@@ -368,9 +372,24 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
       }
       {  // the row's gather input for the producers: grid coordinates, LOD, active levels
         const float fl = lw.floor_only ? 1e-4f : (float)lw.full + lw.frac;
+        // the consumers gather the first kConsLevels levels of their own rows themselves (it
+        // balances the two warpgroups) into A chunk 0, which they also clear
+        {
+          float2 f[kConsLevels];
+#pragma unroll
+          for (int l = 0; l < kConsLevels; ++l) {
+            f[l] = make_float2(0.f, 0.f);
+            if (na > l) f[l] = gather_level(s.lvl[l], u, v, w, __saturatef(fl - (float)l));
+          }
+          uint32_t wds[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+          for (int l = 0; l < kConsLevels; ++l) wds[l] = h2u(__floats2half2_rn(f[l].x, f[l].y));
+          st16(s.A[b], a_off(ctid, 0), make_uint4(wds[0], wds[1], wds[2], wds[3]));
+        }
         if (have) s.samp[b][ctid] = make_float4(u, v, w, fl);
         s.na[b][ctid] = (uint8_t)na;
       }
+      ptx::fence_async_smem();
       // all consumer warps finished (every packet stored) -> the producers stop after round j
       const bool stop = bar_and<kBarCons, 128>(no_more && !packet_live);
       if (ctid == 0) s.stop[b] = stop ? 1 : 0;
