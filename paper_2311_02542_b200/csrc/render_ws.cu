@@ -83,8 +83,8 @@ struct __align__(16) Smem {
   uint4 lvl[kMaxLevels];
   float4 samp[2][128];
   uint8_t na[2][128];                        // per row: active LOD levels (0 = no sample)
-  uint16_t pairs[kWarps][32 * kMaxLevels];   // producers' gather lists of the current round
-  int npairs[kWarps];
+  uint16_t pairs[kWarps * 32 * kMaxLevels];  // the round's gather list, warp lists concatenated
+  int cnt[2][kWarps];                        // per warp: pairs the producers will list
 };
 
 // named barriers with immediate ids, so ptxas reserves only the barriers used (a register id
@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
       list_ready_sync(b);
       WS_T(0);
       if (s.stop[b]) break;
+      int total_pairs;
       {
         // clear this row's features (buffer b's last reader, the MMA of round j-2, is done)
         // and list the (row, level) pairs of producer warp w's 32 rows, level-major
@@ -177,44 +178,39 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
 #pragma unroll
         for (int q = 1; q < 4; ++q) st16(s.A[b], a_off(ctid, q), zero);  // chunk 0: consumers
         const int na = s.na[b][ctid];
-        uint16_t* pc = s.pairs[warp];
+        int npairs = 0, total = 0;  // this warp's list starts after the lower warps' (counted by the consumers)
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+          const int c = s.cnt[b][w];
+          npairs += w < warp ? c : 0;
+          total += c;
+        }
         const unsigned lt = (1u << lane) - 1u;
-        int npairs = 0;
         for (int l = kConsLevels; l < kMaxLevels; ++l) {
           const unsigned m = __ballot_sync(FULL, na > l);
           if (m == 0u) break;
-          if (na > l) pc[npairs + __popc(m & lt)] = (uint16_t)pair_code(lane, l);
+          if (na > l) s.pairs[npairs + __popc(m & lt)] = (uint16_t)pair_code(ctid, l);
           npairs += __popc(m);
         }
-        if (lane == 0) s.npairs[warp] = npairs;
+        total_pairs = total;
       }
       bar_sync<kBarProd, 128>();
-      int pre[kWarps + 1];
-      pre[0] = 0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) pre[w + 1] = pre[w] + s.npairs[w];
-      const int total = pre[kWarps];
+      const int total = total_pairs;
       const uint8_t* Pb = reinterpret_cast<const uint8_t*>(s.samp[b]);
 #pragma unroll 1
       for (int base = 0; base < total; base += 128 * kProdPairs) {
-        uint32_t code[kProdPairs], woff[kProdPairs];
+        uint32_t code[kProdPairs];
         float2 f[kProdPairs];
 #pragma unroll
         for (int q = 0; q < kProdPairs; ++q) {
           const int pi = base + 128 * q + ctid;
-          code[q] = 0xffffu;
-          woff[q] = 0;
-          if (pi < total) {
-            const int w = (pi >= pre[1]) + (pi >= pre[2]) + (pi >= pre[3]);
-            code[q] = s.pairs[w][pi - pre[w]];
-            woff[q] = (uint32_t)w * 32u * 16u;  // the warp's rows in A (a_off) and samp
-          }
+          code[q] = pi < total ? (uint32_t)s.pairs[pi] : 0xffffu;
         }
 #pragma unroll
         for (int q = 0; q < kProdPairs; ++q) {
           f[q] = make_float2(0.f, 0.f);
-          if (code[q] != 0xffffu) {
-            const float4 P = *reinterpret_cast<const float4*>(Pb + woff[q] + (code[q] & 0x1F0u));
+          if (code[q] != 0xffffu) {  // code = the feature's byte offset in A; row * 16 in samp
+            const float4 P = *reinterpret_cast<const float4*>(Pb + (code[q] & 0x7F0u));
             const int lv = pair_level(code[q]);
             const float wl = __saturatef(P.w - (float)lv);
             f[q] = gather_level(s.lvl[lv], P.x, P.y, P.z, wl);
@@ -223,7 +219,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
 #pragma unroll
         for (int q = 0; q < kProdPairs; ++q)
           if (code[q] != 0xffffu)
-            *reinterpret_cast<__half2*>(s.A[b] + woff[q] + code[q]) = __floats2half2_rn(f[q].x, f[q].y);
+            *reinterpret_cast<__half2*>(s.A[b] + code[q]) = __floats2half2_rn(f[q].x, f[q].y);
       }
       ptx::fence_async_smem();
       bar_sync<kBarProd, 128>();  // every producer is done with this round's lists
@@ -388,6 +384,9 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
         }
         if (have) s.samp[b][ctid] = make_float4(u, v, w, fl);
         s.na[b][ctid] = (uint8_t)na;
+        const int mine = na > kConsLevels ? na - kConsLevels : 0;  // the producers' pairs of this row
+        const int wsum = __reduce_add_sync(FULL, (unsigned)mine);
+        if (lane == 0) s.cnt[b][warp] = wsum;
       }
       ptx::fence_async_smem();
       // all consumer warps finished (every packet stored) -> the producers stop after round j
