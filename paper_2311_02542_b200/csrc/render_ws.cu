@@ -38,14 +38,14 @@ using namespace pk;
 
 constexpr int kCtaThreads = 256;  // consumers [0, 128), producers [128, 256)
 #ifndef WS_PROD_PAIRS
-#define WS_PROD_PAIRS 3
+#define WS_PROD_PAIRS 2
 #endif
 constexpr int kProdPairs = WS_PROD_PAIRS;  // pairs per producer thread per gather step
 // named barriers: 0 = __syncthreads (setup / teardown), LIST_READY 1 + b, GATHER_DONE 3 + b,
 // 5 = consumer warpgroup only, 6 = producer warpgroup only
 constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5, kBarProd = 6;
 #ifndef WS_CONS_LEVELS
-#define WS_CONS_LEVELS 1
+#define WS_CONS_LEVELS 0
 #endif
 constexpr int kConsLevels = WS_CONS_LEVELS;  // LOD levels gathered by the consumers (<= 4)
 
@@ -371,15 +371,13 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
         // the consumers gather the first kConsLevels levels of their own rows themselves (it
         // balances the two warpgroups) into A chunk 0, which they also clear
         {
-          float2 f[kConsLevels];
-#pragma unroll
-          for (int l = 0; l < kConsLevels; ++l) {
-            f[l] = make_float2(0.f, 0.f);
-            if (na > l) f[l] = gather_level(s.lvl[l], u, v, w, __saturatef(fl - (float)l));
-          }
           uint32_t wds[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-          for (int l = 0; l < kConsLevels; ++l) wds[l] = h2u(__floats2half2_rn(f[l].x, f[l].y));
+          for (int l = 0; l < kConsLevels; ++l) {
+            float2 f = make_float2(0.f, 0.f);
+            if (na > l) f = gather_level(s.lvl[l], u, v, w, __saturatef(fl - (float)l));
+            wds[l] = h2u(__floats2half2_rn(f.x, f.y));
+          }
           st16(s.A[b], a_off(ctid, 0), make_uint4(wds[0], wds[1], wds[2], wds[3]));
         }
         if (have) s.samp[b][ctid] = make_float4(u, v, w, fl);
