@@ -396,7 +396,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "path": "lumi_render_rows (C ABI, host buffers)" if world == 1 else
+                "path": "lumi_render_rows (C ABI) into pinned host buffers: the kernel stores the pixels over PCIe (zero-copy)" if world == 1 else
                         "StereoFrameDriver + D2H of the gathered frame"},
         "gpu_launches": launches,
         "cpu_baseline": cpu,

@@ -170,7 +170,9 @@ int lumi_model_bytes(const LumiModel* m, uint64_t* bytes);
 /* ---- rendering ------------------------------------------------------------------ */
 /* Drop-in for render_rows (renderer.h:252-278): host planar buffers of the camera's
    full image size, rows [row_begin,row_end) written.  depth/opacity/stats may be NULL;
-   stats receives (row_end-row_begin) entries.  Synchronous. */
+   stats receives (row_end-row_begin) entries.  Synchronous.  Page-locked (pinned) planes
+   are written by the kernel directly (zero-copy, no device->host copy afterwards; set
+   LUMI_ZERO_COPY=0 to disable); pageable planes go through a device staging copy. */
 int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions* opts,
                      int row_begin, int row_end, float* out, float* depth, float* opacity,
                      LumiRowStats* stats);

@@ -589,6 +589,23 @@ int lumi_march_kept_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRen
   return LUMI_OK;
 }
 
+// Device address of page-locked host memory (nullptr for pageable memory, or when
+// LUMI_ZERO_COPY=0 disables direct stores).
+static float* zero_copy_ptr(float* host) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("LUMI_ZERO_COPY");
+    return !(e && e[0] == '0');
+  }();
+  if (!enabled || !host) return nullptr;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+    cudaGetLastError();  // pageable memory on older runtimes reports an error: clear it
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+  return static_cast<float*>(a.devicePointer);
+}
+
 int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions* o, int b,
                      int e, float* out, float* depth, float* opacity, LumiRowStats* stats) {
   if (!m) return fail(LUMI_ERR_INVALID, "null model");
@@ -639,6 +656,14 @@ int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOp
   int64_t* d_rows = reinterpret_cast<int64_t*>(d_buf + plane * nplanes + 64);
   if ((ce = cudaMemsetAsync(d_rows, 0, rows * sizeof(int64_t), s)) != cudaSuccess)
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
+  // Zero-copy output: when the caller's planes are pinned (page-locked, hence mapped into the
+  // device's address space under UVA), the kernel stores the pixels straight into them over
+  // PCIe while it renders -- a packet's 8-pixel rows are 32-byte coalesced writes -- and no
+  // device->host copy follows.  Pageable planes go through the device staging planes.
+  float* z_rgb = zero_copy_ptr(out);
+  float* z_depth = depth ? zero_copy_ptr(depth) : nullptr;
+  float* z_opac = opacity ? zero_copy_ptr(opacity) : nullptr;
+  const bool zero_copy = z_rgb && (!depth || z_depth) && (!opacity || z_opac);
   float* d_depth = depth ? d_buf + 3 * plane : nullptr;
   float* d_opac = opacity ? d_buf + (3 + (depth ? 1 : 0)) * plane : nullptr;
   LumiFrameTarget t{};
@@ -649,19 +674,26 @@ int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOp
   t.width = W;
   t.height = rows;
   t.row_offset = -b;
+  if (zero_copy) {
+    t.rgb = z_rgb;
+    t.depth = z_depth;
+    t.opacity = z_opac;
+    t.height = cam->height;
+    t.row_offset = 0;
+  }
   cudaEventRecord(st->e0, s);
   if ((rc = lumi_render_rows_async(m, cam, o, b, e, &t, s))) return done(rc);
   cudaEventRecord(st->e1, s);
   const size_t full = static_cast<size_t>(W) * cam->height;
-  for (int c = 0; c < 3; ++c)
+  for (int c = 0; c < 3 && !zero_copy; ++c)
     if ((ce = cudaMemcpyAsync(out + c * full + static_cast<size_t>(b) * W, d_buf + c * plane,
                               plane * sizeof(float), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
       return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
-  if (depth &&
+  if (depth && !zero_copy &&
       (ce = cudaMemcpyAsync(depth + static_cast<size_t>(b) * W, d_depth, plane * sizeof(float),
                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
-  if (opacity &&
+  if (opacity && !zero_copy &&
       (ce = cudaMemcpyAsync(opacity + static_cast<size_t>(b) * W, d_opac, plane * sizeof(float),
                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));

@@ -357,3 +357,22 @@ def test_concurrent_workers_and_optional_planes(lumi, torch_cuda, small):
             t.join()
         assert not errs
         assert np.array_equal(par, full), f"rep {rep}"
+
+
+def test_zero_copy_pinned_output_equals_staged(lumi, torch_cuda, small):
+    """lumi_render_rows writes page-locked planes directly from the kernel (zero-copy) and
+    pageable planes through a device staging copy: same pixels, depth, opacity and stats,
+    rows outside [b, e) untouched."""
+    cam = lumi.CameraModel.from_spec(scenes.pinhole(256, 128))
+    opts = lumi.RenderOptions()
+    dm = small["dm"]
+    pg = [np.full((3, 128, 256), -1, np.float32), np.full((128, 256), -1, np.float32),
+          np.full((128, 256), -1, np.float32)]
+    pn = [torch_cuda.full(a.shape, -1.0).pin_memory().numpy() for a in pg]
+    st_pg, st_pn = [], []
+    dm.render_rows(cam, opts, 20, 100, pg[0], pg[1], pg[2], st_pg)
+    dm.render_rows(cam, opts, 20, 100, pn[0], pn[1], pn[2], st_pn)
+    for a, b_ in zip(pg, pn):
+        assert np.array_equal(a, b_)
+    assert (pn[0][:, :20] == -1).all() and (pn[0][:, 100:] == -1).all()
+    assert [s.evals for s in st_pg] == [s.evals for s in st_pn]
