@@ -641,7 +641,7 @@ int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOp
     m->staging.push_back(std::move(st));
     return code;
   };
-  const size_t need = plane * nplanes * sizeof(float) + rows * sizeof(int64_t) + 256;
+  const size_t need = plane * nplanes * sizeof(float) + rows * sizeof(int64_t) + 512;
   cudaError_t ce;
   if (st->bytes < need) {
     cudaFree(st->buf);
@@ -653,7 +653,9 @@ int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOp
   }
   cudaStream_t s = st->s;
   float* d_buf = static_cast<float*>(st->buf);
-  int64_t* d_rows = reinterpret_cast<int64_t*>(d_buf + plane * nplanes + 64);
+  // the per-row eval counters (64-bit atomics) start 256-byte aligned after the planes
+  const size_t rows_off = (plane * nplanes * sizeof(float) + 255) & ~static_cast<size_t>(255);
+  int64_t* d_rows = reinterpret_cast<int64_t*>(static_cast<char*>(st->buf) + rows_off);
   if ((ce = cudaMemsetAsync(d_rows, 0, rows * sizeof(int64_t), s)) != cudaSuccess)
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
   // Zero-copy output: when the caller's planes are pinned (page-locked, hence mapped into the

@@ -199,10 +199,13 @@ def test_split_render_bit_identical(lumi, torch_cuda, small):
 
 
 @pytest.mark.parametrize("variant", ["lod_off", "bias", "nocut", "background", "spp64",
-                                     "chunk7", "rotated"])
+                                     "chunk7", "rotated", "odd_sizes"])
 def test_render_options_vs_oracle(lumi, torch_cuda, small, oracle, variant):
     kw, okw = {}, {}
     spec = scenes.pinhole(64, 48)
+    if variant == "odd_sizes":  # partial packets on both axes, spp not a multiple of 32
+        spec = scenes.pinhole(37, 48)
+        kw["samples_per_ray"] = okw["samples_per_ray"] = 77
     if variant == "lod_off":
         kw["lod_enabled"] = okw["lod_enabled"] = False
     if variant == "bias":
@@ -376,3 +379,25 @@ def test_zero_copy_pinned_output_equals_staged(lumi, torch_cuda, small):
         assert np.array_equal(a, b_)
     assert (pn[0][:, :20] == -1).all() and (pn[0][:, 100:] == -1).all()
     assert [s.evals for s in st_pg] == [s.evals for s in st_pn]
+
+
+@pytest.mark.parametrize("band", [(5, 19), (0, 1), (47, 48), (13, 13)])
+def test_odd_row_bands_every_kernel(lumi, torch_cuda, small, oracle, band):
+    """Row bands that start and end inside a 4-row packet (and empty / one-row bands) on a
+    37-pixel-wide image, every tcgen05 kernel against the oracle; rows outside the band are
+    untouched (renderer.h:252-278)."""
+    spec = scenes.pinhole(37, 48)
+    cam = lumi.CameraModel.from_spec(spec)
+    b, e = band
+    ref = oracle.render_rows(small["model"], ocam(spec), O.render_options(), 0, 48)
+    dm = small["dm"]
+    for kernel in ("ws", "packet", "tc"):
+        dm.set_kernel(kernel)
+        try:
+            out = np.full((3, 48, 37), -1, np.float32)
+            dm.render_rows(cam, lumi.RenderOptions(), b, e, out)
+        finally:
+            dm.set_kernel("ws")
+        assert (out[:, :b] == -1).all() and (out[:, e:] == -1).all(), kernel
+        if e > b:
+            assert np.abs(out[:, b:e] - ref["out"][:, b:e]).max() <= PIX_TOL, kernel
