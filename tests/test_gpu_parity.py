@@ -199,10 +199,14 @@ def test_split_render_bit_identical(lumi, torch_cuda, small):
 
 
 @pytest.mark.parametrize("variant", ["lod_off", "bias", "nocut", "background", "spp64",
-                                     "chunk7", "rotated", "odd_sizes"])
+                                     "chunk7", "rotated", "odd_sizes", "nocontract", "bias_up"])
 def test_render_options_vs_oracle(lumi, torch_cuda, small, oracle, variant):
     kw, okw = {}, {}
     spec = scenes.pinhole(64, 48)
+    if variant == "nocontract":
+        kw["contraction"] = okw["contraction"] = 0
+    if variant == "bias_up":
+        kw["lod_bias"] = okw["lod_bias"] = 1.75
     if variant == "odd_sizes":  # partial packets on both axes, spp not a multiple of 32
         spec = scenes.pinhole(37, 48)
         kw["samples_per_ray"] = okw["samples_per_ray"] = 77
