@@ -153,8 +153,8 @@ int lumi_model_set_occupancy(LumiModel* m, const uint8_t* occupancy, int occ_res
    thread), LUMI_KERNEL_PACKET (tcgen05, warp-wide ray packets streamed candidate-major for
    coherent gathers) or LUMI_KERNEL_SIMT (thread-per-ray fp32 CUDA-core MLP -- the numerical
    cross-check), LUMI_KERNEL_WS (the packet kernel warp-specialised: a producer warpgroup
-   gathers while the consumer warpgroup runs the MLP, pipelined one round apart).  The
-   environment variable LUMI_KERNEL=tc|packet|simt|ws sets the default. */
+   gathers while the consumer warpgroup runs the MLP, pipelined one round apart; the
+   default).  The environment variable LUMI_KERNEL=tc|packet|simt|ws sets the default. */
 enum { LUMI_KERNEL_TC = 0, LUMI_KERNEL_SIMT = 1, LUMI_KERNEL_PACKET = 2, LUMI_KERNEL_WS = 3 };
 int lumi_model_set_kernel(LumiModel* m, int kernel);
 int lumi_model_destroy(LumiModel* m);

@@ -5,9 +5,10 @@
 // before those at i+1.  Every round a warp contributes 32 consecutive samples of its stream
 // as its 32 rows of the CTA's 128-row MLP batch, so the rows of a warp are neighbouring rays
 // at the same distance -- they gather neighbouring (often identical) hash-grid cells, which
-// is what keeps the L1 wavefront count per gather low.  The batch then runs through the five
-// tcgen05 layers exactly as in render_tc.cu, and each ray's owner lane composites its
-// samples of the round in order (renderer.h:170-190).
+// is what keeps the L1 wavefront count per gather low.  The batch then runs through four
+// tcgen05 layers (density L2 folded into colour L1), and each ray's owner lane composites its
+// samples of the round in order (renderer.h:170-190).  The production renderer, render_ws.cu,
+// runs the same stages warp-specialised; this kernel stays as LUMI_KERNEL=packet.
 //
 // Per-sample geometry for the network input is fp32 (position, contraction, LOD footprint):
 // the oracle measures no change against double coordinates (1.24e-4 vs 1.36e-4 max |dPQ| on
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_pk(RenderParams p) {
     }
     PT_MARK(3);
 
-    // ---- MLP: five tcgen05 layers over the 128-row batch (field.h:106-137) -------------
+    // ---- MLP: four tcgen05 layers (density L2 folded into colour L1) over the 128-row batch (field.h:106-137) -------------
     float v32[32];
     // layer 1 reads the gathered features from shared memory (SS form); the hidden layers
     // keep their fp16 activations in TMEM columns [kAcol, kAcol + K/2) as the A operand
