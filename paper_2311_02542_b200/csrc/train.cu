@@ -11,12 +11,13 @@
 //   (scan)            per-ray sample offsets
 //   k_train_samples   thread per ray: one record per kept sample (contracted position, t,
 //                     delta, LOD weights, inner flag)
-//   k_train_forward   thread per sample: bit-exact fp32 encode + fp32 MLP -> sigma, colour
+//   k_train_tiles<0>  the forward of every kept sample in 128-sample tiles (the backward's
+//                     own forward, below): bit-exact fp32 encode + fp32 MLP -> sigma, colour
 //   k_train_loss      thread per ray: front-to-back compositing with the early cut, the
 //                     chunk-rounded evaluated count, ray_loss, composite_backward_sigma
 //                     -> dL/dsigma and dL/dcolour per evaluated sample
 //   (scan + compact)  the evaluated samples of every ray
-//   k_train_backward  persistent, 128-sample tiles: recompute the activations into shared
+//   k_train_tiles<1>  persistent, 128-sample tiles: recompute the activations into shared
 //                     memory, back-propagate through the colour and density MLPs, weight
 //                     gradients accumulated per CTA in shared memory (one owner thread per
 //                     entry, register-blocked over the tile), hash-grid scatter-add with
@@ -25,8 +26,9 @@
 //
 // Compiled with -fmad=false: double compositing/loss arithmetic and float expressions round
 // like the reference's non-FMA translation units; the MLP uses explicit fmaf in the same
-// four-chain order as the SIMT renderer (mlp_simt.cuh), so forward and recomputed
-// activations are bit-identical between k_train_forward and k_train_backward.
+// four-chain order as the SIMT renderer (mlp_simt.cuh, the reference's AVX-512 order), and the
+// forward pass and the backward's recomputation are the same code, so their activations (and
+// ReLU masks) are bit-identical.
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
@@ -139,65 +141,6 @@ __device__ __forceinline__ LodW lodw_of(const TrainSample& s) {
 }
 
 __device__ __forceinline__ d3 ray_dir_of(const TrainParams& p, int r) { return ld3(p.rays[r].dir); }
-
-// ---- forward: sigma and colour of every kept sample (field.h:106-137) ------------------
-// Thread per sample, activations in registers, the fp32 weights staged once per CTA in shared
-// memory (16-B broadcast loads); per output the four-chain fmaf order of mlp_simt.cuh dense().
-template <int OUT, int IN, bool RELU>
-__device__ __forceinline__ void dense_s(const float* W, const float* x, float* y) {
-  const float* b = W + OUT * IN;
-#pragma unroll
-  for (int r = 0; r < OUT; ++r) {
-    const float4* w4 = reinterpret_cast<const float4*>(W + r * IN);
-    float a0 = b[r], a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-    for (int c = 0; c < IN / 4; ++c) {
-      const float4 w = w4[c];
-      a0 = fmaf(w.x, x[4 * c + 0], a0);
-      a1 = fmaf(w.y, x[4 * c + 1], a1);
-      a2 = fmaf(w.z, x[4 * c + 2], a2);
-      a3 = fmaf(w.w, x[4 * c + 3], a3);
-    }
-    const float v = (a0 + a1) + (a2 + a3);
-    y[r] = RELU ? fmaxf(v, 0.f) : v;
-  }
-}
-
-
-__global__ void __launch_bounds__(128, 3) k_train_forward(TrainParams p, const TrainSample* smp, int total,
-                                                       float* sig, float* col) {
-  __shared__ __align__(16) float w[kDensityPad + kColorPad];
-  for (int e = threadIdx.x; e < kDensityParams; e += blockDim.x) w[e] = __ldg(p.mlp.dparams + e);
-  for (int e = threadIdx.x; e < kColorParams; e += blockDim.x) w[kDensityPad + e] = __ldg(p.mlp.cparams + e);
-  __syncthreads();
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= total) return;
-  const TrainSample q = smp[s];
-  float feat[kFeat], h[kHidden], h2[kHidden], dout[1 + kBottleneck], cin[kBottleneck + 16];
-  encode(p.grid, d3{q.c[0], q.c[1], q.c[2]}, lodw_of(q), feat);
-  const float* dp = w;
-  dense_s<kHidden, kFeat, true>(dp, feat, h);
-  dense_s<1 + kBottleneck, kHidden, false>(dp + kHidden * kFeat + kHidden, h, dout);
-  const float sigma = trunc_exp(dout[0]);
-#pragma unroll
-  for (int i = 0; i < kBottleneck; ++i) cin[i] = dout[1 + i];
-  {
-    float sh[16];
-    sh_encode(ray_dir_of(p, q.ray), sh);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) cin[kBottleneck + i] = sh[i];
-  }
-  const float* cp = w + kDensityPad;
-  dense_s<kHidden, kBottleneck + 16, true>(cp, cin, h);
-  cp += kHidden * (kBottleneck + 16) + kHidden;
-  dense_s<kHidden, kHidden, true>(cp, h, h2);
-  cp += kHidden * kHidden + kHidden;
-  float raw[3];
-  dense_s<3, kHidden, false>(cp, h2, raw);
-  sig[s] = sigma;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) col[3 * s + k] = p.mlp.color_space == 0 ? sigmoid(raw[k]) : trunc_exp(raw[k]);
-}
 
 __device__ __forceinline__ double sgn(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0); }
 
@@ -360,7 +303,7 @@ __global__ void __launch_bounds__(128) k_train_compact(TrainParams p, const int*
 
 // y[o][s] for the output blocks o = 4b .. 4b+3, b = h, h + 2, ... (the thread pair of sample s
 // splits the rows): per output the same four-chain fmaf order as mlp_simt.cuh dense(), so
-// activations match k_train_forward bit for bit; four outputs share every activation load.
+// activations are the same in both passes; four outputs share every activation load.
 // W: the layer's weights [OUT x IN] then bias [OUT], in shared memory (16-B aligned rows).
 template <int OUT, int IN, bool RELU>
 __device__ __forceinline__ void fwd_layer(const float* W, const float* x, float* y, int s, int h) {
@@ -492,16 +435,21 @@ __device__ __forceinline__ void scatter_level(const TrainParams& p, int l, doubl
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_train_backward(TrainParams p, const TrainSample* smp,
-                                                                const int* act, int nact,
-                                                                const float* dsig_g, const float* dcol_g) {
+// BWD = false: the forward only, over every kept sample (act == nullptr), writing sigma and
+// colour for the compositing pass -- the same arithmetic the backward recomputes.
+template <bool BWD>
+__global__ void __launch_bounds__(kThreads, 1) k_train_tiles(TrainParams p, const TrainSample* smp,
+                                                             const int* act, int nact,
+                                                             const float* dsig_g, const float* dcol_g,
+                                                             float* sig_out, float* col_out) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, s = tid & (kTile - 1), h = tid >> 7;
   float* X = S.act;
   float* dWd = S.dW;
   float* dWc = S.dW + kDensityParams;
-  for (int e = tid; e < kDensityParams + kColorParams; e += kThreads) S.dW[e] = 0.f;
+  if (BWD)
+    for (int e = tid; e < kDensityParams + kColorParams; e += kThreads) S.dW[e] = 0.f;
   for (int e = tid; e < kDensityParams; e += kThreads) S.wts[e] = __ldg(p.mlp.dparams + e);
   for (int e = tid; e < kColorParams; e += kThreads) S.wts[kDensityPad + e] = __ldg(p.mlp.cparams + e);
   const float* dp = S.wts;
@@ -514,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_backward(TrainParams p, c
     // ---- 1. inputs: features (levels split over the thread pair), SH and the output
     //      gradients (pair thread 1) ----
     {
-      const int si = s < nvalid ? act[tile * kTile + s] : -1;
+      const int si = s < nvalid ? (BWD ? act[tile * kTile + s] : tile * kTile + s) : -1;
       if (h == 0) S.sample[s] = si;
       if (si >= 0) {
         const TrainSample q = smp[si];
@@ -541,10 +489,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_backward(TrainParams p, c
         float ds = 0.f, dc[3] = {0.f, 0.f, 0.f};
         if (si >= 0) {
           sh_encode(ray_dir_of(p, smp[si].ray), sh);
-          ds = dsig_g[si];
-          dc[0] = dcol_g[3 * si + 0];
-          dc[1] = dcol_g[3 * si + 1];
-          dc[2] = dcol_g[3 * si + 2];
+          if (BWD) {
+            ds = dsig_g[si];
+            dc[0] = dcol_g[3 * si + 0];
+            dc[1] = dcol_g[3 * si + 1];
+            dc[2] = dcol_g[3 * si + 2];
+          }
         } else {
 #pragma unroll
           for (int k = 0; k < 16; ++k) sh[k] = 0.f;
@@ -571,6 +521,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_backward(TrainParams p, c
     __syncthreads();
     fwd_layer<3, kHidden, false>(cp + oC3, X + rC2 * kS, X + rCRAW * kS, s, h);
     __syncthreads();
+    if (!BWD) {  // sigma = trunc_exp(raw0), colour head (field.h:116-118, 131-136)
+      if (h == 0 && s < nvalid) {
+        const int si = tile * kTile + s;
+        sig_out[si] = trunc_exp(X[rDOUT * kS + s]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const float raw = X[(rCRAW + k) * kS + s];
+          col_out[3 * si + k] = p.mlp.color_space == 0 ? sigmoid(raw) : trunc_exp(raw);
+        }
+      }
+      continue;
+    }
     // ---- 3. backward (field.h:141-179) -----------------------------------------------------
     if (h == 0) {  // colour head: dL/draw (field.h:148-160); padded rows get zero gradients
 #pragma unroll
@@ -625,9 +587,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_backward(TrainParams p, c
       }
     }
   }
-  __syncthreads();
-  for (int e = tid; e < kDensityParams; e += kThreads) atomicAdd(p.g_density + e, dWd[e]);
-  for (int e = tid; e < kColorParams; e += kThreads) atomicAdd(p.g_color + e, dWc[e]);
+  if (BWD) {
+    __syncthreads();
+    for (int e = tid; e < kDensityParams; e += kThreads) atomicAdd(p.g_density + e, dWd[e]);
+    for (int e = tid; e < kColorParams; e += kThreads) atomicAdd(p.g_color + e, dWc[e]);
+  }
 }
 
 // Deterministic sums over rays: block 0 the loss terms (trainer.cpp:556-559), block 1 + c the
@@ -756,7 +720,21 @@ cudaError_t launch_train_backward(TrainParams p, cudaStream_t s, int num_sms, lo
       (e = act.alloc(T)))
     return e;
   tr::k_train_samples<<<mb, 128, 0, s>>>(p, words, masks.p, off.p, smp.p);
-  if (total > 0) tr::k_train_forward<<<(unsigned)((total + 127) / 128), 128, 0, s>>>(p, smp.p, total, sig.p, col.p);
+  static bool attr = false;
+  const size_t smem = sizeof(tr::Smem);
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(tr::k_train_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem)) ||
+        (e = cudaFuncSetAttribute(tr::k_train_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem)))
+      return e;
+    attr = true;
+  }
+  if (total > 0) {
+    const int ftiles = (total + tr::kTile - 1) / tr::kTile;
+    tr::k_train_tiles<false><<<std::min(ftiles, num_sms), tr::kThreads, smem, s>>>(
+        p, smp.p, nullptr, total, nullptr, nullptr, sig.p, col.p);
+  }
   if ((e = cudaMemsetAsync(evals.p + p.nrays, 0, sizeof(int), s))) return e;
   tr::k_train_loss<<<rb, 128, 0, s>>>(p, off.p, cnt.p, smp.p, sig.p, col.p, wbuf.p, evals.p, dsig.p,
                                       dcol.p, terms.p);
@@ -768,17 +746,9 @@ cudaError_t launch_train_backward(TrainParams p, cudaStream_t s, int num_sms, lo
   if (eval_total) *eval_total = nact;
   tr::k_train_compact<<<rb, 128, 0, s>>>(p, off.p, aoff.p, evals.p, act.p);
   if (nact > 0) {
-    static bool attr = false;
-    const size_t smem = sizeof(tr::Smem);
-    if (!attr) {
-      if ((e = cudaFuncSetAttribute(tr::k_train_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem)))
-        return e;
-      attr = true;
-    }
     const int tiles = (nact + tr::kTile - 1) / tr::kTile;
-    tr::k_train_backward<<<std::min(tiles, num_sms), tr::kThreads, smem, s>>>(p, smp.p, act.p, nact,
-                                                                              dsig.p, dcol.p);
+    tr::k_train_tiles<true><<<std::min(tiles, num_sms), tr::kThreads, smem, s>>>(
+        p, smp.p, act.p, nact, dsig.p, dcol.p, nullptr, nullptr);
   }
   tr::k_train_reduce<<<1 + p.ncams, 256, 0, s>>>(p, terms.p);
   return cudaGetLastError();
