@@ -29,7 +29,7 @@ def _worker(rank, world, port, result_dir):
         S, W = 48, 40  # two 48-row eyes stacked
         H = 2 * S
         assign = equal_assignment(H, world)
-        cost = [1.0, 2.5]  # rank 1 is 2.5x slower per row
+        cost = [1.0, 2.5, 1.5, 1.0][:world]  # per-row cost of each rank
         for frame in range(8):
             img = torch.full((3, H, W), -1.0)
             rr = assign.ranges[rank]
@@ -62,6 +62,21 @@ def test_two_rank_gather_and_rebalance(tmp_path):
     assert np.array_equal(r0, r1)  # identical partition on every rank
     # throughput-proportional: rank 0 (2.5x faster per row) converges to ~5/7 of 96 rows
     assert abs(int(r0[0]) - round(96 * 2.5 / 3.5)) <= 2, r0
+
+
+def test_four_rank_gather_and_rebalance(tmp_path):
+    """Four ranks with per-row costs 1 : 2.5 : 1.5 : 1 -- bands crossing the eye seam, uneven
+    gathers, and the dampened throughput-proportional split (scheduler.cpp:68-87)."""
+    torch = pytest.importorskip("torch")
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(4, _free_port(), str(tmp_path)), nprocs=4, join=True)
+    rows = [np.load(tmp_path / f"rows{r}.npy") for r in range(4)]
+    for r in rows[1:]:
+        assert np.array_equal(r, rows[0])
+    speed = np.array([1 / 1.0, 1 / 2.5, 1 / 1.5, 1 / 1.0])
+    want = 96 * speed / speed.sum()
+    assert np.abs(rows[0] - want).max() <= 2.5, (rows[0], want)
+    assert rows[0].sum() == 96
 
 
 def test_eye_bands_split_at_seam():
