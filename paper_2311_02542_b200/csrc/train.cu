@@ -39,7 +39,11 @@ namespace lumi_dev {
 namespace tr {
 
 constexpr int kTile = 128;              // samples per backward tile
-constexpr int kThreads = 256;           // two threads per sample
+#ifndef LUMI_TRAIN_SPLIT
+#define LUMI_TRAIN_SPLIT 4
+#endif
+constexpr int kSplit = LUMI_TRAIN_SPLIT;  // threads per sample (they split rows / levels)
+constexpr int kThreads = kTile * kSplit;
 constexpr int kS = kTile + 4;           // activation row stride (floats): 16-B aligned rows
 constexpr int kIn = kBottleneck + 16;   // colour-network input width
 // activation rows in shared memory
@@ -301,7 +305,7 @@ __global__ void __launch_bounds__(128) k_train_compact(TrainParams p, const int*
 
 // ---- backward over 128-sample tiles ------------------------------------------------------
 
-// y[o][s] for the output blocks o = 4b .. 4b+3, b = h, h + 2, ... (the thread pair of sample s
+// y[o][s] for the output blocks o = 4b .. 4b+3, b = h, h + kSplit, ... (the kSplit threads of sample s
 // splits the rows): per output the same four-chain fmaf order as mlp_simt.cuh dense(), so
 // activations are the same in both passes; four outputs share every activation load.
 // W: the layer's weights [OUT x IN] then bias [OUT], in shared memory (16-B aligned rows).
@@ -310,7 +314,7 @@ __device__ __forceinline__ void fwd_layer(const float* W, const float* x, float*
   const float* bias = W + OUT * IN;
   constexpr int NB = (OUT + 3) / 4;
 #pragma unroll 1
-  for (int b = h; b < NB; b += 2) {
+  for (int b = h; b < NB; b += kSplit) {
     float a[4][4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -350,7 +354,7 @@ template <int OUT, int IN, int NI, bool MASK>
 __device__ __forceinline__ void bwd_data(const float* W, const float* dy, const float* x, float* dx,
                                          int s, int h) {
 #pragma unroll 1
-  for (int b = h; b < NI / 4; b += 2) {
+  for (int b = h; b < NI / 4; b += kSplit) {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll 8
     for (int o = 0; o < OUT; ++o) {
@@ -459,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_tiles(TrainParams p, cons
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int nvalid = min(kTile, nact - tile * kTile);
     __syncthreads();  // previous tile's scatter reads FEAT; dW updates are owner-only
-    // ---- 1. inputs: features (levels split over the thread pair), SH and the output
+    // ---- 1. inputs: features (levels split over the sample's threads), SH and the output
     //      gradients (pair thread 1) ----
     {
       const int si = s < nvalid ? (BWD ? act[tile * kTile + s] : tile * kTile + s) : -1;
@@ -469,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_tiles(TrainParams p, cons
         const LodW lw = lodw_of(q);
         const double u = dmul(dadd(q.c[0], 2.0), 0.25), v = dmul(dadd(q.c[1], 2.0), 0.25),
                      w = dmul(dadd(q.c[2], 2.0), 0.25);
-        for (int l = h; l < kMaxLevels; l += 2) {  // encode (grid.h:90-114), bit-exact
+        for (int l = h; l < kMaxLevels; l += kSplit) {  // encode (grid.h:90-114), bit-exact
           float2 f = make_float2(0.f, 0.f);
           if (l < p.grid.levels) {
             const float wl = lod_weight_at(lw, l);
@@ -479,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_tiles(TrainParams p, cons
           X[(rFEAT + 2 * l + 1) * kS + s] = f.y;
         }
       } else {
-        for (int l = h; l < kMaxLevels; l += 2) {
+        for (int l = h; l < kMaxLevels; l += kSplit) {
           X[(rFEAT + 2 * l) * kS + s] = 0.f;
           X[(rFEAT + 2 * l + 1) * kS + s] = 0.f;
         }
@@ -513,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_tiles(TrainParams p, cons
     __syncthreads();
     fwd_layer<1 + kBottleneck, kHidden, false>(dp + oD2, X + rH * kS, X + rDOUT * kS, s, h);
     __syncthreads();
-    for (int b = h; b < kBottleneck; b += 2) X[(rCIN + b) * kS + s] = X[(rDOUT + 1 + b) * kS + s];
+    for (int b = h; b < kBottleneck; b += kSplit) X[(rCIN + b) * kS + s] = X[(rDOUT + 1 + b) * kS + s];
     __syncthreads();
     fwd_layer<kHidden, kIn, true>(cp + oC1, X + rCIN * kS, X + rC1 * kS, s, h);
     __syncthreads();
@@ -574,13 +578,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_tiles(TrainParams p, cons
     __syncthreads();
     bwd_data<kHidden, kFeat, kFeat, false>(dp + oD1, X + rH * kS, nullptr, X + rFEAT * kS, s, h);
     __syncthreads();
-    // ---- 4. hash-grid scatter-add (grid.h:118-137), levels split over the thread pair ----
+    // ---- 4. hash-grid scatter-add (grid.h:118-137), levels split over the sample's threads ----
     if (s < nvalid) {
       const TrainSample q = smp[S.sample[s]];
       const LodW lw = lodw_of(q);
       const double u = dmul(dadd(q.c[0], 2.0), 0.25), v = dmul(dadd(q.c[1], 2.0), 0.25),
                    w = dmul(dadd(q.c[2], 2.0), 0.25);
-      for (int l = h; l < p.grid.levels; l += 2) {
+      for (int l = h; l < p.grid.levels; l += kSplit) {
         const float wl = lod_weight_at(lw, l);
         if (!(wl > 0.f)) continue;
         scatter_level(p, l, u, v, w, wl, X[(rFEAT + 2 * l) * kS + s], X[(rFEAT + 2 * l + 1) * kS + s]);
