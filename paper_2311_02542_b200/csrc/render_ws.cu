@@ -1,20 +1,22 @@
-// render_ws.cu -- warp-specialised packet renderer.
+// render_ws.cu -- warp-specialised packet renderer (the production frame kernel).
 //
 // The packet kernel (render_pk.cu) is latency bound with 16 warps per SM, and every resource
 // that would admit more row-owning warps is full (TMEM 4 x 128 columns, 128 registers x 512
 // threads, 57 KB of shared memory x 4).  Here each CTA pairs a CONSUMER warpgroup -- the four
-// row-owning warps: packet streams, geometry, gather lists, the tcgen05 MLP and compositing --
-// with a PRODUCER warpgroup of four warps that only runs the hash-grid gather (half the
-// instructions).  The two are pipelined one round apart through double-buffered layer-1 A
-// tiles and gather lists, synchronised with named barriers (one pair per buffer), so a CTA of
-// 8 warps fits 3 times per SM: 24 warps instead of 16.  The math of every stage is the packet
-// kernel's (pk_parts.cuh); only the schedule differs:
+// row-owning warps: packet streams, geometry, the tcgen05 MLP and compositing -- with a
+// PRODUCER warpgroup of four warps that clears the A rows, builds the gather list and runs the
+// hash-grid gather (half the instructions).  The two are pipelined one round apart through
+// double-buffered layer-1 A tiles and row inputs, synchronised with named barriers (one pair
+// per buffer), so a CTA of 8 warps fits 3 times per SM: 24 warps instead of 16.  The math of
+// every stage is the packet kernel's (pk_parts.cuh); only the schedule differs:
 //
-//   consumers, iteration j:  fill/geometry/list of round j into buffer j&1
+//   consumers, iteration j:  fill + geometry of round j into buffer j&1 (per row: grid
+//                            coordinates, LOD, active levels; per warp: its pair count)
 //                            -> arrive LIST_READY[j&1]
 //                            -> wait GATHER_DONE[(j-1)&1] -> MLP + composite of round j-1
-//   producers, iteration j:  wait LIST_READY[j&1] -> gather round j (all four warps' lists,
-//                            dealt over 128 threads) -> arrive GATHER_DONE[j&1]
+//   producers, iteration j:  wait LIST_READY[j&1] -> clear A rows, write ONE concatenated
+//                            level-major list whose codes are the features' A offsets ->
+//                            gather it over 128 threads -> arrive GATHER_DONE[j&1]
 //
 // Because round j is filled before round j-1 is composited, a packet whose stream ends is
 // stored only after the last round holding its rows is composited (one idle round per packet
