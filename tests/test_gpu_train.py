@@ -103,6 +103,22 @@ def test_train_backward_matches_oracle(L, torch_cuda, oracle, case):
     assert ev.sum() > 0 and loss.total > 0
 
 
+def test_train_backward_per_camera_sampling_intervals(L, torch_cuda, oracle):
+    """Cameras with their own (t_near, t_far) (trainer.cpp:553 marches each ray with its
+    camera's interval): per-camera sample distances, 128 samples per ray."""
+    import dataclasses
+    from paper_2311_02542_b200 import train as T
+    field, dm, om = _models(L, oracle, scenes.SMALL)
+    cams = scenes.train_cameras(192, 3)
+    cams = [dataclasses.replace(c, t_near=tn, t_far=tf)
+            for c, (tn, tf) in zip(cams, [(0.05, 10.0), (0.2, 2.5), (0.1, 6.0)])]
+    rays = scenes.train_batch(cams, 64, seed=21)
+    o = dict(samples_per_ray=128)
+    loss, ev = _compare(L, oracle, dm, om, rays, cams, np.array([0.02, 0.0, 0.07]),
+                        L.RenderOptions(**o), O.render_options(**o), T.TrainConfig())
+    assert ev.sum() > 0
+
+
 def test_train_backward_reference_batch_full_model(L, torch_cuda, oracle):
     """The reference's batch shape (50 images x 256 rays, trainer.h:20-21) on the full
     T=2^22 model (dense level 0)."""
