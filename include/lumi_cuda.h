@@ -187,6 +187,13 @@ int lumi_march_kept_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRen
                           int row_begin, int row_end, uint32_t* mask, int32_t* counts,
                           void* stream);
 
+/* The renderer's tcgen05 MLP alone over a dense batch (RadianceField::forward_chunk after
+   the encoding, field.h:114-136): features [n][32] fp16, view directions [n][3] fp32 -> out
+   [n][4] fp32 (sigma, r, g, b).  Device pointers, enqueued on `stream`.  For measuring the
+   tensor-core stage in isolation and checking it against the oracle. */
+int lumi_mlp_batch_async(LumiModel* m, const void* features, const float* dirs, int n, float* out,
+                         void* stream);
+
 /* ---- checkpoint ingest (host) ---------------------------------------------------- */
 /* LUMICKPT v1 (proj/src/scene.cpp:286-394, occupancy.cpp:200-243). */
 typedef struct LumiCheckpointInfo {

@@ -785,6 +785,19 @@ int lumi_bake_occupancy(LumiModel* m, const LumiCameraDesc* cams, int ncams, int
   return done(LUMI_OK);
 }
 
+int lumi_mlp_batch_async(LumiModel* m, const void* features, const float* dirs, int n, float* out,
+                         void* stream) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  if (n < 0 || (n > 0 && (!features || !dirs || !out))) return fail(LUMI_ERR_INVALID, "mlp_batch: bad buffers");
+  if ((reinterpret_cast<uintptr_t>(features) & 15) != 0)
+    return fail(LUMI_ERR_INVALID, "mlp_batch: features must be 16-byte aligned");
+  DeviceGuard dg(m->device);
+  lumi_dev::MlpDev mlp{m->d_dparams, m->d_cparams, m->d_fused, m->desc.color_space};
+  cudaError_t e = launch_mlp_batch(mlp, features, dirs, n, out, m->num_sms, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(LUMI_ERR_CUDA, std::string("mlp_batch: ") + cudaGetErrorString(e));
+  return LUMI_OK;
+}
+
 // ---- training reverse path (trainer.cpp:549-561) ------------------------------------------
 
 static_assert(sizeof(LumiTrainRay) == sizeof(lumi_dev::LumiTrainRayDev), "LumiTrainRay layout");

@@ -1,0 +1,178 @@
+// mlp_batch.cu -- the renderer's tcgen05 MLP on an isolated dense batch ("report
+// tensor-pipe utilisation from ncu on an isolated dense batch, not only the fused kernel").
+//
+// RadianceField::forward_chunk (field.h:106-137) minus the encoding: n samples of 32 fp16
+// hash-grid features ([n][32], row-major) and a per-sample view direction go through exactly
+// the production kernel's four layers (pk_parts.cuh: density L1 SS-form from shared memory,
+// density L2 folded into colour L1 as one N=80 layer, colour L2, colour L3, activations in
+// TMEM, biases as an extra K step) and out come sigma and the three colour channels.
+// Persistent, 4 CTAs of 128 threads per SM (TMEM: 128 columns each); each 128-row tile is
+// loaded with 16-byte vector loads into the chunk-major A tile.  Numerics are the renderer's,
+// so it doubles as a parity check of the MLP stage alone (tests/test_gpu_parity.py).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "pk_parts.cuh"
+
+namespace lumi_dev {
+namespace mb {
+
+using namespace pk;
+
+struct __align__(16) Smem {
+  uint8_t A[128 * (32 + kKb) * 2];
+  uint8_t W1[64 * (32 + kKb) * 2];
+  uint8_t F[80 * (80 + kKb) * 2];
+  uint8_t C2[64 * (64 + kKb) * 2];
+  uint8_t C3[16 * (64 + kKb) * 2];
+  uint64_t mbar;
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(128, 4) k_mlp_batch(MlpDev mlp, const __half* __restrict__ feat,
+                                                      const float* __restrict__ dirs, int n,
+                                                      float4* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const float* dp = mlp.dparams;
+  const float* cp = mlp.cparams;
+  const float* c2 = cp + 64 * 32 + 64;
+  const float* c3 = c2 + 64 * 64 + 64;
+  load_weight_tile(s.W1, dp, 64, 64, 32);
+  load_weight_tile(s.F, mlp.fused, kHidden + 1, 80, 80);
+  load_weight_tile(s.C2, c2, 64, 64, 64);
+  load_weight_tile(s.C3, c3, 3, 16, 64);
+  st16(s.A, a_off(tid, 4), make_uint4(0x3C00u, 0u, 0u, 0u));
+  st16(s.A, a_off(tid, 5), make_uint4(0u, 0u, 0u, 0u));
+  if (tid == 0) {
+    ptx::mbar_init(&s.mbar, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0) ptx::tmem_alloc<kTmemCols>(&s.tmem_base);
+  ptx::fence_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+  const uint32_t t_lane = tmem + ((uint32_t)(warp * 32) << 16);
+  {
+    const uint32_t ones[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    ptx::tmem_st8(t_lane + kOnesCol, ones);
+    ptx::tmem_st_wait();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+  }
+  const uint32_t a_tmem = tmem + kAcol, ones_tmem = tmem + kOnesCol, a_lane = t_lane + kAcol;
+  uint32_t phase = 0;
+  const int tiles = (n + 127) / 128;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int row = tile * 128 + tid;
+    const bool have = row < n;
+    // this row's 32 fp16 features -> A chunks 0..3 (four 16-byte vectors)
+    const uint4* src = reinterpret_cast<const uint4*>(feat + (size_t)row * 32);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) st16(s.A, a_off(tid, q), have ? __ldg(src + q) : make_uint4(0, 0, 0, 0));
+    float dx = 0.f, dy = 0.f, dz = 1.f;
+    if (have) {
+      dx = __ldg(dirs + 3 * (size_t)row);
+      dy = __ldg(dirs + 3 * (size_t)row + 1);
+      dz = __ldg(dirs + 3 * (size_t)row + 2);
+    }
+    ptx::fence_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    float v32[32];
+    if (tid == 0) {
+      ptx::tc_fence_after();
+      issue_layer<64, 32>(s.A, s.W1, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+    relu64_to_tmem(t_lane, a_lane);
+    {
+      float sh[16];
+      sh_encode(d3{(double)dx, (double)dy, (double)dz}, sh);
+      uint32_t wv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) wv[j] = pack2(sh[2 * j], sh[2 * j + 1]);
+      ptx::tmem_st8(t_lane + kShCol, wv);
+      ptx::tmem_st_wait();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      ptx::tc_fence_after();
+      issue_layer_ts<80, 80>(a_tmem, ones_tmem, s.F, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+    ptx::tmem_ld16(t_lane + 64, v32);
+    ptx::tmem_ld_wait();
+    const float sigma = trunc_exp_fast(v32[0]);
+    relu64_to_tmem(t_lane, a_lane);
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      ptx::tc_fence_after();
+      issue_layer_ts<64, 64>(a_tmem, ones_tmem, s.C2, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+    relu64_to_tmem(t_lane, a_lane);
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      ptx::tc_fence_after();
+      issue_layer_ts<16, 64>(a_tmem, ones_tmem, s.C3, tmem);
+      ptx::mma_commit(&s.mbar);
+    }
+    ptx::mbar_wait(&s.mbar, phase);
+    phase ^= 1;
+    ptx::tc_fence_after();
+    ptx::tmem_ld16(t_lane, v32);
+    ptx::tmem_ld_wait();
+    ptx::tc_fence_before();
+    if (have) {
+      float rgb[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) rgb[k] = mlp.color_space == 0 ? sigmoid_fast(v32[k]) : trunc_exp_fast(v32[k]);
+      out[row] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
+    }
+    __syncthreads();  // the A tile and TMEM are rewritten by the next tile
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 0) ptx::tmem_dealloc<kTmemCols>(tmem);
+}
+
+}  // namespace mb
+}  // namespace lumi_dev
+
+using namespace lumi_dev;
+
+cudaError_t launch_mlp_batch(const MlpDev& mlp, const void* feat, const float* dirs, int n, float* out,
+                             int num_sms, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = sizeof(mb::Smem);
+  static bool attr = false;
+  cudaError_t e;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(mb::k_mlp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+      return e;
+    attr = true;
+  }
+  const int tiles = (n + 127) / 128;
+  mb::k_mlp_batch<<<std::min(tiles, 4 * num_sms), 128, smem, s>>>(
+      mlp, static_cast<const __half*>(feat), dirs, n, reinterpret_cast<float4*>(out));
+  return cudaGetLastError();
+}

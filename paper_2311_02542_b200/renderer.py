@@ -357,6 +357,14 @@ class DeviceModel:
                                                row_end, C.c_void_p(mask_ptr),
                                                C.c_void_p(counts_ptr), C.c_void_p(stream)))
 
+    def mlp_batch_async(self, features_ptr: int, dirs_ptr: int, n: int, out_ptr: int,
+                        stream: int = 0) -> None:
+        """The renderer's tcgen05 MLP alone: device features [n][32] fp16 and directions
+        [n][3] fp32 -> out [n][4] fp32 (sigma, r, g, b) (field.h:114-136)."""
+        check(_abi.lib().lumi_mlp_batch_async(self.h, C.c_void_p(features_ptr),
+                                              C.c_void_p(dirs_ptr), int(n),
+                                              C.c_void_p(out_ptr), C.c_void_p(stream)))
+
     def bake_occupancy(self, cams: Sequence[CameraModel], samples_per_ray: int,
                        points_per_axis: int, resolution: int, alpha: float,
                        want_probe: bool = False):

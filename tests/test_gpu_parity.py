@@ -405,3 +405,28 @@ def test_odd_row_bands_every_kernel(lumi, torch_cuda, small, oracle, band):
         assert (out[:, :b] == -1).all() and (out[:, e:] == -1).all(), kernel
         if e > b:
             assert np.abs(out[:, b:e] - ref["out"][:, b:e]).max() <= PIX_TOL, kernel
+
+
+def test_mlp_batch_vs_oracle(lumi, torch_cuda, small, oracle):
+    """The tcgen05 MLP stage alone (lumi_mlp_batch_async) on oracle-encoded features of random
+    points: sigma and colour against RadianceField::forward_chunk (field.h:106-137) with fp16
+    operands (colour within 2e-3, sigma within 1 % -- sigma = exp(raw) magnifies the fp16
+    rounding of the 64-wide dot products)."""
+    torch = torch_cuda
+    rng = np.random.default_rng(8)
+    n = 4096
+    pos = rng.uniform(-1.8, 1.8, (n, 3))
+    lodw = np.ones((n, 16), np.float32)
+    d = rng.normal(size=3)
+    d /= np.linalg.norm(d)
+    sh = oracle.sh_encode(d)
+    sigma, color, feat = oracle.field_forward(small["model"], pos, lodw, sh)
+    f16 = torch.from_numpy(np.ascontiguousarray(feat.T)).half().cuda()
+    dirs = torch.from_numpy(np.tile(d, (n, 1)).astype(np.float32)).cuda()
+    out = torch.zeros((n, 4), dtype=torch.float32, device="cuda")
+    small["dm"].mlp_batch_async(f16.data_ptr(), dirs.data_ptr(), n, out.data_ptr(),
+                                torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    assert np.abs(o[:, 1:] - color.T).max() <= 2e-3
+    assert np.abs(o[:, 0] / sigma - 1).max() <= 1e-2
