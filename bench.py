@@ -120,6 +120,22 @@ def measured_peaks():
         return {}
 
 
+def gather_roofline(achieved, table_log2: int):
+    """The gather rate against the MEASURED rate of the same gather code in isolation
+    (tools/bench_gather.py -> profiles/r01_bench_gather.json: all 16 levels of packet-coherent
+    points on this table), the attainable ceiling of an irregular fp16 gather on this GPU."""
+    try:
+        g = json.load(open(os.path.join(ROOT, "profiles", "r01_bench_gather.json")))
+        peak = g["results"][f"T2^{table_log2}_coherent"]["gather_GBs"]
+    except Exception:
+        return None
+    if achieved is None:
+        return None
+    return {"bound": "gather", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "peak_source": "profiles/r01_bench_gather.json (tools/bench_gather.py, coherent points)"}
+
+
 def ncu_traffic(kernel: str):
     """dram bytes per launch from the committed ncu --set full capture, if any."""
     try:
@@ -390,6 +406,7 @@ def run_ours(args):
                                     f"{level_samples / max(world, 1):.3e} level-samples in "
                                     f"{render_launches} {kname} launches, {render_ms:.1f} ms "
                                     f"(CUDA events on the launch stream)"},
+        "roofline_gather": gather_roofline(achieved, spec.table_log2),
         "roofline_mlp": {"bound": "tensor", "achieved": None if mlp_tflops is None else round(mlp_tflops, 2),
                          "peak": peaks.get("bf16_tflops_sustained", 1398.6), "unit": "TFLOP/s",
                          "algorithmic": "18,944 FLOP per evaluated sample"},

@@ -194,6 +194,12 @@ int lumi_march_kept_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRen
 int lumi_mlp_batch_async(LumiModel* m, const void* features, const float* dirs, int n, float* out,
                          void* stream);
 
+/* The hash-grid gather alone (benchmark of the attainable gather rate): n points, every level
+   of each through the renderer's gather (fp16 table); coherent != 0 gives each warp an 8x4
+   patch of neighbouring points (like a ray packet), 0 uniform random points.  out: device
+   [n] floats.  Level-samples gathered = n * levels. */
+int lumi_gather_bench_async(LumiModel* m, int n, int coherent, float* out, void* stream);
+
 /* ---- checkpoint ingest (host) ---------------------------------------------------- */
 /* LUMICKPT v1 (proj/src/scene.cpp:286-394, occupancy.cpp:200-243). */
 typedef struct LumiCheckpointInfo {

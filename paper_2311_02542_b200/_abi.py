@@ -106,6 +106,7 @@ SIGNATURES = {
     "lumi_render_rows": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp], C.c_int),
     "lumi_render_rows_async": ([_vp, _vp, _vp, _i, _i, _vp, _vp], C.c_int),
     "lumi_march_kept_async": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp], C.c_int),
+    "lumi_gather_bench_async": ([_vp, _i, _i, _vp, _vp], C.c_int),
     "lumi_mlp_batch_async": ([_vp, _vp, _vp, _i, _vp, _vp], C.c_int),
     "lumi_checkpoint_read": ([C.c_char_p, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "lumi_bake_occupancy": ([_vp, _vp, _i, _i, _i, _i, _f, _vp, _vp], C.c_int),

@@ -785,6 +785,27 @@ int lumi_bake_occupancy(LumiModel* m, const LumiCameraDesc* cams, int ncams, int
   return done(LUMI_OK);
 }
 
+int lumi_gather_bench_async(LumiModel* m, int n, int coherent, float* out, void* stream) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  if (n < 0 || (n > 0 && !out)) return fail(LUMI_ERR_INVALID, "gather_bench: bad buffers");
+  DeviceGuard dg(m->device);
+  RenderParams rp;
+  LumiCameraDesc dummy{};
+  dummy.rot[0] = dummy.rot[4] = dummy.rot[8] = 1.0;
+  dummy.fx = dummy.fy = 1.0;
+  dummy.width = dummy.height = 1;
+  dummy.t_near = 0.05;
+  dummy.t_far = 10.0;
+  LumiRenderOptions o{};
+  o.samples_per_ray = 2;
+  o.chunk_size = 32;
+  int rc = make_params(m, &dummy, &o, 0, 0, &rp);
+  if (rc) return rc;
+  cudaError_t e = launch_gather_bench(rp.grid, n, coherent, out, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(LUMI_ERR_CUDA, std::string("gather_bench: ") + cudaGetErrorString(e));
+  return LUMI_OK;
+}
+
 int lumi_mlp_batch_async(LumiModel* m, const void* features, const float* dirs, int n, float* out,
                          void* stream) {
   if (!m) return fail(LUMI_ERR_INVALID, "null model");

@@ -1,5 +1,7 @@
-// mlp_batch.cu -- the renderer's tcgen05 MLP on an isolated dense batch ("report
-// tensor-pipe utilisation from ncu on an isolated dense batch, not only the fused kernel").
+// mlp_batch.cu -- the renderer's two stages in isolation: the tcgen05 MLP on a
+// dense batch ("report tensor-pipe utilisation from ncu on an isolated dense batch, not only
+// the fused kernel") and, at the end of the file, the hash-grid gather (the attainable gather
+// rate, the denominator for the L2-resident tables of C1/C2).
 //
 // RadianceField::forward_chunk (field.h:106-137) minus the encoding: n samples of 32 fp16
 // hash-grid features ([n][32], row-major) and a per-sample view direction go through exactly
@@ -174,5 +176,65 @@ cudaError_t launch_mlp_batch(const MlpDev& mlp, const void* feat, const float* d
   const int tiles = (n + 127) / 128;
   mb::k_mlp_batch<<<std::min(tiles, 4 * num_sms), 128, smem, s>>>(
       mlp, static_cast<const __half*>(feat), dirs, n, reinterpret_cast<float4*>(out));
+  return cudaGetLastError();
+}
+
+// ---- the hash-grid gather in isolation: the attainable gather rate ----------------------
+// report the gather against a measured gather peak (the table of C1/C2 is
+// L2-resident, so HBM is the wrong denominator there).  Every thread evaluates all levels of
+// one point with the renderer's own gather_level (fp16 table, 8 corners, fp16 weights, FHFMA);
+// points are either uniform random (no reuse between neighbouring threads) or coherent (the
+// 32 lanes of a warp sample a small neighbourhood, like a packet of neighbouring rays).
+namespace lumi_dev {
+namespace mb {
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+__device__ __forceinline__ float u01(uint32_t h) { return (h >> 8) * (1.f / 16777216.f); }
+
+__global__ void __launch_bounds__(256) k_gather_bench(GridDev g, int n, int coherent, float* out) {
+  __shared__ uint4 lvl[kMaxLevels];
+  for (int l = threadIdx.x; l < kMaxLevels; l += blockDim.x) {
+    const int res = l < g.levels ? g.res[l] : 1;
+    const unsigned long long base =
+        reinterpret_cast<unsigned long long>(g.table16 + (l < g.levels ? g.offset2[l] : 0));
+    lvl[l] = make_uint4((uint32_t)res, ((g.dense_mask >> l) & 1u) ? 0u : g.hash_mask[l],
+                        (uint32_t)base, (uint32_t)(base >> 32));
+  }
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float u, v, w;
+  if (coherent) {  // warp = an 8x4 patch of rays at one distance: ~1e-3 apart in the unit cube
+    const uint32_t wid = (uint32_t)i >> 5, lane = (uint32_t)i & 31u;
+    u = 0.25f + 0.5f * u01(hash32(3u * wid + 1u)) + 1e-3f * (float)(lane & 7u);
+    v = 0.25f + 0.5f * u01(hash32(3u * wid + 2u)) + 1e-3f * (float)(lane >> 3);
+    w = 0.25f + 0.5f * u01(hash32(3u * wid + 3u));
+  } else {
+    u = u01(hash32(3u * i + 1u));
+    v = u01(hash32(3u * i + 2u));
+    w = u01(hash32(3u * i + 3u));
+  }
+  float acc = 0.f;
+  for (int l = 0; l < g.levels; ++l) {
+    const float2 f = pk::gather_level(lvl[l], u, v, w, 1.f);
+    acc += f.x + f.y;
+  }
+  out[i] = acc;
+}
+
+}  // namespace mb
+}  // namespace lumi_dev
+
+cudaError_t launch_gather_bench(const lumi_dev::GridDev& g, int n, int coherent, float* out,
+                                cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  lumi_dev::mb::k_gather_bench<<<(n + 255) / 256, 256, 0, s>>>(g, n, coherent, out);
   return cudaGetLastError();
 }

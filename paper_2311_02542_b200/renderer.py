@@ -365,6 +365,11 @@ class DeviceModel:
                                               C.c_void_p(dirs_ptr), int(n),
                                               C.c_void_p(out_ptr), C.c_void_p(stream)))
 
+    def gather_bench_async(self, n: int, coherent: bool, out_ptr: int, stream: int = 0) -> None:
+        """The renderer's hash-grid gather alone over n points x all levels (benchmark)."""
+        check(_abi.lib().lumi_gather_bench_async(self.h, int(n), 1 if coherent else 0,
+                                                 C.c_void_p(out_ptr), C.c_void_p(stream)))
+
     def bake_occupancy(self, cams: Sequence[CameraModel], samples_per_ray: int,
                        points_per_axis: int, resolution: int, alpha: float,
                        want_probe: bool = False):
