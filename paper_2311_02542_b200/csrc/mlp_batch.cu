@@ -222,9 +222,16 @@ __global__ void __launch_bounds__(256) k_gather_bench(GridDev g, int n, int cohe
     w = u01(hash32(3u * i + 3u));
   }
   float acc = 0.f;
-  for (int l = 0; l < g.levels; ++l) {
-    const float2 f = pk::gather_level(lvl[l], u, v, w, 1.f);
-    acc += f.x + f.y;
+  // four levels in flight per thread (32 independent corner loads), the most ILP the
+  // renderer's producers could hold in registers
+#pragma unroll 1
+  for (int l0 = 0; l0 < g.levels; l0 += 4) {
+    float2 f[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      f[q] = l0 + q < g.levels ? pk::gather_level(lvl[l0 + q], u, v, w, 1.f) : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc += f[q].x + f[q].y;
   }
   out[i] = acc;
 }
