@@ -430,3 +430,23 @@ def test_mlp_batch_vs_oracle(lumi, torch_cuda, small, oracle):
     o = out.cpu().numpy()
     assert np.abs(o[:, 1:] - color.T).max() <= 2e-3
     assert np.abs(o[:, 0] / sigma - 1).max() <= 1e-2
+
+
+@pytest.mark.parametrize("kernel", ["ws", "packet", "tc", "simt"])
+def test_empty_grid_renders_background(lumi, torch_cuda, small, kernel):
+    """An empty occupancy grid marches no samples (proj/tests/test_renderer.cpp:201-217): every
+    pixel is the background, depth and opacity 0, zero evaluations."""
+    grid = lumi.OccupancyGrid(128, np.zeros(128 ** 3, np.uint8))
+    dm = lumi.DeviceModel(small["field"], grid, 0)
+    dm.set_kernel(kernel)
+    cam = lumi.CameraModel.from_spec(scenes.pinhole(64, 40))
+    bg = (0.25, 0.5, 0.125)
+    out = np.full((3, 40, 64), -1, np.float32)
+    depth = np.full((40, 64), -1, np.float32)
+    opac = np.full((40, 64), -1, np.float32)
+    stats = []
+    dm.render_rows(cam, lumi.RenderOptions(background=bg), 0, 40, out, depth, opac, stats)
+    for c in range(3):
+        assert (out[c] == np.float32(bg[c])).all()
+    assert not depth.any() and not opac.any()
+    assert sum(s.evals for s in stats) == 0
