@@ -14,6 +14,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.h"
 #include "pk_parts.cuh"
 
@@ -242,6 +244,11 @@ __global__ void __launch_bounds__(256) k_gather_bench(GridDev g, int n, int cohe
 cudaError_t launch_gather_bench(const lumi_dev::GridDev& g, int n, int coherent, float* out,
                                 cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  // LUMI_GATHER_CARVEOUT=<0..100>: shared-memory carveout, i.e. how much of the 256 KB of L1 +
+  // shared memory is left to the L1 data cache (the renderers run with ~20 KB of L1)
+  if (const char* c = std::getenv("LUMI_GATHER_CARVEOUT"))
+    cudaFuncSetAttribute(lumi_dev::mb::k_gather_bench, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         std::atoi(c));
   lumi_dev::mb::k_gather_bench<<<(n + 255) / 256, 256, 0, s>>>(g, n, coherent, out);
   return cudaGetLastError();
 }

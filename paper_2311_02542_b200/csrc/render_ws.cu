@@ -38,7 +38,13 @@ namespace ws {
 
 using namespace pk;
 
-constexpr int kCtaThreads = 256;  // consumers [0, 128), producers [128, 256)
+#ifndef WS_PROD_WARPS
+#define WS_PROD_WARPS 4
+#endif
+constexpr int kProdWarps = WS_PROD_WARPS;              // producer warps (4 or 8)
+constexpr int kProdThreads = 32 * kProdWarps;
+constexpr int kCtaThreads = 128 + kProdThreads;        // consumers [0, 128), producers after
+constexpr int kCtasPerSm = kProdWarps == 4 ? 3 : 2;    // (registers: <= 85 per thread)
 #ifndef WS_PROD_PAIRS
 #define WS_PROD_PAIRS 2
 #endif
@@ -124,10 +130,11 @@ __device__ __forceinline__ void gather_done_arrive(int b) {
   if (b) bar_arrive<kBarGather + 1, kCtaThreads>(); else bar_arrive<kBarGather, kCtaThreads>();
 }
 
-__global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
+__global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
-  const int tid = threadIdx.x, wg = tid >> 7, ctid = tid & 127, warp = ctid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, wg = tid >= 128 ? 1 : 0, ctid = wg ? tid - 128 : tid, warp = ctid >> 5,
+            lane = tid & 31;
   const unsigned FULL = 0xffffffffu;
 
   // ---- setup (all 256 threads) -------------------------------------------------------------
@@ -140,8 +147,10 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
   load_weight_tile(s.C2, c2, 64, 64, 64);
   load_weight_tile(s.C3, c3, 3, 16, 64);
   // constant ones block of both A buffers (never overwritten)
-  st16(s.A[wg], a_off(ctid, 4), make_uint4(0x3C00u, 0u, 0u, 0u));
-  st16(s.A[wg], a_off(ctid, 5), make_uint4(0u, 0u, 0u, 0u));
+  if (ctid < 128) {
+    st16(s.A[wg], a_off(ctid, 4), make_uint4(0x3C00u, 0u, 0u, 0u));
+    st16(s.A[wg], a_off(ctid, 5), make_uint4(0u, 0u, 0u, 0u));
+  }
   for (int l = tid; l < kMaxLevels; l += kCtaThreads) {
     const int res = l < p.grid.levels ? p.grid.res[l] : 1;
     const bool dense = (p.grid.dense_mask >> l) & 1u;
@@ -172,8 +181,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
       list_ready_sync(b);
       WS_T(0);
       if (s.stop[b]) break;
-      int total_pairs;
-      {
+      if (ctid < 128) {  // producer thread ctid < 128: row ctid
         // clear this row's features (buffer b's last reader, the MMA of round j-2, is done)
         // and list the (row, level) pairs of producer warp w's 32 rows, level-major
         const uint4 zero = make_uint4(0, 0, 0, 0);
@@ -194,18 +202,20 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
           if (na > l) s.pairs[npairs + __popc(m & lt)] = (uint16_t)pair_code(ctid, l);
           npairs += __popc(m);
         }
-        total_pairs = total;
+        (void)total;
       }
-      bar_sync<kBarProd, 128>();
-      const int total = total_pairs;
+      bar_sync<kBarProd, kProdThreads>();
+      int total = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) total += s.cnt[b][w];
       const uint8_t* Pb = reinterpret_cast<const uint8_t*>(s.samp[b]);
 #pragma unroll 1
-      for (int base = 0; base < total; base += 128 * kProdPairs) {
+      for (int base = 0; base < total; base += kProdThreads * kProdPairs) {
         uint32_t code[kProdPairs];
         float2 f[kProdPairs];
 #pragma unroll
         for (int q = 0; q < kProdPairs; ++q) {
-          const int pi = base + 128 * q + ctid;
+          const int pi = base + kProdThreads * q + ctid;
           code[q] = pi < total ? (uint32_t)s.pairs[pi] : 0xffffu;
         }
 #pragma unroll
@@ -224,7 +234,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_render_ws(RenderParams p) {
             *reinterpret_cast<__half2*>(s.A[b] + code[q]) = __floats2half2_rn(f[q].x, f[q].y);
       }
       ptx::fence_async_smem();
-      bar_sync<kBarProd, 128>();  // every producer is done with this round's lists
+      bar_sync<kBarProd, kProdThreads>();  // every producer is done with this round's lists
       gather_done_arrive(b);
       WS_T(1);
     }
@@ -551,10 +561,16 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
     blocks_per_sm = std::max(1, std::min({by_regs, by_smem, 4}));  // TMEM: 128 columns per CTA
     if (std::getenv("LUMI_MAX_CTAS"))
       blocks_per_sm = std::max(1, std::min(blocks_per_sm, std::atoi(std::getenv("LUMI_MAX_CTAS"))));
+    // only the shared memory the resident CTAs need; the rest of the 256 KB stays L1 data cache,
+    // which the irregular hash-grid gather depends on
+    const int carve = (int)std::ceil(100.0 * blocks_per_sm * (double)(smem + 1024) / smem_sm);
+    if ((e = cudaFuncSetAttribute(ws::k_render_ws, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  std::min(100, carve))) != cudaSuccess)
+      return e;
     if (std::getenv("LUMI_DEBUG"))
       std::fprintf(stderr, "[lumi] k_render_ws: %zu B smem (SM %d), %d regs, occupancy API %d, "
-                   "by regs %d, by smem %d -> %d CTAs/SM\n", smem, smem_sm, fa.numRegs, n, by_regs,
-                   by_smem, blocks_per_sm);
+                   "by regs %d, by smem %d -> %d CTAs/SM, carveout %d%%\n", smem, smem_sm, fa.numRegs,
+                   n, by_regs, by_smem, blocks_per_sm, std::min(100, carve));
   }
   p.tile_w = pk::kPW;
   p.tile_h = pk::kPH;
