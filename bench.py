@@ -327,7 +327,7 @@ def run_ours(args):
         for k in range(e2e_steps):
             drv.frame(args.warmup + k)
             if rank == 0:
-                host.copy_(drv.rgb, non_blocking=True)
+                host.copy_(drv.frame_buffer(args.warmup + k), non_blocking=True)
             torch.cuda.synchronize()
         dist.barrier()
         e2e_s = time.perf_counter() - t0
@@ -335,6 +335,9 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = rays_frame * e2e_steps / e2e_s / 1e6
+    if world > 1:
+        drv.close()
+        dist.barrier()  # rank 0's frame buffers outlive the peers' mappings
 
     if rank != 0:
         if world > 1:
@@ -382,7 +385,7 @@ def run_ours(args):
         "dtype": "f64 geometry / f32 field", "data": "synthetic (seeded init_random + reference-baked occupancy)",
         "config": {"workload": f"{args.config}: {cfg.description}", "eye_size": cfg.eye_size,
                    "eyes": 2, "table_size": spec.table_size, "rays_per_frame": rays_frame,
-                   "samples_per_ray": opts.samples_per_ray, "parallelism": f"rows{world}",
+                   "samples_per_ray": opts.samples_per_ray, "parallelism": f"rows{world}", "gather": drv.gather or "none",
                    "l2": ("inputs larger than L2 (hash table %.0f MB fp32, the kernel reads its %.0f MB "
                           "fp16 copy; L2 is 126 MB)" if field.grid_params.nbytes / 2 > 126e6
                           else "hash table %.0f MB fp32 / %.0f MB fp16 fits in L2 (no flush between frames)")

@@ -27,6 +27,11 @@
  *                                                            proj/src/trainer.cpp:228-235
  *   lumi_model_device_params, lumi_model_params_updated
  *                               in-place parameter access for a device-side optimizer
+ *   lumi_ipc_export, lumi_ipc_open, lumi_ipc_close
+ *                               the frame gather of run_frame (results gathered by row
+ *                               index into one shared Image, proj/src/scheduler.cpp:114-152)
+ *                               as peer memory: a rank maps rank 0's frame buffer and its
+ *                               render kernel stores its band there over NVLink
  *
  * All device work is sm_100a CUDA (paper_2311_02542_b200/csrc); there is no CPU
  * fallback -- without a usable B200 the calls fail with LUMI_ERR_CUDA.
@@ -290,6 +295,19 @@ int lumi_adam_step_async(float* params, const float* grads, float* mom, float* v
    fused density-L2/colour-L1 layer).  Synchronous. */
 int lumi_model_device_params(LumiModel* m, float** table, float** density, float** color);
 int lumi_model_params_updated(LumiModel* m);
+
+/* ---- peer-memory frame gather ------------------------------------------
+   lumi_ipc_export: an inter-process handle (LUMI_IPC_HANDLE_BYTES opaque bytes) for the
+   device allocation holding dev_ptr, plus dev_ptr's byte offset inside it.
+   lumi_ipc_open: maps a handle exported by another process into this process on `device`
+   (peer access enabled lazily); *dev_ptr = mapped base + offset, usable as the `rgb` /
+   `depth` / `opacity` planes of a LumiFrameTarget, so the render kernel writes straight into
+   the exporting GPU's memory.  lumi_ipc_close unmaps a pointer returned by lumi_ipc_open.
+   A process cannot open its own handle (LUMI_ERR_CUDA). */
+#define LUMI_IPC_HANDLE_BYTES 64
+int lumi_ipc_export(const void* dev_ptr, void* handle, uint64_t* offset);
+int lumi_ipc_open(int device, const void* handle, uint64_t offset, void** dev_ptr);
+int lumi_ipc_close(int device, void* dev_ptr);
 
 /* ---- row scheduler (host) ------------------------------------------------------- */
 int lumi_equal_assignment(int height, int workers, int32_t* rows, double* shares);

@@ -116,6 +116,9 @@ SIGNATURES = {
     "lumi_adam_step_async": ([_vp, _vp, _vp, _vp, _u64] + [_f] * 6 + [_vp], C.c_int),
     "lumi_model_device_params": ([_vp, _vp, _vp, _vp], C.c_int),
     "lumi_model_params_updated": ([_vp], C.c_int),
+    "lumi_ipc_export": ([_vp, _vp, _vp], C.c_int),
+    "lumi_ipc_open": ([_i, _vp, _u64, _vp], C.c_int),
+    "lumi_ipc_close": ([_i, _vp], C.c_int),
     "lumi_equal_assignment": ([_i, _i, _vp, _vp], C.c_int),
     "lumi_assign_rows": ([_i, _i, _vp, _vp, _d, _vp, _vp], C.c_int),
     "lumi_next_assignment": ([_i, _i, _vp, _vp, _vp, _i, _d, _vp, _vp], C.c_int),

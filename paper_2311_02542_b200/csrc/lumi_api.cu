@@ -1016,6 +1016,68 @@ static void round_rows(const double* shares, int n, int height, int32_t* rows) {
   }
 }
 
+// ---- peer-memory frame gather ----------------------------------------------------------
+// The reference's workers store their rows into one shared Image (scheduler.cpp:114-152); here
+// a rank maps rank 0's frame buffer and its render kernel stores its band there over NVLink.
+// The handle names the whole cudaMalloc allocation (a torch caching-allocator segment), so the
+// pointer's offset inside it travels alongside; the allocation base comes from the driver's
+// cuMemGetAddressRange, fetched through the runtime (no -lcuda link).
+static std::mutex g_ipc_mu;
+static std::map<void*, void*> g_ipc_maps;  // returned pointer -> mapped allocation base
+
+int lumi_ipc_export(const void* ptr, void* handle, uint64_t* offset) {
+  if (!ptr || !handle || !offset) return fail(LUMI_ERR_INVALID, "null argument");
+  using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static GetRange get_range = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &fn, 12000, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<GetRange>(fn);
+  }();
+  if (!get_range) return fail(LUMI_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  const auto p = reinterpret_cast<unsigned long long>(ptr);
+  if (get_range(&base, &size, p) != 0) return fail(LUMI_ERR_INVALID, "ipc export: not a device allocation");
+  cudaIpcMemHandle_t h;
+  LUMI_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(h) == LUMI_IPC_HANDLE_BYTES, "handle size");
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = p - base;
+  return LUMI_OK;
+}
+
+int lumi_ipc_open(int device, const void* handle, uint64_t offset, void** out) {
+  if (!handle || !out) return fail(LUMI_ERR_INVALID, "null argument");
+  DeviceGuard dg(device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  LUMI_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  void* p = static_cast<char*>(base) + offset;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  g_ipc_maps[p] = base;
+  *out = p;
+  return LUMI_OK;
+}
+
+int lumi_ipc_close(int device, void* ptr) {
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto it = g_ipc_maps.find(ptr);
+    if (it == g_ipc_maps.end()) return fail(LUMI_ERR_INVALID, "ipc close: pointer was not opened here");
+    base = it->second;
+    g_ipc_maps.erase(it);
+  }
+  DeviceGuard dg(device);
+  LUMI_CUDA_TRY(cudaIpcCloseMemHandle(base));
+  return LUMI_OK;
+}
+
 int lumi_equal_assignment(int height, int workers, int32_t* rows, double* shares) {
   if (workers < 1) return fail(LUMI_ERR_INVALID, "assignment: need at least one worker");
   if (height < workers) return fail(LUMI_ERR_INVALID, "assignment: more workers than rows");

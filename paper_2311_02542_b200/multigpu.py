@@ -1,8 +1,17 @@
 """Stereo eyebuffer frames across GPUs: one process per GPU (torch.distributed for the
 plumbing), rows of the stacked dual-eye image split by the paper's dynamic,
 throughput-proportional scheduler (proj/src/scheduler.cpp:68-87, 154-162; §5), and
-finished bands gathered to rank 0 over NVLink with NCCL point-to-point transfers (the bands
-are unequal, so an all-gather does not fit).
+the bands gathered to rank 0 over NVLink one of two ways:
+
+* ``gather="p2p"`` (default): rank 0's two frame buffers (frames alternate between them) are
+  mapped into every rank through CUDA IPC handles (`lumi_ipc_export` / `lumi_ipc_open`), and
+  each rank's render kernel stores its band's pixels straight into rank 0's memory as it
+  renders -- the gather IS the kernel's epilogue, there is no separate transfer.  The per-frame
+  exchange of band times (which every rank waits on after its own kernel finished) orders
+  those stores before rank 0 reads the frame; alternating buffers keep a fast rank's next
+  frame off the buffer rank 0 may still be copying out.
+* ``gather="nccl"``: finished bands are sent to rank 0 with batched NCCL point-to-point
+  transfers (the bands are unequal, so an all-gather does not fit).
 
 With world size 1 the same driver renders the whole frame on one GPU with no collective.
 """
@@ -75,27 +84,76 @@ class StereoFrameDriver:
     planar frame.  Each rank renders its scheduler band; rank 0 receives the others."""
 
     def __init__(self, torch, model: DeviceModel, eye_size: int, opts: RenderOptions,
-                 rank: int = 0, world: int = 1, dampening: float = 0.5, gather: bool = True,
+                 rank: int = 0, world: int = 1, dampening: float = 0.5, gather="p2p",
                  dist=None, counters: bool = False):
         self.torch, self.dm, self.S, self.opts = torch, model, int(eye_size), opts
-        self.rank, self.world, self.damp, self.gather, self.dist = rank, world, dampening, gather, dist
+        if gather is True:
+            gather = "p2p"
+        if gather not in (False, None, "p2p", "nccl"):
+            raise ValueError(f"gather must be 'p2p', 'nccl' or False, got {gather!r}")
+        self.rank, self.world, self.damp, self.dist = rank, world, dampening, dist
+        self.gather = gather if world > 1 else None
         self.H, self.W = 2 * self.S, self.S
         self.assign: WorkerAssignment = equal_assignment(self.H, world)
-        dev = torch.device("cuda", torch.cuda.current_device())
-        self.rgb = torch.zeros((3, self.H, self.W), dtype=torch.float32, device=dev)
+        self.dev = dev = torch.device("cuda", torch.cuda.current_device())
+        # frames alternate between two buffers; with the p2p gather rank 0's are the targets of
+        # every rank's kernel (ranks > 0 map them and keep no frame of their own)
+        nbuf = 2 if self.gather == "p2p" else 1
+        self.frames = [torch.zeros((3, self.H, self.W), dtype=torch.float32, device=dev)
+                       for _ in range(nbuf if rank == 0 or self.gather != "p2p" else 0)]
+        self._targets_ptr = [f.data_ptr() for f in self.frames]
+        self._peer = []
+        if self.gather == "p2p":
+            self._map_rank0_frames(dev.index)
+        self.rgb = self.frames[0] if self.frames else None
         self.stats = torch.zeros(4, dtype=torch.int64, device=dev) if counters else None
         self.ev0 = torch.cuda.Event(enable_timing=True)
         self.ev1 = torch.cuda.Event(enable_timing=True)
         self.launches = 0
         self.history: List[FrameStats] = []
 
+    def _map_rank0_frames(self, device: int) -> None:
+        import ctypes as C
+        L = _abi.lib()
+        handles = None
+        if self.rank == 0:
+            handles = []
+            for f in self.frames:
+                h = (C.c_uint8 * 64)()
+                off = C.c_uint64()
+                _abi.check(L.lumi_ipc_export(C.c_void_p(f.data_ptr()), h, C.byref(off)))
+                handles.append((bytes(h), off.value))
+        box = [handles]
+        self.dist.broadcast_object_list(box, src=0)
+        if self.rank != 0:
+            for h, off in box[0]:
+                p = C.c_void_p()
+                hb = (C.c_uint8 * 64).from_buffer_copy(h)
+                _abi.check(L.lumi_ipc_open(device, hb, C.c_uint64(off), C.byref(p)))
+                self._peer.append(p.value)
+            self._targets_ptr = list(self._peer)
+
+    def close(self) -> None:
+        """Unmaps rank 0's frames (p2p gather); rank 0 must keep its buffers alive until every
+        rank has closed, so callers end with a barrier."""
+        if self._peer:
+            self.torch.cuda.synchronize()
+            for p in self._peer:
+                _abi.check(_abi.lib().lumi_ipc_close(self.torch.cuda.current_device(), p))
+            self._peer = []
+            self._targets_ptr = []
+
+    def frame_buffer(self, frame: int):
+        """Rank 0's [3, H, W] buffer holding `frame` (None on ranks > 0 with the p2p gather)."""
+        return self.frames[frame % len(self.frames)] if self.frames else None
+
     def cameras(self, frame: int) -> List[CameraModel]:
         rot, origin = scenes.head_pose(frame)
         return [CameraModel.from_spec(c) for c in scenes.eye_cameras(self.S, rot, origin)]
 
-    def _target(self, eye: int) -> _abi.FrameTarget:
+    def _target(self, eye: int, frame: int) -> _abi.FrameTarget:
         t = _abi.FrameTarget()
-        t.rgb = self.rgb.data_ptr()
+        t.rgb = self._targets_ptr[frame % len(self._targets_ptr)]
         t.work_stats = self.stats.data_ptr() if self.stats is not None else None
         t.width, t.height, t.row_offset = self.W, self.H, eye * self.S
         return t
@@ -105,21 +163,24 @@ class StereoFrameDriver:
         stream = self.torch.cuda.current_stream().cuda_stream
         band = self.assign.ranges[self.rank]
         cams = self.cameras(frame)
+        if self.frames:
+            self.rgb = self.frame_buffer(frame)
         self.ev0.record()
         for eye, b, e in eye_bands(band.begin, band.end, self.S):
-            self.dm.render_rows_async(cams[eye], self.opts, b, e, self._target(eye), stream)
+            self.dm.render_rows_async(cams[eye], self.opts, b, e, self._target(eye, frame), stream)
             self.launches += 1 if self.dm.kernel == "simt" else 2  # march pass + render
         self.ev1.record()
 
     def gather_bands(self) -> None:
-        if self.gather:
+        if self.gather == "nccl":
             gather_bands(self.dist, self.rgb, self.assign, self.rank, self.world)
 
     def rebalance(self) -> FrameStats:
         """Per-rank render time of the frame just finished -> next assignment."""
         self.ev1.synchronize()
+        dev = "cpu" if self.world > 1 and self.dist.get_backend() == "gloo" else self.dev
         ms = exchange_ms(self.torch, self.dist, float(self.ev0.elapsed_time(self.ev1)),
-                         self.world, self.rgb.device)
+                         self.world, dev)
         st, self.assign = rebalance(self.assign, ms, self.W, self.damp)
         self.history.append(st)
         return st
