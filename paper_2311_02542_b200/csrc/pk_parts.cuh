@@ -130,20 +130,28 @@ __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane)
 
 // One hash-grid level of one sample from the fp16 table (grid.h:96-113, 144-167): fp32 grid
 // coordinates, 32-bit entry indices off the level's base address, fp16 trilinear weights
-// (HMUL2) accumulated in fp32 by FHFMA in two interleaved chains per feature.
-__device__ __forceinline__ float2 gather_level(uint4 L, float u, float v, float s, float wl) {
+// (HMUL2) accumulated in fp32 by FHFMA in two interleaved chains per feature.  Split in three
+// so a thread can put the corner loads of several pairs in flight before it consumes any:
+// gather_prep (cell, corner indices, fractions), the 8 loads, gather_combine.
+struct GatherPrep {
+  const __half2* base;  // the level's first entry
+  uint32_t idx[8];
+  float fu, fv, fs;
+};
+
+__device__ __forceinline__ void gather_prep(uint4 L, float u, float v, float s, GatherPrep& g) {
   const int res = (int)L.x;
   const float r = (float)res;
-  const __half2* __restrict__ base =
-      reinterpret_cast<const __half2*>(((unsigned long long)L.w << 32) | L.z);  // level's first pair
+  g.base = reinterpret_cast<const __half2*>(((unsigned long long)L.w << 32) | L.z);
   const float pu = u * r, pv = v * r, ps = s * r;
   const int iu = min((int)pu, res - 1), iv = min((int)pv, res - 1), is = min((int)ps, res - 1);
-  uint32_t idx[8];
-  corner_indices(L.y == 0u, iu, iv, is, (uint32_t)res + 1u, L.y, idx);
-  __half2 e[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) e[k] = __ldg(base + idx[k]);  // one IMAD.WIDE per corner
-  const float fu = pu - (float)iu, fv = pv - (float)iv, fs = ps - (float)is;
+  corner_indices(L.y == 0u, iu, iv, is, (uint32_t)res + 1u, L.y, g.idx);
+  g.fu = pu - (float)iu;
+  g.fv = pv - (float)iv;
+  g.fs = ps - (float)is;
+}
+
+__device__ __forceinline__ float2 gather_combine(const __half2* e, float fu, float fv, float fs, float wl) {
   const __half2 hu = __floats2half2_rn(1.f - fu, fu);
   const __half2 w0 = __hmul2(hu, __float2half2_rn(1.f - fv));
   const __half2 w1 = __hmul2(hu, __float2half2_rn(fv));
@@ -157,6 +165,15 @@ __device__ __forceinline__ float2 gather_level(uint4 L, float u, float v, float 
     b[k & 1] = fma_f32_f16(tri, __high2half(e[k]), b[k & 1]);
   }
   return make_float2((a[0] + a[1]) * wl, (b[0] + b[1]) * wl);
+}
+
+__device__ __forceinline__ float2 gather_level(uint4 L, float u, float v, float s, float wl) {
+  GatherPrep g;
+  gather_prep(L, u, v, s, g);
+  __half2 e[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) e[k] = __ldg(g.base + g.idx[k]);  // one IMAD.WIDE per corner
+  return gather_combine(e, g.fu, g.fv, g.fs, wl);
 }
 
 // trunc_exp / sigmoid (network.h:41-57) with the MUFU exp2 / reciprocal: ~2 ulp, far below the

@@ -267,6 +267,9 @@ __global__ void __launch_bounds__(128) k_march_mask(RenderParams p) {
 
 // Filtered march pass: the same kept bitmask, decided in fp32 with a certified error bound
 // (occupied_filtered, render_common.cuh) and the exact double test only where fp32 cannot decide.
+#ifndef LUMI_MARCH_EXIT
+#define LUMI_MARCH_EXIT 1
+#endif
 __global__ void __launch_bounds__(128) k_march_mask_fast(RenderParams p) {
   __shared__ double s_ts[kMaxSamples];
   __shared__ float s_tf[kMaxSamples];
@@ -292,6 +295,18 @@ __global__ void __launch_bounds__(128) k_march_mask_fast(RenderParams p) {
   const float3 df = make_float3((float)d.x, (float)d.y, (float)d.z);
   const float onorm = fabsf(of.x) + fabsf(of.y) + fabsf(of.z);
   const InsideMarch im = inside_march_setup(p, of, df);
+#if LUMI_MARCH_EXIT
+  // beyond the ray's exit from the unit cube (slab test in fp32, 1e-3 slack) the inside fast
+  // path can only answer "undecided": go straight to the general test there
+  float t_exit = 3.4e38f;
+  {
+    const float dd[3] = {df.x, df.y, df.z}, oo[3] = {of.x, of.y, of.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (dd[a] != 0.f) t_exit = fminf(t_exit, ((dd[a] > 0.f ? 1.f : -1.f) - oo[a]) / dd[a]);
+    t_exit = t_exit * 1.001f + 1e-3f;
+  }
+#endif
   int count = 0;
   for (int w0 = 0; w0 < p.mask_words; ++w0) {
     uint32_t bits = 0, unsure = 0;
@@ -300,7 +315,11 @@ __global__ void __launch_bounds__(128) k_march_mask_fast(RenderParams p) {
 #pragma unroll 4
       for (int b = 0; b < hi; ++b) {
         const float tf = s_tf[w0 * 32 + b];
+#if LUMI_MARCH_EXIT
+        int r = tf < t_exit ? occupied_inside(p, im, tf) : -1;
+#else
         int r = occupied_inside(p, im, tf);  // -1: not certified inside the unit cube
+#endif
         if (r < 0) r = occupied_filtered(p, of, df, onorm, tf);
         bits |= (uint32_t)(r & 1) << b;
         unsure |= (uint32_t)(r >> 1) << b;

@@ -38,6 +38,9 @@ namespace ws {
 
 using namespace pk;
 
+#ifndef WS_GATHER_BATCH
+#define WS_GATHER_BATCH 1
+#endif
 #ifndef WS_PROD_WARPS
 #define WS_PROD_WARPS 4
 #endif
@@ -46,7 +49,7 @@ constexpr int kProdThreads = 32 * kProdWarps;
 constexpr int kCtaThreads = 128 + kProdThreads;        // consumers [0, 128), producers after
 constexpr int kCtasPerSm = kProdWarps == 4 ? 3 : 2;    // (registers: <= 85 per thread)
 #ifndef WS_PROD_PAIRS
-#define WS_PROD_PAIRS 2
+#define WS_PROD_PAIRS 3
 #endif
 constexpr int kProdPairs = WS_PROD_PAIRS;  // pairs per producer thread per gather step
 // named barriers: 0 = __syncthreads (setup / teardown), LIST_READY 1 + b, GATHER_DONE 3 + b,
@@ -218,6 +221,28 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           const int pi = base + kProdThreads * q + ctid;
           code[q] = pi < total ? (uint32_t)s.pairs[pi] : 0xffffu;
         }
+#if WS_GATHER_BATCH
+        // branch-free over the pairs (a missing pair re-gathers pair 0 of the round and is not
+        // stored), so all kProdPairs x 8 corner loads are in flight before the first FHFMA
+        GatherPrep gp[kProdPairs];
+        float wl[kProdPairs];
+#pragma unroll
+        for (int q = 0; q < kProdPairs; ++q) {
+          const uint32_t c = code[q] != 0xffffu ? code[q] : (uint32_t)s.pairs[0];
+          // code = the feature's byte offset in A; row * 16 in samp
+          const float4 P = *reinterpret_cast<const float4*>(Pb + (c & 0x7F0u));
+          const int lv = pair_level(c);
+          wl[q] = __saturatef(P.w - (float)lv);
+          gather_prep(s.lvl[lv], P.x, P.y, P.z, gp[q]);
+        }
+        __half2 e[kProdPairs][8];
+#pragma unroll
+        for (int q = 0; q < kProdPairs; ++q)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) e[q][k] = __ldg(gp[q].base + gp[q].idx[k]);
+#pragma unroll
+        for (int q = 0; q < kProdPairs; ++q) f[q] = gather_combine(e[q], gp[q].fu, gp[q].fv, gp[q].fs, wl[q]);
+#else
 #pragma unroll
         for (int q = 0; q < kProdPairs; ++q) {
           f[q] = make_float2(0.f, 0.f);
@@ -228,6 +253,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
             f[q] = gather_level(s.lvl[lv], P.x, P.y, P.z, wl);
           }
         }
+#endif
 #pragma unroll
         for (int q = 0; q < kProdPairs; ++q)
           if (code[q] != 0xffffu)
