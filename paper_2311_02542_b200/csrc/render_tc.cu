@@ -267,6 +267,10 @@ __global__ void __launch_bounds__(128) k_march_mask(RenderParams p) {
 
 // Filtered march pass: the same kept bitmask, decided in fp32 with a certified error bound
 // (occupied_filtered, render_common.cuh) and the exact double test only where fp32 cannot decide.
+#ifndef LUMI_MARCH_UNROLL
+#define LUMI_MARCH_UNROLL 8
+#endif
+constexpr int kMarchUnroll = LUMI_MARCH_UNROLL;
 #ifndef LUMI_MARCH_EXIT
 #define LUMI_MARCH_EXIT 1
 #endif
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(128) k_march_mask_fast(RenderParams p) {
     uint32_t bits = 0, unsure = 0;
     if (valid) {
       const int hi = min(32, p.n - w0 * 32);
-#pragma unroll 4
+#pragma unroll kMarchUnroll
       for (int b = 0; b < hi; ++b) {
         const float tf = s_tf[w0 * 32 + b];
 #if LUMI_MARCH_EXIT
