@@ -38,9 +38,6 @@ namespace ws {
 
 using namespace pk;
 
-#ifndef WS_GATHER_BATCH
-#define WS_GATHER_BATCH 1
-#endif
 #ifndef WS_PROD_WARPS
 #define WS_PROD_WARPS 4
 #endif
@@ -214,24 +211,23 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       const uint8_t* Pb = reinterpret_cast<const uint8_t*>(s.samp[b]);
 #pragma unroll 1
       for (int base = 0; base < total; base += kProdThreads * kProdPairs) {
+        // branch-free over the pairs (past the end of the list a lane re-gathers the last pair
+        // and does not store it), so all kProdPairs x 8 corner loads are in flight before the
+        // first FHFMA; code = the feature's byte offset in A, row * 16 in samp
         uint32_t code[kProdPairs];
-        float2 f[kProdPairs];
+        bool ok[kProdPairs];
 #pragma unroll
         for (int q = 0; q < kProdPairs; ++q) {
           const int pi = base + kProdThreads * q + ctid;
-          code[q] = pi < total ? (uint32_t)s.pairs[pi] : 0xffffu;
+          ok[q] = pi < total;
+          code[q] = s.pairs[ok[q] ? pi : total - 1];
         }
-#if WS_GATHER_BATCH
-        // branch-free over the pairs (a missing pair re-gathers pair 0 of the round and is not
-        // stored), so all kProdPairs x 8 corner loads are in flight before the first FHFMA
         GatherPrep gp[kProdPairs];
         float wl[kProdPairs];
 #pragma unroll
         for (int q = 0; q < kProdPairs; ++q) {
-          const uint32_t c = code[q] != 0xffffu ? code[q] : (uint32_t)s.pairs[0];
-          // code = the feature's byte offset in A; row * 16 in samp
-          const float4 P = *reinterpret_cast<const float4*>(Pb + (c & 0x7F0u));
-          const int lv = pair_level(c);
+          const float4 P = *reinterpret_cast<const float4*>(Pb + (code[q] & 0x7F0u));
+          const int lv = pair_level(code[q]);
           wl[q] = __saturatef(P.w - (float)lv);
           gather_prep(s.lvl[lv], P.x, P.y, P.z, gp[q]);
         }
@@ -241,23 +237,10 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
 #pragma unroll
           for (int k = 0; k < 8; ++k) e[q][k] = __ldg(gp[q].base + gp[q].idx[k]);
 #pragma unroll
-        for (int q = 0; q < kProdPairs; ++q) f[q] = gather_combine(e[q], gp[q].fu, gp[q].fv, gp[q].fs, wl[q]);
-#else
-#pragma unroll
         for (int q = 0; q < kProdPairs; ++q) {
-          f[q] = make_float2(0.f, 0.f);
-          if (code[q] != 0xffffu) {  // code = the feature's byte offset in A; row * 16 in samp
-            const float4 P = *reinterpret_cast<const float4*>(Pb + (code[q] & 0x7F0u));
-            const int lv = pair_level(code[q]);
-            const float wl = __saturatef(P.w - (float)lv);
-            f[q] = gather_level(s.lvl[lv], P.x, P.y, P.z, wl);
-          }
+          const float2 f = gather_combine(e[q], gp[q].fu, gp[q].fv, gp[q].fs, wl[q]);
+          if (ok[q]) *reinterpret_cast<__half2*>(s.A[b] + code[q]) = __floats2half2_rn(f.x, f.y);
         }
-#endif
-#pragma unroll
-        for (int q = 0; q < kProdPairs; ++q)
-          if (code[q] != 0xffffu)
-            *reinterpret_cast<__half2*>(s.A[b] + code[q]) = __floats2half2_rn(f[q].x, f[q].y);
       }
       ptx::fence_async_smem();
       bar_sync<kBarProd, kProdThreads>();  // every producer is done with this round's lists
