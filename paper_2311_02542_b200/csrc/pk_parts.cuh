@@ -133,6 +133,9 @@ __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane)
 // (HMUL2) accumulated in fp32 by FHFMA in two interleaved chains per feature.  Split in three
 // so a thread can put the corner loads of several pairs in flight before it consumes any:
 // gather_prep (cell, corner indices, fractions), the 8 loads, gather_combine.
+#ifndef LUMI_GATHER_HACC
+#define LUMI_GATHER_HACC 1
+#endif
 struct GatherPrep {
   const __half2* base;  // the level's first entry
   uint32_t idx[8];
@@ -157,6 +160,17 @@ __device__ __forceinline__ float2 gather_combine(const __half2* e, float fu, flo
   const __half2 w1 = __hmul2(hu, __float2half2_rn(fv));
   const __half2 gs2 = __float2half2_rn(1.f - fs), fs2 = __float2half2_rn(fs);
   const __half2 t[4] = {__hmul2(w0, gs2), __hmul2(w1, gs2), __hmul2(w0, fs2), __hmul2(w1, fs2)};
+#if LUMI_GATHER_HACC
+  // both features at once in packed fp16 (HFMA2), two chains, one widening add at the end
+  __half2 c[2];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const __half2 tri = (k & 1) ? __high2half2(t[k >> 1]) : __low2half2(t[k >> 1]);
+    c[k & 1] = k < 2 ? __hmul2(e[k], tri) : __hfma2(e[k], tri, c[k & 1]);
+  }
+  const float2 x = __half22float2(c[0]), y = __half22float2(c[1]);
+  return make_float2((x.x + y.x) * wl, (x.y + y.y) * wl);
+#else
   float a[2] = {0.f, 0.f}, b[2] = {0.f, 0.f};
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -165,6 +179,7 @@ __device__ __forceinline__ float2 gather_combine(const __half2* e, float fu, flo
     b[k & 1] = fma_f32_f16(tri, __high2half(e[k]), b[k & 1]);
   }
   return make_float2((a[0] + a[1]) * wl, (b[0] + b[1]) * wl);
+#endif
 }
 
 __device__ __forceinline__ float2 gather_level(uint4 L, float u, float v, float s, float wl) {
