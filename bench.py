@@ -252,9 +252,18 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # LUMI_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0 over gloo, so the N>1 path
+    # (scheduler bands, peer-memory gather through CUDA IPC, rebalancing) runs on a one-GPU box
+    shared = os.environ.get("LUMI_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
+    red_dev = "cpu" if shared else "cuda"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = scenes.CONFIGS[args.config]
     spec = cfg.model
     field, grid = load_scene(spec)
@@ -289,14 +298,14 @@ def run_ours(args):
     march_ms, render_ms, render_launches = dm.take_timing()
     elapsed = float(t_start.elapsed_time(t_end))
     if world > 1:
-        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        t = torch.tensor([elapsed], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
     counters = drv.counters()
     launches = drv.launches
     if world > 1:
         t = torch.tensor([float(x) for x in counters] + [float(launches), kernel_ms],
-                         dtype=torch.float64, device="cuda")
+                         dtype=torch.float64, device=red_dev)
         dist.all_reduce(t)
         counters = t[:4].cpu().numpy()
         launches = int(t[4].item())
@@ -331,7 +340,7 @@ def run_ours(args):
             torch.cuda.synchronize()
         dist.barrier()
         e2e_s = time.perf_counter() - t0
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = rays_frame * e2e_steps / e2e_s / 1e6
@@ -386,6 +395,7 @@ def run_ours(args):
         "config": {"workload": f"{args.config}: {cfg.description}", "eye_size": cfg.eye_size,
                    "eyes": 2, "table_size": spec.table_size, "rays_per_frame": rays_frame,
                    "samples_per_ray": opts.samples_per_ray, "parallelism": f"rows{world}", "gather": drv.gather or "none",
+                   **({"shared_gpu_test": True} if shared else {}),
                    "l2": ("inputs larger than L2 (hash table %.0f MB fp32, the kernel reads its %.0f MB "
                           "fp16 copy; L2 is 126 MB)" if field.grid_params.nbytes / 2 > 126e6
                           else "hash table %.0f MB fp32 / %.0f MB fp16 fits in L2 (no flush between frames)")
