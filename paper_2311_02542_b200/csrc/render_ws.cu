@@ -44,7 +44,19 @@ using namespace pk;
 constexpr int kProdWarps = WS_PROD_WARPS;              // producer warps (4 or 8)
 constexpr int kProdThreads = 32 * kProdWarps;
 constexpr int kCtaThreads = 128 + kProdThreads;        // consumers [0, 128), producers after
-constexpr int kCtasPerSm = kProdWarps == 4 ? 3 : 2;    // (registers: <= 85 per thread)
+// WS_REGSPLIT: 8 producer warps at 3 CTAs/SM (56 registers per thread at launch); the
+// warpgroups then trade registers with setmaxnreg: consumers up to WS_CONS_REGS, producers
+// down to WS_PROD_REGS (128 * C + 256 * P <= 384 * 56)
+#ifndef WS_REGSPLIT
+#define WS_REGSPLIT 0
+#endif
+#ifndef WS_CONS_REGS
+#define WS_CONS_REGS 80
+#endif
+#ifndef WS_PROD_REGS
+#define WS_PROD_REGS 40
+#endif
+constexpr int kCtasPerSm = (kProdWarps == 4 || WS_REGSPLIT) ? 3 : 2;  // (registers: <= 85 per thread)
 #ifndef WS_PROD_PAIRS
 #define WS_PROD_PAIRS 3
 #endif
@@ -169,6 +181,14 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = s.tmem_base;
+#if WS_REGSPLIT
+  static_assert(128 * WS_CONS_REGS + kProdThreads * WS_PROD_REGS <= kCtaThreads * (65536 / (kCtaThreads * kCtasPerSm) / 8 * 8),
+                "register split exceeds the launch allocation");
+  if (wg == 1)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(WS_PROD_REGS));
+  else
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WS_CONS_REGS));
+#endif
 #ifdef LUMI_PHASE_TIMING
   long long t_last = clock64();
 #endif
