@@ -184,10 +184,18 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
 #if WS_REGSPLIT
   static_assert(128 * WS_CONS_REGS + kProdThreads * WS_PROD_REGS <= kCtaThreads * (65536 / (kCtaThreads * kCtasPerSm) / 8 * 8),
                 "register split exceeds the launch allocation");
-  if (wg == 1)
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(WS_PROD_REGS));
-  else
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WS_CONS_REGS));
+  // the warpgroup giving registers up decreases first, the other one increases
+  if ((wg == 1) == (WS_PROD_REGS < WS_CONS_REGS)) {
+    if (wg == 1)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(WS_PROD_REGS));
+    else
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(WS_CONS_REGS));
+  } else {
+    if (wg == 1)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WS_PROD_REGS));
+    else
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WS_CONS_REGS));
+  }
 #endif
 #ifdef LUMI_PHASE_TIMING
   long long t_last = clock64();
