@@ -246,6 +246,7 @@ def run_ours(args):
     import paper_2311_02542_b200 as L
     from paper_2311_02542_b200 import _abi, scenes
     from paper_2311_02542_b200.multigpu import StereoFrameDriver
+    from paper_2311_02542_b200.scheduler import aggregate_stats
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -287,8 +288,10 @@ def run_ours(args):
     t_end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         t_start.record()
+        frames = []
         for k in range(args.steps):
             st = drv.frame(args.warmup + k)
+            frames.append(st)
             kernel_ms += st.worker_ms[rank]
         t_end.record()
         torch.cuda.synchronize()
@@ -311,6 +314,7 @@ def run_ours(args):
         launches = int(t[4].item())
     sec = elapsed / 1000.0
     value = rays_frame * args.steps / sec / 1e6
+    fstats = aggregate_stats(frames)
     fps = args.steps / sec
 
     # ---- end to end through the public API with host buffers -------------------------
@@ -402,6 +406,9 @@ def run_ours(args):
                          % (field.grid_params.nbytes / 1e6, field.grid_params.nbytes / 2e6),
                    "kernel": kname},
         "fps": round(fps, 3),
+        # FrameStats of the timed frames (frame time = the slowest band's device ms, as
+        # run_frame's wall time is the slowest worker's) through the native aggregate_stats
+        "frame_stats": {k: round(getattr(fstats, k), 3) for k in ("mean_fps", "std_fps", "p99_fps")},
         "render_ms_per_step": round(kernel_ms / args.steps, 3),  # rank-0 march+render span
         "kernels": {"march_ms_per_launch": round(march_ms / max(render_launches, 1), 3),
                     f"{kname}_ms_per_launch": round(render_ms / max(render_launches, 1), 3),
