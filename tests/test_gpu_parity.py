@@ -450,3 +450,29 @@ def test_empty_grid_renders_background(lumi, torch_cuda, small, kernel):
         assert (out[c] == np.float32(bg[c])).all()
     assert not depth.any() and not opac.any()
     assert sum(s.evals for s in stats) == 0
+
+
+def test_render_c3_full_model_vs_oracle(lumi, torch_cuda, oracle):
+    """Config C3's model (T=2^22: level 0 dense, levels 1-15 hashed, reference-baked occupancy)
+    on a 2048^2 eye of the head path: the production kernel renders the whole eye, the oracle
+    a band of rows through the centre and every 256th row."""
+    s = scenes.FULL
+    cfg = O.field_config(s.levels, s.features_per_level, s.base_resolution, s.per_level_scale,
+                         s.table_size, s.hidden_width, s.bottleneck, 0)
+    params = oracle.synth_params(cfg, s.seed, s.amplitude)
+    bits, res, _ = load_occ(s.name)
+    om = oracle.model(params, bits, res)
+    _, _, dm = product_model(lumi, s, bits, res)
+    rot, org = scenes.head_pose(23)
+    spec = scenes.eye_cameras(2048, rot, org)[1]
+    cam = lumi.CameraModel.from_spec(spec)
+    out, _, opac, stats = _render(lumi, dm, cam, lumi.RenderOptions())
+    rows = list(range(1016, 1024)) + list(range(0, 2048, 256))
+    errs = []
+    for y in rows:
+        ref = oracle.render_rows(om, ocam(spec), O.render_options(), y, y + 1)
+        errs.append(np.abs(out[:, y] - ref["out"][:, y]).max())
+        assert np.abs(opac[y] - ref["opacity"][y]).max() <= PIX_TOL, y
+    print(f"C3 sampled rows max|dPQ|={max(errs):.3e}")
+    assert max(errs) <= PIX_TOL
+    assert sum(st.evals for st in stats) > 0
