@@ -38,6 +38,9 @@ namespace ws {
 
 using namespace pk;
 
+#ifndef WS_SHARED_ONES
+#define WS_SHARED_ONES 1
+#endif
 #ifndef WS_PROD_WARPS
 #define WS_PROD_WARPS 4
 #endif
@@ -86,7 +89,14 @@ __device__ unsigned long long g_ws_cycles[6];
 #endif
 
 struct __align__(16) Smem {
+#if WS_SHARED_ONES
+  // double-buffered layer-1 A tiles, features only (chunk-major, a_off); the bias step's
+  // [1 0 ... 0] block is one shared pair of core matrices read with SBO = 0 by every row group
+  uint8_t A[2][128 * 32 * 2];
+  uint8_t ones[2 * 128];
+#else
   uint8_t A[2][128 * (32 + kKb) * 2];  // double-buffered layer-1 A tiles (chunk-major, a_off)
+#endif
   uint8_t W1[64 * (32 + kKb) * 2];
   uint8_t F[80 * (80 + kKb) * 2];
   uint8_t C2[64 * (64 + kKb) * 2];
@@ -106,6 +116,20 @@ struct __align__(16) Smem {
   uint16_t pairs[kWarps * 32 * kMaxLevels];  // the round's gather list, warp lists concatenated
   int cnt[2][kWarps];                        // per warp: pairs the producers will list
 };
+
+// layer 1 with the bias step's A from the shared ones block (LBO 128 B between its two core
+// matrices, SBO 0: every 8-row group reads the same [1 0 ... 0] rows)
+__device__ __forceinline__ void issue_layer1_shared_ones(const uint8_t* A, const uint8_t* ones,
+                                                         const uint8_t* B, uint32_t d_tmem) {
+  constexpr uint32_t idesc = ptx::idesc_f16_f32<128, 64>();
+  constexpr uint32_t sbo = ((32 + kKb) / 8) * 128;
+  const uint32_t a = ptx::smem_addr(A), o = ptx::smem_addr(ones), b = ptx::smem_addr(B);
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk)
+    ptx::mma_f16(d_tmem, ptx::make_smem_desc(a + kk * 2 * kALbo, kALbo, 128),
+                 ptx::make_smem_desc(b + kk * 256, 128, sbo), idesc, kk > 0 ? 1u : 0u);
+  ptx::mma_f16(d_tmem, ptx::make_smem_desc(o, 128, 0), ptx::make_smem_desc(b + 2 * 256, 128, sbo), idesc, 1u);
+}
 
 // named barriers with immediate ids, so ptxas reserves only the barriers used (a register id
 // would reserve all 16, which caps residency at one CTA per SM)
@@ -158,11 +182,15 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
   load_weight_tile(s.F, p.mlp.fused, kHidden + 1, 80, 80);
   load_weight_tile(s.C2, c2, 64, 64, 64);
   load_weight_tile(s.C3, c3, 3, 16, 64);
+#if WS_SHARED_ONES
+  if (tid < 16) st16(s.ones, (uint32_t)tid * 16u, make_uint4(tid < 8 ? 0x3C00u : 0u, 0u, 0u, 0u));
+#else
   // constant ones block of both A buffers (never overwritten)
   if (ctid < 128) {
     st16(s.A[wg], a_off(ctid, 4), make_uint4(0x3C00u, 0u, 0u, 0u));
     st16(s.A[wg], a_off(ctid, 5), make_uint4(0u, 0u, 0u, 0u));
   }
+#endif
   for (int l = tid; l < kMaxLevels; l += kCtaThreads) {
     const int res = l < p.grid.levels ? p.grid.res[l] : 1;
     const bool dense = (p.grid.dense_mask >> l) & 1u;
@@ -453,7 +481,11 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         float v32[32];
         if (issuer) {
           ptx::tc_fence_after();
+#if WS_SHARED_ONES
+          issue_layer1_shared_ones(s.A[bp], s.ones, s.W1, tmem);
+#else
           issue_layer<64, 32>(s.A[bp], s.W1, tmem);
+#endif
           ptx::mma_commit(&s.mbar);
         }
         ptx::mbar_wait(&s.mbar, phase);
