@@ -41,6 +41,9 @@ using namespace pk;
 #ifndef WS_SHARED_ONES
 #define WS_SHARED_ONES 1
 #endif
+#ifndef WS_PREFETCH
+#define WS_PREFETCH 1
+#endif
 #ifndef WS_PROD_WARPS
 #define WS_PROD_WARPS 4
 #endif
@@ -329,6 +332,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
     bool packet_live = false, no_more = false, pending = false;
     int last_round = -1;  // the last round holding rows of the pending packet
     int word = 0, g_next = 0, word_total = 0;
+#if WS_PREFETCH
+    // one packet id and one mask word ahead: the atomic and the word load are off the fill's
+    // dependency chain
+    long long next_pkt = 0;
+    if (lane == 0) next_pkt = (long long)atomicAdd(p.work_counter, 1u);
+    uint32_t next_bits = 0;
+#endif
     uint32_t phase = 0;
 
 #pragma unroll 1
@@ -339,7 +349,14 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       while (take < 32 && !no_more && !pending) {
         if (!packet_live) {
           long long pkt = 0;
+#if WS_PREFETCH
+          if (lane == 0) {
+            pkt = next_pkt;
+            next_pkt = (long long)atomicAdd(p.work_counter, 1u);
+          }
+#else
           if (lane == 0) pkt = (long long)atomicAdd(p.work_counter, 1u);
+#endif
           pkt = __shfl_sync(FULL, pkt, 0);
           if (pkt >= total_packets) {
             no_more = true;
@@ -367,6 +384,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           packet_live = true;
           word = -1;
           g_next = word_total = 0;
+#if WS_PREFETCH
+          next_bits = r.valid ? __ldg(p.kept_mask + r.id) : 0u;
+#endif
         }
         if (g_next < word_total) {
           const int n = min(32 - take, word_total - g_next);
@@ -390,7 +410,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           break;
         }
         ++word;
+#if WS_PREFETCH
+        const uint32_t bits = r.alive ? next_bits : 0u;
+        if (word + 1 < p.mask_words && r.alive)
+          next_bits = __ldg(p.kept_mask + (size_t)(word + 1) * p.total_rays + r.id);
+#else
         const uint32_t bits = r.alive ? __ldg(p.kept_mask + (size_t)word * p.total_rays + r.id) : 0u;
+#endif
         int run = 0;
         for (int i = 0; i < 32; ++i) {
           const uint32_t bb = __ballot_sync(FULL, (bits >> i) & 1u);
