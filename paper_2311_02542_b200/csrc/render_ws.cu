@@ -78,7 +78,7 @@ constexpr int kConsLevels = WS_CONS_LEVELS;  // LOD levels gathered by the consu
 #ifdef LUMI_PHASE_TIMING
 // warp-cycles: producers [wait list, gather], consumers [fill+geometry+list, wait gather, MLP,
 // composite]
-__device__ unsigned long long g_ws_cycles[6];
+__device__ unsigned long long g_ws_cycles[8];
 #define WS_T(k)                                                    \
   do {                                                             \
     const long long _t = clock64();                                \
@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         g_next = 0;
         word_total = run;
       }
+      WS_T(6);
       const bool have = lane < take;
       {
         s.own[b][warp][lane] = 0u;
@@ -490,6 +491,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         if (lane == 0) s.cnt[b][warp] = wsum;
       }
       ptx::fence_async_smem();
+      WS_T(7);
       // all consumer warps finished (every packet stored) -> the producers stop after round j
       const bool stop = bar_and<kBarCons, 128>(no_more && !packet_live);
       if (ctid == 0) s.stop[b] = stop ? 1 : 0;
@@ -686,19 +688,20 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
   if (ev) cudaEventRecord(ev[1], s);
   const long long grid = std::min<long long>((long long)blocks_per_sm * num_sms, (packets + 3) / 4);
 #ifdef LUMI_PHASE_TIMING
-  unsigned long long z6[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long z6[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpyToSymbolAsync(ws::g_ws_cycles, z6, sizeof(z6), 0, cudaMemcpyHostToDevice, s);
 #endif
   ws::k_render_ws<<<(unsigned)grid, ws::kCtaThreads, smem, s>>>(p);
 #ifdef LUMI_PHASE_TIMING
   {
-    unsigned long long c[6];
+    unsigned long long c[8];
     cudaMemcpyFromSymbolAsync(c, ws::g_ws_cycles, sizeof(c), 0, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    const double tp = (double)(c[0] + c[1]), tc = (double)(c[2] + c[3] + c[4] + c[5]);
-    std::fprintf(stderr, "[lumi] ws producers: wait list %.1f%% gather %.1f%% | consumers: fill %.1f%% "
-                 "wait gather %.1f%% mlp %.1f%% composite %.1f%%\n", 100 * c[0] / tp, 100 * c[1] / tp,
-                 100 * c[2] / tc, 100 * c[3] / tc, 100 * c[4] / tc, 100 * c[5] / tc);
+    const double tp = (double)(c[0] + c[1]), tc = (double)(c[2] + c[3] + c[4] + c[5] + c[6] + c[7]);
+    std::fprintf(stderr, "[lumi] ws producers: wait list %.1f%% gather %.1f%% | consumers: stream fill %.1f%% "
+                 "geometry %.1f%% fill barrier %.1f%% wait gather %.1f%% mlp %.1f%% composite %.1f%%\n",
+                 100 * c[0] / tp, 100 * c[1] / tp, 100 * c[6] / tc, 100 * c[7] / tc, 100 * c[2] / tc,
+                 100 * c[3] / tc, 100 * c[4] / tc, 100 * c[5] / tc);
   }
 #endif
   if (ev) cudaEventRecord(ev[2], s);
