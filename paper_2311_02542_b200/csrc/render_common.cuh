@@ -43,6 +43,10 @@ struct RenderParams {
   // kept_mask[word * total_rays + id], kept_count[id]
   uint32_t* kept_mask;
   uint16_t* kept_count;
+  // optional, written by the march pass for the packet renderer: fp32 direction of each ray id
+  // and of its right neighbour (x + 1.5), SoA [6][total_rays], so a warp starting a packet
+  // loads its rays instead of running the double-precision ray generation on its critical path
+  float* ray_dirs;
   int mask_words;
   long long total_rays;
 };

@@ -240,6 +240,20 @@ __device__ __forceinline__ void finish(const RenderParams& p, Ray& r, Counters& 
 // March pass: every candidate of every ray through the exact occupancy test
 // (renderer.h:205-208), one thread per ray in tile-major id order; writes the kept bitmask
 // [word][ray] and the kept count.  Uniform 256-iteration loops, no divergence on ray length.
+// RenderParams::ray_dirs for the packet renderer: the ray's fp32 direction and its right
+// neighbour's (renderer.h:264-265), from the same double ray generation
+__device__ __forceinline__ void store_ray_dirs(const RenderParams& p, long long idx, bool valid, int x, int y,
+                                               const d3& d) {
+  const d3 nn = valid ? ray_dir(p.cam, (double)x + 1.5, (double)y + 0.5) : d3{0, 0, 1};
+  const size_t T = (size_t)p.total_rays;
+  p.ray_dirs[idx] = (float)d.x;
+  p.ray_dirs[T + idx] = (float)d.y;
+  p.ray_dirs[2 * T + idx] = (float)d.z;
+  p.ray_dirs[3 * T + idx] = (float)nn.x;
+  p.ray_dirs[4 * T + idx] = (float)nn.y;
+  p.ray_dirs[5 * T + idx] = (float)nn.z;
+}
+
 __global__ void __launch_bounds__(128) k_march_mask(RenderParams p) {
   __shared__ double s_ts[kMaxSamples];
   for (int i = threadIdx.x; i < p.n; i += blockDim.x) s_ts[i] = p.ts[i];
@@ -250,6 +264,7 @@ __global__ void __launch_bounds__(128) k_march_mask(RenderParams p) {
   const bool valid = ray_pixel(p, idx, x, y);
   const d3 o{p.cam.origin[0], p.cam.origin[1], p.cam.origin[2]};
   const d3 d = valid ? ray_dir(p.cam, (double)x + 0.5, (double)y + 0.5) : d3{0, 0, 1};
+  if (p.ray_dirs && idx < p.total_rays) store_ray_dirs(p, idx, valid, x, y, d);
   int count = 0;
   for (int w0 = 0; w0 < p.mask_words; ++w0) {
     uint32_t bits = 0;
@@ -292,6 +307,7 @@ __global__ void __launch_bounds__(128) k_march_mask_fast(RenderParams p) {
   const bool valid = idx < p.total_rays && ray_pixel(p, idx, x, y);
   const d3 o{p.cam.origin[0], p.cam.origin[1], p.cam.origin[2]};
   const d3 d = valid ? ray_dir(p.cam, (double)x + 0.5, (double)y + 0.5) : d3{0, 0, 1};
+  if (p.ray_dirs && idx < p.total_rays) store_ray_dirs(p, idx, valid, x, y, d);
   s_dir[warp][lane][0] = d.x;
   s_dir[warp][lane][1] = d.y;
   s_dir[warp][lane][2] = d.z;

@@ -44,6 +44,9 @@ using namespace pk;
 #ifndef WS_PREFETCH
 #define WS_PREFETCH 1
 #endif
+#ifndef WS_MARCH_DIRS
+#define WS_MARCH_DIRS 1
+#endif
 #ifndef WS_PROD_WARPS
 #define WS_PROD_WARPS 4
 #endif
@@ -369,10 +372,17 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           r.valid = r.x < p.cam.width && r.y < p.row_end;
           r.alive = r.valid;
           if (r.valid) {
+#if WS_MARCH_DIRS
+            const size_t T = (size_t)p.total_rays;
+            const float* rd = p.ray_dirs + rid;
+            r.d = make_float3(__ldg(rd), __ldg(rd + T), __ldg(rd + 2 * T));
+            r.nd = make_float3(__ldg(rd + 3 * T), __ldg(rd + 4 * T), __ldg(rd + 5 * T));
+#else
             const d3 dd = ray_dir(p.cam, (double)r.x + 0.5, (double)r.y + 0.5);
             const d3 nn = ray_dir(p.cam, (double)r.x + 1.5, (double)r.y + 0.5);
             r.d = make_float3((float)dd.x, (float)dd.y, (float)dd.z);
             r.nd = make_float3((float)nn.x, (float)nn.y, (float)nn.z);
+#endif
             r.kept_total = __ldg(p.kept_count + rid);
             ++cnt.rays;
             cnt.marched += p.n;
@@ -680,6 +690,10 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
   if ((e = cudaMallocAsync(&p.kept_mask, (size_t)p.total_rays * p.mask_words * 4, s)) != cudaSuccess)
     return e;
   if ((e = cudaMallocAsync(&p.kept_count, (size_t)p.total_rays * 2, s)) != cudaSuccess) return e;
+#if WS_MARCH_DIRS
+  if ((e = cudaMallocAsync(&p.ray_dirs, (size_t)p.total_rays * 6 * sizeof(float), s)) != cudaSuccess)
+    return e;
+#endif
   if ((e = cudaMemsetAsync(p.work_counter, 0, sizeof(unsigned int), s)) != cudaSuccess) return e;
   RenderParams pm = p;
   pm.work_stats = nullptr;
@@ -708,5 +722,6 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   cudaFreeAsync(p.kept_mask, s);
   cudaFreeAsync(p.kept_count, s);
+  if (p.ray_dirs) cudaFreeAsync(p.ray_dirs, s);
   return cudaGetLastError();
 }
