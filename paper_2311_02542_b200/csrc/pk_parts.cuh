@@ -213,6 +213,15 @@ __device__ __forceinline__ int nth_set_bit(uint32_t m, int k) {
   return pos;
 }
 
+#ifndef LUMI_FLOAT_ACCUM
+#define LUMI_FLOAT_ACCUM 1
+#endif
+#if LUMI_FLOAT_ACCUM
+using accum_t = float;
+#else
+using accum_t = double;
+#endif
+
 // The owner-lane state of one ray of the packet.
 struct Ray {
   bool valid, alive;  // pixel inside the range / still compositing
@@ -220,7 +229,11 @@ struct Ray {
   float3 d, nd;       // fp32 directions for the network-input geometry
   int kept_total, contributing;
   bool term;
-  double trans, px, py, pz, depth, opac;
+  double trans;
+  // the running colour / depth / opacity sums: each step is evaluated in double and, with
+  // LUMI_FLOAT_ACCUM, rounded to fp32 (5 registers fewer in the row-owning warps); the
+  // transmittance, which decides the termination cut, stays double
+  accum_t px, py, pz, depth, opac;
 };
 
 struct Counters {
