@@ -366,10 +366,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
             break;
           }
           const long long rid = pkt * 32 + lane;
-          r.x = (int)(pkt % packets_x) * kPW + (lane % kPW);
-          r.y = p.row_begin + (int)(pkt / packets_x) * kPH + lane / kPW;
+          // the pixel and the kept count are re-derived when the packet is stored: fewer
+          // registers live across the rounds
+          const int px_ = (int)(pkt % packets_x) * kPW + (lane % kPW);
+          const int py_ = p.row_begin + (int)(pkt / packets_x) * kPH + lane / kPW;
           r.id = (int)rid;
-          r.valid = r.x < p.cam.width && r.y < p.row_end;
+          r.valid = px_ < p.cam.width && py_ < p.row_end;
           r.alive = r.valid;
           if (r.valid) {
 #if WS_MARCH_DIRS
@@ -378,12 +380,11 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
             r.d = make_float3(__ldg(rd), __ldg(rd + T), __ldg(rd + 2 * T));
             r.nd = make_float3(__ldg(rd + 3 * T), __ldg(rd + 4 * T), __ldg(rd + 5 * T));
 #else
-            const d3 dd = ray_dir(p.cam, (double)r.x + 0.5, (double)r.y + 0.5);
-            const d3 nn = ray_dir(p.cam, (double)r.x + 1.5, (double)r.y + 0.5);
+            const d3 dd = ray_dir(p.cam, (double)px_ + 0.5, (double)py_ + 0.5);
+            const d3 nn = ray_dir(p.cam, (double)px_ + 1.5, (double)py_ + 0.5);
             r.d = make_float3((float)dd.x, (float)dd.y, (float)dd.z);
             r.nd = make_float3((float)nn.x, (float)nn.y, (float)nn.z);
 #endif
-            r.kept_total = __ldg(p.kept_count + rid);
             ++cnt.rays;
             cnt.marched += p.n;
           }
@@ -616,9 +617,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       // a finished packet is stored once its last round is composited (renderer.h:233-236)
       if (pending && j - 1 >= last_round) {
         if (r.valid) {
+          const long long pk_ = r.id >> 5;
+          const int px_ = (int)(pk_ % packets_x) * kPW + (lane % kPW);
+          const int py_ = p.row_begin + (int)(pk_ / packets_x) * kPH + lane / kPW;
+          const int kept_total = __ldg(p.kept_count + r.id);
           RayResult res{r.px, r.py, r.pz, r.depth, r.opac,
-                        chunk_evals(r.term, r.contributing, r.kept_total, p.chunk), r.contributing};
-          store_ray(p, r.x, r.y, res, r.trans);
+                        chunk_evals(r.term, r.contributing, kept_total, p.chunk), r.contributing};
+          store_ray(p, px_, py_, res, r.trans);
         }
         pending = false;
         packet_live = false;
