@@ -53,17 +53,19 @@ using namespace pk;
 constexpr int kProdWarps = WS_PROD_WARPS;              // producer warps (4 or 8)
 constexpr int kProdThreads = 32 * kProdWarps;
 constexpr int kCtaThreads = 128 + kProdThreads;        // consumers [0, 128), producers after
-// WS_REGSPLIT: 8 producer warps at 3 CTAs/SM (56 registers per thread at launch); the
-// warpgroups then trade registers with setmaxnreg: consumers up to WS_CONS_REGS, producers
-// down to WS_PROD_REGS (128 * C + 256 * P <= 384 * 56)
+// WS_REGSPLIT: the warpgroups trade registers with setmaxnreg after the launch allocation
+// (80 per thread at 3 CTAs x 256 threads): the consumers, whose MLP epilogues and compositing
+// state are the register-bound side, get WS_CONS_REGS, the producers keep WS_PROD_REGS
+// (128 * C + kProdThreads * P <= kCtaThreads * launch).  With 8 producer warps (3 CTAs x 384
+// threads, 56 per thread at launch) the split is 88 / 40.
 #ifndef WS_REGSPLIT
-#define WS_REGSPLIT 0
+#define WS_REGSPLIT 1
 #endif
 #ifndef WS_CONS_REGS
-#define WS_CONS_REGS 80
+#define WS_CONS_REGS 88
 #endif
 #ifndef WS_PROD_REGS
-#define WS_PROD_REGS 40
+#define WS_PROD_REGS (WS_PROD_WARPS == 4 ? 72 : 40)
 #endif
 constexpr int kCtasPerSm = (kProdWarps == 4 || WS_REGSPLIT) ? 3 : 2;  // (registers: <= 85 per thread)
 #ifndef WS_PROD_PAIRS
