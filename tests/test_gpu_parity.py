@@ -476,3 +476,38 @@ def test_render_c3_full_model_vs_oracle(lumi, torch_cuda, oracle):
     print(f"C3 sampled rows max|dPQ|={max(errs):.3e}")
     assert max(errs) <= PIX_TOL
     assert sum(st.evals for st in stats) > 0
+
+
+def test_exact_march_pass_feeds_the_renderer(tmp_path):
+    """LUMI_MARCH_EXACT=1 swaps the production march pass for the double-precision one (A/B and
+    debugging); it must feed the packet renderer the same kept masks and ray directions, so the
+    C1 frame matches the reference golden to the same bar.  The switch is read once per
+    process, hence the subprocess."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+from conftest import GOLDEN, load_occ
+import paper_2311_02542_b200 as L
+from paper_2311_02542_b200 import scenes
+s = scenes.SMALL
+cfg = L.FieldConfig(grid=L.HashGridConfig(s.levels, s.features_per_level, s.base_resolution,
+                                          s.per_level_scale, s.table_size))
+bits, res, _ = load_occ(s.name)
+dm = L.DeviceModel(L.RadianceField.synthetic(cfg, s.seed, s.amplitude), L.OccupancyGrid(res, bits), 0)
+cam = L.CameraModel.from_spec(scenes.pinhole(256, 256))
+out = np.zeros((3, 256, 256), np.float32)
+dm.render_rows(cam, L.RenderOptions(), 0, 256, out)
+ref = np.load(GOLDEN + "/render_c1.npz")["out"]
+print(float(np.abs(out - ref).max()))
+'''
+    import os
+    env = dict(os.environ, LUMI_MARCH_EXACT="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    err = float(r.stdout.strip().splitlines()[-1])
+    print(f"exact march C1 max|dPQ|={err:.3e}")
+    assert err <= PIX_TOL
