@@ -6,7 +6,9 @@ d=/tmp/variant_$name; rm -rf $d; mkdir -p $d
 cd "$(dirname "$0")/../paper_2311_02542_b200/csrc" || exit 1
 mkdir -p ../lib/ab
 for f in *.cu; do
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
+  extra=""
+  [ "$f" = train.cu ] && extra="-fmad=false"  # as in the Makefile: the training path rounds like the reference
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $extra \
     -I../../include "$@" -Xptxas -v -c $f -o $d/${f%.cu}.o 2> $d/${f%.cu}.ptxas.txt || { cat $d/${f%.cu}.ptxas.txt; exit 1; }
 done
 for f in *.cpp; do g++ -std=c++17 -O2 -fPIC -I../../include -c $f -o $d/${f%.cpp}.o; done
