@@ -12,10 +12,14 @@
 //   * re-entrant: concurrent calls on disjoint rows from run_frame workers are safe; each
 //     worker thread may pick its GPU with lumi::cuda::set_thread_device().
 // The field/grid are uploaded once per (object, device) and re-uploaded when their contents
-// change (a cheap fingerprint is checked on every call), matching the reference's
-// "read-only during a frame" rule (SPEC.md volume_renderer).
+// change, matching the reference's "read-only during a frame" rule (SPEC.md volume_renderer).
+// The fingerprint checked on every call covers the whole occupancy grid and both MLPs, and
+// samples the hash-grid table (every ~n/4096-th float): after an edit that touches only table
+// entries (e.g. an optimizer step on the grid), call lumi::cuda::invalidate() -- it drops the
+// cached device copies so the next call re-uploads.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <map>
@@ -109,10 +113,17 @@ class DeviceField {
     p.resize(field.color_net().parameter_count());
     field.color_net().copy_params(p.data());
     mix(p.data(), p.size() * sizeof(float));
-    const size_t occ = grid.occupied_count();
+    // every occupancy bit, 64 voxels per mixing step
     const int res = grid.resolution();
-    mix(&occ, sizeof(occ));
     mix(&res, sizeof(res));
+    const size_t nv = grid.voxel_count();
+    for (size_t i = 0; i < nv; i += 64) {
+      uint64_t w = 0;
+      const size_t hi = std::min<size_t>(64, nv - i);
+      for (size_t b = 0; b < hi; ++b) w |= static_cast<uint64_t>(grid.occupied_bit(i + b)) << b;
+      h = (h ^ w) * 0x9E3779B97F4A7C15ULL;
+      h ^= h >> 29;
+    }
     return h;
   }
 
@@ -163,10 +174,20 @@ inline std::shared_ptr<DeviceField> device_field(const RadianceField<float>& fie
   return slot;
 }
 
-// Drops every cached device copy (e.g. before destroying the field).
+// Drops every cached device copy (e.g. before destroying the field).  In-flight renders keep
+// their copy alive through the shared_ptr they hold.
 inline void release_all() {
   std::lock_guard<std::mutex> lk(cache_mutex());
   cache().clear();
+}
+
+// Forces a re-upload of every cached copy of `field` on its next render (needed after edits the
+// sampled table fingerprint cannot see, see the header comment).
+template <class FieldT>
+inline void invalidate(const FieldT& field) {
+  std::lock_guard<std::mutex> lk(cache_mutex());
+  for (auto it = cache().begin(); it != cache().end();)
+    it = std::get<0>(it->first) == static_cast<const void*>(&field) ? cache().erase(it) : std::next(it);
 }
 
 }  // namespace cuda

@@ -23,8 +23,6 @@
  *                               ray_loss + backward_ray      proj/src/trainer.cpp:549-561,
  *                               proj/include/lumi/train_step.h:16-154, renderer.h:110-120,
  *                               field.h:141-179, network.h:115-136, grid.h:118-137
- *   lumi_adam_step_async        simd::adam_step              proj/include/lumi/simd.h:106-121,
- *                                                            proj/src/trainer.cpp:228-235
  *   lumi_model_device_params, lumi_model_params_updated
  *                               in-place parameter access for a device-side optimizer
  *   lumi_ipc_export, lumi_ipc_open, lumi_ipc_close
@@ -154,12 +152,13 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
                       const float* density_params, const float* color_params,
                       const uint8_t* occupancy, int occ_res, LumiModel** out);
 int lumi_model_set_occupancy(LumiModel* m, const uint8_t* occupancy, int occ_res);
-/* Frame-renderer variant: LUMI_KERNEL_TC (persistent tcgen05 MLP kernel, one live ray per
-   thread), LUMI_KERNEL_PACKET (tcgen05, warp-wide ray packets streamed candidate-major for
-   coherent gathers) or LUMI_KERNEL_SIMT (thread-per-ray fp32 CUDA-core MLP -- the numerical
-   cross-check), LUMI_KERNEL_WS (the packet kernel warp-specialised: a producer warpgroup
-   gathers while the consumer warpgroup runs the MLP, pipelined one round apart; the
-   default).  The environment variable LUMI_KERNEL=tc|packet|simt|ws sets the default. */
+/* Frame-renderer variant: LUMI_KERNEL_WS (the production kernel: warp-wide 8x4 ray packets
+   streamed candidate-major, a producer warpgroup gathering the hash grid while a consumer
+   warpgroup runs the tcgen05 MLP and composites, pipelined one round apart; the default) or
+   LUMI_KERNEL_SIMT (thread-per-ray fp32 CUDA-core field with bit-exact features -- the
+   numerical cross-check).  LUMI_KERNEL_TC / LUMI_KERNEL_PACKET name the round-1 kernels that
+   LUMI_KERNEL_WS superseded; selecting them returns LUMI_ERR_UNSUPPORTED.  The environment
+   variable LUMI_KERNEL=simt|ws sets the default. */
 enum { LUMI_KERNEL_TC = 0, LUMI_KERNEL_SIMT = 1, LUMI_KERNEL_PACKET = 2, LUMI_KERNEL_WS = 3 };
 int lumi_model_set_kernel(LumiModel* m, int kernel);
 int lumi_model_destroy(LumiModel* m);
@@ -284,11 +283,6 @@ int lumi_train_backward(LumiModel* m, const LumiTrainRay* rays, int nrays, const
                         const double* alpha_v, int ncams, const LumiRenderOptions* opts,
                         const LumiLossConfig* loss, const LumiTrainGrads* grads,
                         int32_t* ray_evals, int32_t* ray_contrib);
-/* simd::adam_step (simd.h:106-121) on device arrays of n floats: c1 = 1/(1-beta1^t),
-   c2 = 1/(1-beta2^t) precomputed by the caller (trainer.cpp:230-231). */
-int lumi_adam_step_async(float* params, const float* grads, float* mom, float* vel, uint64_t n,
-                         float lr, float beta1, float beta2, float eps, float c1, float c2,
-                         void* stream);
 /* The model's device-resident fp32 parameters (table in the grid.h:58-74 layout, density and
    colour nets weights-then-bias), for an in-place device optimizer.  After changing them,
    lumi_model_params_updated() rebuilds the derived copies the renderers read (fp16 table,

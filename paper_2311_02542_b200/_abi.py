@@ -113,7 +113,6 @@ SIGNATURES = {
     "lumi_train_backward_async": ([_vp, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp],
                                   C.c_int),
     "lumi_train_backward": ([_vp, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp], C.c_int),
-    "lumi_adam_step_async": ([_vp, _vp, _vp, _vp, _u64] + [_f] * 6 + [_vp], C.c_int),
     "lumi_model_device_params": ([_vp, _vp, _vp, _vp], C.c_int),
     "lumi_model_params_updated": ([_vp], C.c_int),
     "lumi_ipc_export": ([_vp, _vp, _vp], C.c_int),

@@ -3,8 +3,38 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "render_common.cuh"
+
+// Kernel attributes (cudaFuncSetAttribute: dynamic shared memory, carveout) belong to the
+// device context, and the drop-in drives several GPUs from one process (run_frame workers, one
+// per device, scheduler.cpp:114-152): every launcher keeps its one-time setup PER DEVICE, and
+// the first calls of concurrent workers serialise on the mutex instead of racing.
+struct PerDeviceInit {
+  static constexpr int kMaxDevices = 64;
+  std::mutex mu;
+  int value[kMaxDevices];
+  PerDeviceInit() {
+    for (int& v : value) v = -1;
+  }
+  // init(int* out) runs once per device (the current one); *out is cached and returned
+  template <class F>
+  cudaError_t get(F&& init, int* out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(mu);
+    if (value[dev] < 0) {
+      int v = 0;
+      if ((e = init(&v)) != cudaSuccess) return e;
+      value[dev] = v < 0 ? 0 : v;
+    }
+    *out = value[dev];
+    return cudaSuccess;
+  }
+};
 
 namespace lumi_dev {
 
@@ -76,19 +106,11 @@ struct TrainParams {
   int32_t* ray_contrib;
 };
 
-struct AdamConsts {
-  float lr, beta1, beta2, eps, c1, c2;
-};
-
 }  // namespace lumi_dev
 
 cudaError_t launch_render_simt(const lumi_dev::RenderParams& p, cudaStream_t s);
 cudaError_t launch_march_kept(const lumi_dev::RenderParams& p, uint32_t* mask, int32_t* counts,
                               cudaStream_t s);
-// ev (optional): 3 events recorded before the march pass, between march and render, after render
-cudaError_t launch_render_tc(lumi_dev::RenderParams p, cudaStream_t s, int num_sms,
-                             cudaEvent_t* ev = nullptr);
-size_t render_tc_smem_bytes();
 cudaError_t launch_march_mask(const lumi_dev::RenderParams& p, cudaStream_t s);
 // public [pixel][word] kept mask through the production (filtered) march pass
 cudaError_t launch_march_public(lumi_dev::RenderParams p, uint32_t* mask, int32_t* counts,
@@ -97,14 +119,11 @@ cudaError_t launch_gather_bench(const lumi_dev::GridDev& g, int n, int coherent,
                                 cudaStream_t s);
 cudaError_t launch_mlp_batch(const lumi_dev::MlpDev& mlp, const void* feat, const float* dirs, int n,
                              float* out, int num_sms, cudaStream_t s);
+// ev (optional): 3 events recorded before the march pass, between march and render, after render
 cudaError_t launch_render_ws(lumi_dev::RenderParams p, cudaStream_t s, int num_sms,
-                             cudaEvent_t* ev = nullptr);
-cudaError_t launch_render_pk(lumi_dev::RenderParams p, cudaStream_t s, int num_sms,
                              cudaEvent_t* ev = nullptr);
 cudaError_t launch_to_half(const float* src, void* dst_half, uint64_t n, cudaStream_t s);
 cudaError_t launch_bake(const lumi_dev::BakeParams& p, cudaStream_t s);
 cudaError_t launch_train_backward(lumi_dev::TrainParams p, cudaStream_t s, int num_sms,
                                   long long* kept_total, long long* eval_total);
 size_t train_backward_smem_bytes();
-cudaError_t launch_adam(float* p, const float* g, float* m, float* v, uint64_t n,
-                        lumi_dev::AdamConsts k, cudaStream_t s);

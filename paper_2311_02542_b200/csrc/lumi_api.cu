@@ -151,8 +151,6 @@ int check_opts(const LumiRenderOptions* o) {
 
 }  // namespace
 
-constexpr unsigned kCounterSlots = 64;
-
 // One host-buffer render_rows call's device resources (reused across calls).
 struct Staging {
   cudaStream_t s = nullptr;
@@ -179,8 +177,6 @@ struct LumiModel {
   float* d_fused = nullptr;  // density L2 folded into colour L1 (packet kernel), see fuse_l2_c1
   uint8_t* d_occ = nullptr;
   int occ_res = 0;
-  unsigned int* d_counter = nullptr;  // kCounterSlots per-launch tile counters
-  std::atomic<unsigned> counter_slot{0};
   int kernel = LUMI_KERNEL_WS;
   int num_sms = 148;
   std::mutex mu;
@@ -282,7 +278,7 @@ int make_params(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions
   p->chunk = o->chunk_size;
   p->row_begin = b;
   p->row_end = e;
-  p->work_counter = m->d_counter + (m->counter_slot.fetch_add(1) % kCounterSlots) * 32;
+  p->work_counter = nullptr;  // allocated per launch by the launcher (stream-ordered)
   return LUMI_OK;
 }
 
@@ -429,14 +425,12 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
   if ((e = cudaMalloc(&m->d_table, lay.total_floats * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&m->d_dparams, lay.density_params * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&m->d_cparams, lay.color_params * sizeof(float))) != cudaSuccess ||
-      (e = cudaMalloc(&m->d_counter, kCounterSlots * 32 * sizeof(unsigned int))) != cudaSuccess ||
       (e = cudaMemcpy(m->d_table, table, lay.total_floats * sizeof(float),
                       cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(m->d_dparams, dparams, lay.density_params * sizeof(float),
                       cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(m->d_cparams, cparams, lay.color_params * sizeof(float),
                       cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMemset(m->d_counter, 0, kCounterSlots * 32 * sizeof(unsigned int))) != cudaSuccess ||
       (e = cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess ||
       (e = keep_pool_memory(device)) != cudaSuccess ||
       (e = cudaMalloc(&m->d_table16, lay.total_floats * 2)) != cudaSuccess ||
@@ -453,10 +447,7 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
   if ((rc = lumi_model_set_occupancy(m, occ, occ_res))) return cleanup(rc);
   if (const char* k = std::getenv("LUMI_KERNEL")) {
     const std::string ks(k);
-    m->kernel = ks == "simt"     ? LUMI_KERNEL_SIMT
-                : ks == "tc"     ? LUMI_KERNEL_TC
-                : ks == "packet" ? LUMI_KERNEL_PACKET
-                                 : LUMI_KERNEL_WS;
+    m->kernel = ks == "simt" ? LUMI_KERNEL_SIMT : LUMI_KERNEL_WS;
   }
   *out = m;
   return LUMI_OK;
@@ -487,7 +478,6 @@ int lumi_model_destroy(LumiModel* m) {
   cudaFree(m->d_cparams);
   cudaFree(m->d_fused);
   cudaFree(m->d_occ);
-  cudaFree(m->d_counter);
   for (auto& kv : m->ts_cache) cudaFree(kv.second.first);
   for (auto& a : m->ev_pool)
     for (auto x : a) cudaEventDestroy(x);
@@ -498,8 +488,9 @@ int lumi_model_destroy(LumiModel* m) {
 
 int lumi_model_set_kernel(LumiModel* m, int kernel) {
   if (!m) return fail(LUMI_ERR_INVALID, "null model");
-  if (kernel != LUMI_KERNEL_TC && kernel != LUMI_KERNEL_SIMT && kernel != LUMI_KERNEL_PACKET &&
-      kernel != LUMI_KERNEL_WS)
+  if (kernel == LUMI_KERNEL_TC || kernel == LUMI_KERNEL_PACKET)
+    return fail(LUMI_ERR_UNSUPPORTED, "kernel variant retired (superseded by LUMI_KERNEL_WS)");
+  if (kernel != LUMI_KERNEL_SIMT && kernel != LUMI_KERNEL_WS)
     return fail(LUMI_ERR_INVALID, "unknown kernel variant");
   m->kernel = kernel;
   return LUMI_OK;
@@ -536,12 +527,8 @@ int lumi_render_rows_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRe
     if (ev) LUMI_CUDA_TRY(cudaEventRecord(ev[1], st));
     LUMI_CUDA_TRY(launch_render_simt(p, st));
     if (ev) LUMI_CUDA_TRY(cudaEventRecord(ev[2], st));
-  } else if (m->kernel == LUMI_KERNEL_PACKET) {
-    LUMI_CUDA_TRY(launch_render_pk(p, st, m->num_sms, ev));
-  } else if (m->kernel == LUMI_KERNEL_WS) {
-    LUMI_CUDA_TRY(launch_render_ws(p, st, m->num_sms, ev));
   } else {
-    LUMI_CUDA_TRY(launch_render_tc(p, st, m->num_sms, ev));
+    LUMI_CUDA_TRY(launch_render_ws(p, st, m->num_sms, ev));
   }
   return LUMI_OK;
 }
@@ -952,19 +939,6 @@ int lumi_train_backward(LumiModel* m, const LumiTrainRay* rays, int nrays, const
       (ray_contrib && nr && (e = cudaMemcpy(ray_contrib, d_co, nr * sizeof(int32_t), cudaMemcpyDeviceToHost))))
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(e)));
   return done(LUMI_OK);
-}
-
-int lumi_adam_step_async(float* params, const float* grads, float* mom, float* vel, uint64_t n,
-                         float lr, float beta1, float beta2, float eps, float c1, float c2,
-                         void* stream) {
-  if (n && (!params || !grads || !mom || !vel)) return fail(LUMI_ERR_INVALID, "adam_step: null buffer");
-  const bool aligned = ((reinterpret_cast<uintptr_t>(params) | reinterpret_cast<uintptr_t>(grads) |
-                         reinterpret_cast<uintptr_t>(mom) | reinterpret_cast<uintptr_t>(vel)) & 15) == 0;
-  if (!aligned) return fail(LUMI_ERR_INVALID, "adam_step: buffers must be 16-byte aligned");
-  lumi_dev::AdamConsts k{lr, beta1, beta2, eps, c1, c2};
-  cudaError_t e = launch_adam(params, grads, mom, vel, n, k, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return fail(LUMI_ERR_CUDA, std::string("adam_step: ") + cudaGetErrorString(e));
-  return LUMI_OK;
 }
 
 int lumi_model_device_params(LumiModel* m, float** table, float** density, float** color) {

@@ -168,13 +168,13 @@ cudaError_t launch_mlp_batch(const MlpDev& mlp, const void* feat, const float* d
                              int num_sms, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const size_t smem = sizeof(mb::Smem);
-  static bool attr = false;
-  cudaError_t e;
-  if (!attr) {
-    if ((e = cudaFuncSetAttribute(mb::k_mlp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
-      return e;
-    attr = true;
-  }
+  static PerDeviceInit once;
+  int ok = 0;
+  cudaError_t e = once.get([&](int* v) {
+    *v = 1;
+    return cudaFuncSetAttribute(mb::k_mlp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }, &ok);
+  if (e != cudaSuccess) return e;
   const int tiles = (n + 127) / 128;
   mb::k_mlp_batch<<<std::min(tiles, 4 * num_sms), 128, smem, s>>>(
       mlp, static_cast<const __half*>(feat), dirs, n, reinterpret_cast<float4*>(out));

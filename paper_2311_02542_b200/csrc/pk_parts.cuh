@@ -1,4 +1,5 @@
-// pk_parts.cuh -- pieces shared by the packet renderers (render_pk.cu, render_ws.cu): the
+// pk_parts.cuh -- pieces of the packet renderer (render_ws.cu) and the isolated MLP / gather
+// benchmarks (mlp_batch.cu): the
 // TMEM / A-tile layout, the tcgen05 layer issue and epilogue helpers, the hash-grid gather of
 // one (sample, level) pair, and the per-ray compositing state.
 #pragma once

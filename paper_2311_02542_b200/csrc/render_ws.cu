@@ -1,6 +1,6 @@
 // render_ws.cu -- warp-specialised packet renderer (the production frame kernel).
 //
-// The packet kernel (render_pk.cu) is latency bound with 16 warps per SM, and every resource
+// The round-1 packet kernel (render_pk.cu, retired) was latency bound with 16 warps per SM, and every resource
 // that would admit more row-owning warps is full (TMEM 4 x 128 columns, 128 registers x 512
 // threads, 57 KB of shared memory x 4).  Here each CTA pairs a CONSUMER warpgroup -- the four
 // row-owning warps: packet streams, geometry, the tcgen05 MLP and compositing -- with a
@@ -651,41 +651,45 @@ size_t render_ws_smem_bytes() { return sizeof(ws::Smem); }
 cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEvent_t* ev) {
   const long long rays = (long long)(p.row_end - p.row_begin) * p.cam.width;
   if (rays <= 0) return cudaSuccess;
-  static int blocks_per_sm = -1;
+  static PerDeviceInit once;
   const size_t smem = render_ws_smem_bytes();
-  cudaError_t e;
-  if (blocks_per_sm < 0) {
-    if ((e = cudaFuncSetAttribute(ws::k_render_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  int blocks_per_sm = 0;
+  cudaError_t e = once.get([&](int* out) {
+    cudaError_t x;
+    if ((x = cudaFuncSetAttribute(ws::k_render_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem)) != cudaSuccess)
-      return e;
-    if ((e = cudaFuncSetAttribute(ws::k_render_ws, cudaFuncAttributePreferredSharedMemoryCarveout,
+      return x;
+    if ((x = cudaFuncSetAttribute(ws::k_render_ws, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   100)) != cudaSuccess)
-      return e;
+      return x;
     int n = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ws::k_render_ws, ws::kCtaThreads, smem)) !=
+    if ((x = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ws::k_render_ws, ws::kCtaThreads, smem)) !=
         cudaSuccess)
-      return e;
+      return x;
     cudaFuncAttributes fa;
-    if ((e = cudaFuncGetAttributes(&fa, ws::k_render_ws)) != cudaSuccess) return e;
+    if ((x = cudaFuncGetAttributes(&fa, ws::k_render_ws)) != cudaSuccess) return x;
     int dev = 0, smem_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    if ((x = cudaGetDevice(&dev)) != cudaSuccess ||
+        (x = cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev)) != cudaSuccess)
+      return x;
     const int by_regs = 65536 / (((fa.numRegs * 32 + 255) / 256) * 256 * (ws::kCtaThreads / 32));
     const int by_smem = smem_sm / (int)(smem + 1024);
-    blocks_per_sm = std::max(1, std::min({by_regs, by_smem, 4}));  // TMEM: 128 columns per CTA
-    if (std::getenv("LUMI_MAX_CTAS"))
-      blocks_per_sm = std::max(1, std::min(blocks_per_sm, std::atoi(std::getenv("LUMI_MAX_CTAS"))));
+    int b = std::max(1, std::min({by_regs, by_smem, 4}));  // TMEM: 128 columns per CTA
+    if (std::getenv("LUMI_MAX_CTAS")) b = std::max(1, std::min(b, std::atoi(std::getenv("LUMI_MAX_CTAS"))));
     // only the shared memory the resident CTAs need; the rest of the 256 KB stays L1 data cache,
     // which the irregular hash-grid gather depends on
-    const int carve = (int)std::ceil(100.0 * blocks_per_sm * (double)(smem + 1024) / smem_sm);
-    if ((e = cudaFuncSetAttribute(ws::k_render_ws, cudaFuncAttributePreferredSharedMemoryCarveout,
+    const int carve = (int)std::ceil(100.0 * b * (double)(smem + 1024) / smem_sm);
+    if ((x = cudaFuncSetAttribute(ws::k_render_ws, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   std::min(100, carve))) != cudaSuccess)
-      return e;
+      return x;
     if (std::getenv("LUMI_DEBUG"))
-      std::fprintf(stderr, "[lumi] k_render_ws: %zu B smem (SM %d), %d regs, occupancy API %d, "
-                   "by regs %d, by smem %d -> %d CTAs/SM, carveout %d%%\n", smem, smem_sm, fa.numRegs,
-                   n, by_regs, by_smem, blocks_per_sm, std::min(100, carve));
-  }
+      std::fprintf(stderr, "[lumi] k_render_ws on device %d: %zu B smem (SM %d), %d regs, occupancy API %d, "
+                   "by regs %d, by smem %d -> %d CTAs/SM, carveout %d%%\n", dev, smem, smem_sm, fa.numRegs,
+                   n, by_regs, by_smem, b, std::min(100, carve));
+    *out = b;
+    return cudaSuccess;
+  }, &blocks_per_sm);
+  if (e != cudaSuccess) return e;
   p.tile_w = pk::kPW;
   p.tile_h = pk::kPH;
   p.tiles_x = (p.cam.width + pk::kPW - 1) / pk::kPW;
@@ -701,6 +705,9 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
   if ((e = cudaMallocAsync(&p.ray_dirs, (size_t)p.total_rays * 6 * sizeof(float), s)) != cudaSuccess)
     return e;
 #endif
+  // the packet counter of THIS launch (stream-ordered allocation: concurrent launches on other
+  // streams never share it)
+  if ((e = cudaMallocAsync(&p.work_counter, 256, s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(p.work_counter, 0, sizeof(unsigned int), s)) != cudaSuccess) return e;
   RenderParams pm = p;
   pm.work_stats = nullptr;
@@ -729,6 +736,7 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   cudaFreeAsync(p.kept_mask, s);
   cudaFreeAsync(p.kept_count, s);
+  cudaFreeAsync(p.work_counter, s);
   if (p.ray_dirs) cudaFreeAsync(p.ray_dirs, s);
   return cudaGetLastError();
 }

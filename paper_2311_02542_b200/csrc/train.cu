@@ -635,37 +635,6 @@ __global__ void __launch_bounds__(256) k_train_reduce(TrainParams p, const doubl
   if (threadIdx.x == 0) p.alpha_grad[c] += tot;
 }
 
-// simd::adam_step (simd.h:106-121), elementwise, float4 body + scalar tail
-__global__ void __launch_bounds__(256) k_adam(float* __restrict__ pm, const float* __restrict__ g,
-                                              float* __restrict__ mom, float* __restrict__ vel,
-                                              uint64_t n, AdamConsts k) {
-  const uint64_t n4 = n / 4;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  auto one = [&](float& p_, float g_, float& m_, float& v_) {
-    const float mi = k.beta1 * m_ + (1.f - k.beta1) * g_;
-    const float vi = k.beta2 * v_ + (1.f - k.beta2) * g_ * g_;
-    m_ = mi;
-    v_ = vi;
-    const float mhat = mi * k.c1, vhat = vi * k.c2;
-    p_ -= k.lr * mhat / (sqrtf(vhat) + k.eps);
-  };
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-    float4 P = reinterpret_cast<float4*>(pm)[i];
-    const float4 G = __ldg(reinterpret_cast<const float4*>(g) + i);
-    float4 M = reinterpret_cast<float4*>(mom)[i];
-    float4 V = reinterpret_cast<float4*>(vel)[i];
-    one(P.x, G.x, M.x, V.x);
-    one(P.y, G.y, M.y, V.y);
-    one(P.z, G.z, M.z, V.z);
-    one(P.w, G.w, M.w, V.w);
-    reinterpret_cast<float4*>(pm)[i] = P;
-    reinterpret_cast<float4*>(mom)[i] = M;
-    reinterpret_cast<float4*>(vel)[i] = V;
-  }
-  for (uint64_t i = 4 * n4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    one(pm[i], g[i], mom[i], vel[i]);
-}
-
 }  // namespace tr
 }  // namespace lumi_dev
 
@@ -724,16 +693,19 @@ cudaError_t launch_train_backward(TrainParams p, cudaStream_t s, int num_sms, lo
       (e = act.alloc(T)))
     return e;
   tr::k_train_samples<<<mb, 128, 0, s>>>(p, words, masks.p, off.p, smp.p);
-  static bool attr = false;
+  static PerDeviceInit once;
   const size_t smem = sizeof(tr::Smem);
-  if (!attr) {
-    if ((e = cudaFuncSetAttribute(tr::k_train_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem)) ||
-        (e = cudaFuncSetAttribute(tr::k_train_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem)))
-      return e;
-    attr = true;
-  }
+  int ok = 0;
+  if ((e = once.get([&](int* v) {
+         *v = 1;
+         cudaError_t x = cudaFuncSetAttribute(tr::k_train_tiles<true>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+         if (x == cudaSuccess)
+           x = cudaFuncSetAttribute(tr::k_train_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem);
+         return x;
+       }, &ok)))
+    return e;
   if (total > 0) {
     const int ftiles = (total + tr::kTile - 1) / tr::kTile;
     tr::k_train_tiles<false><<<std::min(ftiles, num_sms), tr::kThreads, smem, s>>>(
@@ -758,11 +730,3 @@ cudaError_t launch_train_backward(TrainParams p, cudaStream_t s, int num_sms, lo
   return cudaGetLastError();
 }
 
-cudaError_t launch_adam(float* p, const float* g, float* m, float* v, uint64_t n, AdamConsts k,
-                        cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
-  const uint64_t want = (n / 4 + 255) / 256;
-  const unsigned blocks = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), 148ull * 16);
-  tr::k_adam<<<blocks, 256, 0, s>>>(p, g, m, v, n, k);
-  return cudaGetLastError();
-}

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import itertools
 import os
 import math
 import threading
@@ -36,6 +37,12 @@ __all__ = [
 
 def _p(a) -> Optional[int]:
     return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# Content versions come from ONE process-wide counter, so a new object never repeats a version a
+# dead object (whose id() Python may reuse) had: a cached device copy can only match the object
+# and the edit it was made from.
+_versions = itertools.count(1)
 
 
 @dataclass
@@ -97,7 +104,7 @@ class RadianceField:
         self.grid_params = np.zeros(self.layout.total_floats, np.float32)
         self.density_params = np.zeros(self.layout.density_params, np.float32)
         self.color_params = np.zeros(self.layout.color_params, np.float32)
-        self.version = 0
+        self.version = next(_versions)
 
     def config(self) -> FieldConfig:
         return self.cfg
@@ -106,7 +113,7 @@ class RadianceField:
         d = self.cfg.desc()
         check(_abi.lib().lumi_synth_params(C.byref(d), int(seed), float(amp), _p(self.grid_params),
                                            _p(self.density_params), _p(self.color_params)))
-        self.version += 1
+        self.version = next(_versions)
 
     def init_random(self, seed: int) -> None:
         """RadianceField::init_random (field.h:88-93), bit-identical pcg32 stream."""
@@ -127,7 +134,7 @@ class RadianceField:
 
     def touch(self) -> None:
         """Call after editing parameters in place so cached device copies refresh."""
-        self.version += 1
+        self.version = next(_versions)
 
 
 class OccupancyGrid:
@@ -148,7 +155,7 @@ class OccupancyGrid:
             if bits.size != n:
                 raise Error("occupancy: bit count does not match resolution")
             self.bits = (bits != 0).astype(np.uint8)
-        self.version = 0
+        self.version = next(_versions)
 
     def resolution(self) -> int:
         return self.res
@@ -176,7 +183,7 @@ class OccupancyGrid:
         return int(self.bits.sum())
 
     def touch(self) -> None:
-        self.version += 1
+        self.version = next(_versions)
 
 
 class ContractionMode(enum.IntEnum):
@@ -283,9 +290,8 @@ class DeviceModel:
         self._lock = threading.Lock()
 
     def set_kernel(self, kernel: str) -> None:
-        """'ws' (warp-specialised packet kernel, default), 'packet' (packet-coherent tcgen05
-        kernel), 'tc' (one ray per thread tcgen05 kernel) or 'simt' (fp32 CUDA-core
-        cross-check)."""
+        """'ws' (the warp-specialised tcgen05 packet kernel, default) or 'simt' (fp32
+        CUDA-core cross-check with bit-exact features)."""
         k = {"tc": _abi.LUMI_KERNEL_TC, "simt": _abi.LUMI_KERNEL_SIMT,
              "packet": _abi.LUMI_KERNEL_PACKET, "ws": _abi.LUMI_KERNEL_WS}[kernel]
         check(_abi.lib().lumi_model_set_kernel(self.h, k))
@@ -386,22 +392,56 @@ class DeviceModel:
 
 
 _cache_lock = threading.Lock()
+# field -> grid -> device -> DeviceModel; both levels are weak, so a dead field or grid drops
+# its device copies (and their device memory)
 _model_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
-def _device_model(field: RadianceField, grid: OccupancyGrid, device: int) -> DeviceModel:
+class _Lease:
+    """A render's hold on a cached DeviceModel: a model replaced while renders still use it is
+    closed by the last of them, never under a running render."""
+
+    def __init__(self, m: DeviceModel):
+        self.m = m
+
+    def __enter__(self) -> DeviceModel:
+        return self.m
+
+    def __exit__(self, *a):
+        with _cache_lock:
+            self.m._users -= 1
+            if self.m._retired and self.m._users == 0:
+                self.m.close()
+
+
+def _retire(m: DeviceModel) -> None:
+    # caller holds _cache_lock
+    m._retired = True
+    if m._users == 0:
+        m.close()
+
+
+def _device_model(field: RadianceField, grid: OccupancyGrid, device: int) -> _Lease:
     with _cache_lock:
-        per_field = _model_cache.setdefault(field, {})
-        key = (device, id(grid))
-        m = per_field.get(key)
+        per_grid = _model_cache.setdefault(field, weakref.WeakKeyDictionary())
+        per_dev = per_grid.setdefault(grid, {})
+        m = per_dev.get(device)
         if m is None or m.field_version != field.version:
             if m is not None:
-                m.close()
+                _retire(m)
             m = DeviceModel(field, grid, device)
-            per_field[key] = m
+            m._users, m._retired = 0, False
+            per_dev[device] = m
         elif m.grid_version != grid.version:
-            m.set_occupancy(grid)
-        return m
+            if m._users == 0:
+                m.set_occupancy(grid)
+            else:  # in use by another render: give this one a fresh copy
+                _retire(m)
+                m = DeviceModel(field, grid, device)
+                m._users, m._retired = 0, False
+                per_dev[device] = m
+        m._users += 1
+        return _Lease(m)
 
 
 def render_rows(field: RadianceField, grid: OccupancyGrid, cam: CameraModel, opts: RenderOptions,
@@ -416,8 +456,9 @@ def render_rows(field: RadianceField, grid: OccupancyGrid, cam: CameraModel, opt
 
     if not (row_begin >= 0 and row_end <= cam.height and row_begin <= row_end):
         raise Error("render_rows: row range outside image")
-    m = _device_model(field, grid, device)
-    m.render_rows(cam, opts, row_begin, row_end, arr(out), arr(depth_out), arr(opacity_out), stats)
+    with _device_model(field, grid, device) as m:
+        m.render_rows(cam, opts, row_begin, row_end, arr(out), arr(depth_out), arr(opacity_out),
+                      stats)
 
 
 def lod_levels_of(cfg: FieldConfig) -> List[int]:

@@ -5,7 +5,9 @@ Mirrors the per-ray body of the reference training loop (proj/src/trainer.cpp:54
 ``backward_ray`` (train_step.h:127-154: ``composite_backward_sigma`` renderer.h:110-120,
 ``RadianceField::backward_chunk`` field.h:141-179, ``Mlp::backward`` network.h:115-136,
 ``MultiResHashGrid::encode_backward`` grid.h:118-137), accumulated into ``FieldGradients``
-(field.h:48-62), plus the ``adam_step`` update (simd.h:106-121, trainer.cpp:228-235).
+(field.h:48-62).  The optimizer (``adam_step``, simd.h:106-121) and the training loop are out
+of scope; tools/device_trainer.py shows a device-resident loop
+built on this reverse path.
 """
 from __future__ import annotations
 
@@ -114,75 +116,3 @@ def train_backward(model: DeviceModel, rays: np.ndarray, cameras: Sequence[Camer
     check(_abi.lib().lumi_train_backward(model.h, _p(rays), n, _p(tnf), _p(av), len(cameras),
                                          C.byref(od), C.byref(lc), C.byref(g), _p(ev), _p(co)))
     return (LossTerms(loss.total, loss.image, loss.depth, loss.dvar, loss.dist), ev[:n], co[:n])
-
-
-def adam_c(beta: float, t: int) -> float:
-    """1 / (1 - beta^t) as trainer.cpp:230-231 computes it (double, then float)."""
-    return float(np.float32(1.0 / (1.0 - math.pow(beta, t))))
-
-
-class DeviceTrainer:
-    """A device-resident optimisation step over a DeviceModel: zero the gradients, run the
-    reverse path for a batch of rays, apply Adam to the grid and both networks in place
-    (trainer.cpp:547-625, the field-parameter part), refresh the renderer's derived copies.
-    Device memory comes from torch (plumbing); every kernel is in liblumi_cuda.so."""
-
-    def __init__(self, model: DeviceModel, cameras: Sequence[CameraModel], cfg: TrainConfig,
-                 alpha_v: Sequence[float]):
-        import torch
-
-        self.torch = torch
-        self.model, self.cfg = model, cfg
-        self.cameras = list(cameras)
-        self.alpha_v = np.ascontiguousarray(alpha_v, np.float64)
-        dev = torch.device("cuda", model.device)
-        lay = _abi.GridLayout()
-        d = model.cfg.desc()
-        check(_abi.lib().lumi_field_layout(C.byref(d), C.byref(lay)))
-        sizes = (int(lay.total_floats), int(lay.density_params), int(lay.color_params))
-        z = lambda k: torch.zeros(k, dtype=torch.float32, device=dev)  # noqa: E731
-        self.grads = [z(k) for k in sizes]
-        self.m = [z(k) for k in sizes]
-        self.v = [z(k) for k in sizes]
-        self.alpha_grad = torch.zeros(len(self.cameras), dtype=torch.float64, device=dev)
-        self.loss = torch.zeros(5, dtype=torch.float64, device=dev)
-        t, dp, cp = C.c_void_p(), C.c_void_p(), C.c_void_p()
-        check(_abi.lib().lumi_model_device_params(model.h, C.byref(t), C.byref(dp), C.byref(cp)))
-        self.params = (t.value, dp.value, cp.value)
-        self.sizes = sizes
-        self.t = 0
-
-    def step(self, rays, depth_active: bool = True, opts: Optional[RenderOptions] = None,
-             stream: int = 0) -> LossTerms:
-        """One iteration on a device tensor of LumiTrainRay records (uint8 [n, 128]) or a
-        host TRAIN_RAY_DTYPE array (copied)."""
-        torch = self.torch
-        if isinstance(rays, np.ndarray):
-            host = _check_rays(rays)
-            rays = torch.from_numpy(host.view(np.uint8).reshape(-1, 128)).to(self.grads[0].device)
-        n = int(rays.shape[0])
-        opts = opts or RenderOptions(samples_per_ray=self.cfg.samples_per_ray,
-                                     termination_transmittance=self.cfg.termination_transmittance)
-        for b in (*self.grads, self.alpha_grad, self.loss):
-            b.zero_()
-        g = _abi.TrainGrads(self.grads[0].data_ptr(), self.grads[1].data_ptr(),
-                            self.grads[2].data_ptr(), self.alpha_grad.data_ptr(),
-                            self.loss.data_ptr())
-        tnf = _cam_tnf(self.cameras)
-        lc = self.cfg.loss_desc(1.0 / max(n, 1), depth_active)
-        od = opts.desc()
-        L = _abi.lib()
-        check(L.lumi_train_backward_async(self.model.h, rays.data_ptr(), n, _p(tnf),
-                                          _p(self.alpha_v), len(self.cameras), C.byref(od),
-                                          C.byref(lc), C.byref(g), None, None, stream))
-        self.t += 1
-        c = self.cfg
-        for k, (ptr, size) in enumerate(zip(self.params, self.sizes)):
-            lr = c.lr_grid if k == 0 else c.lr_net
-            check(L.lumi_adam_step_async(ptr, self.grads[k].data_ptr(), self.m[k].data_ptr(),
-                                         self.v[k].data_ptr(), size, lr, c.beta1, c.beta2,
-                                         c.adam_eps, adam_c(c.beta1, self.t),
-                                         adam_c(c.beta2, self.t), stream))
-        check(L.lumi_model_params_updated(self.model.h))
-        lv = self.loss.cpu().numpy()
-        return LossTerms(*map(float, lv))

@@ -25,6 +25,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 
 def main():
@@ -52,7 +53,8 @@ def main():
     cmodels = [L.CameraModel.from_spec(c) for c in cams]
     av = np.linspace(0.0, 0.2, a.cameras)
     cfg = T.TrainConfig()
-    tr = T.DeviceTrainer(dm, cmodels, cfg, av)
+    import device_trainer as DT
+    tr = DT.DeviceTrainer(dm, cmodels, cfg, av)
     d_rays = torch.from_numpy(rays.view(np.uint8).reshape(-1, 128)).cuda()
     lib = _abi.lib()
     g = _abi.TrainGrads(tr.grads[0].data_ptr(), tr.grads[1].data_ptr(), tr.grads[2].data_ptr(),
@@ -72,12 +74,10 @@ def main():
                                                  stream))
 
     def adam(t):
-        for k, (ptr, size) in enumerate(zip(tr.params, tr.sizes)):
+        for k, (p, size) in enumerate(zip(tr.param_views, tr.sizes)):
             lr = cfg.lr_grid if k == 0 else cfg.lr_net
-            _abi.check(lib.lumi_adam_step_async(ptr, tr.grads[k].data_ptr(), tr.m[k].data_ptr(),
-                                                tr.v[k].data_ptr(), size, lr, cfg.beta1, cfg.beta2,
-                                                cfg.adam_eps, T.adam_c(cfg.beta1, t),
-                                                T.adam_c(cfg.beta2, t), stream))
+            DT.adam_step(torch, p, tr.grads[k], tr.m[k], tr.v[k], lr, cfg.beta1, cfg.beta2,
+                         cfg.adam_eps, DT.adam_c(cfg.beta1, t), DT.adam_c(cfg.beta2, t))
 
     def timed(fn, steps):
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

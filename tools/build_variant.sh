@@ -13,4 +13,4 @@ for f in *.cu; do
 done
 for f in *.cpp; do g++ -std=c++17 -O2 -fPIC -I../../include -c $f -o $d/${f%.cpp}.o; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../lib/ab/$name.so $d/*.o -lcudart
-grep -h -A2 "k_render_pk\|k_render_tc" $d/*.ptxas.txt | grep -E "registers|spill" | head -4
+grep -h -A2 "k_render_ws\|k_march" $d/*.ptxas.txt | grep -E "registers|spill" | head -4
