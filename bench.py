@@ -28,6 +28,11 @@ sys.path.insert(0, ROOT)
 METRIC = "Mrays/sec and fps for dual 2K×2K eyebuffers at 1/2/4/8 B200 vs CPU ref"
 UNIT = "Mrays/s"
 GATHER_BYTES_PER_LEVEL_SAMPLE = 8 * 2 * 4  # 8 corners x 2 features x fp32
+# what the timed kernels compute in: the hash table and the MLP operands are fp16 (tcgen05
+# kind::f16, fp32 accumulators in TMEM), sample positions / contraction / LOD are fp32 (the
+# occupancy decisions certified against the reference's double arithmetic, undecided ones
+# re-tested in f64), the transmittance that decides the early cut is f64
+DTYPE = "fp16 table + fp16 MLP operands (fp32 accum), fp32 geometry/LOD, f64 transmittance"
 MLP_FLOP_PER_SAMPLE = 18944  # 9,472 MACs per evaluated sample
 
 
@@ -42,23 +47,63 @@ def parse():
                     help="target CPU time of the reference baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-checkpoint", action="store_true",
+                    help="build the scene in memory instead of through a LUMICKPT round trip")
     return ap.parse_args()
 
 
-def load_scene(spec):
-    """Synthetic bake of SURVEY.md §8d: seeded parameters + the reference-baked occupancy."""
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: launch N ranks (one per GPU) with
+    torch.distributed.run on 127.0.0.1, as the driver does; rank 0's JSON line passes through.
+    NCCL's INIT log stays on so the communicator's N ranks are visible in the output."""
+    import socket
+    shared = os.environ.get("LUMI_BENCH_SHARED_GPU") == "1"
+    if not shared:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: this host has {have} CUDA device(s)")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def occupancy_bits(spec):
+    """The scene's occupancy bits: the reference-baked 128^3 grid of SURVEY.md §8d (committed
+    fixture), or all-occupied for the dense stress config."""
+    if spec.dense_occupancy:
+        return spec.occ_res, np.ones(spec.occ_res ** 3, np.uint8)
+    z = np.load(os.path.join(ROOT, "tests", "golden", f"occ_{spec.name.replace('-dense', '')}.npz"))
+    res = int(z["res"])
+    return res, np.unpackbits(z["bits"])[: res ** 3]
+
+
+def load_scene(spec, via_checkpoint: bool = True):
+    """Synthetic bake of SURVEY.md §8d: seeded parameters + the reference-baked occupancy,
+    written to a LUMICKPT v1 checkpoint (save_checkpoint, scene.cpp:320-351) and loaded back
+    through the product's checkpoint reader (load_checkpoint, scene.cpp:353-394) -- the model
+    reaches the GPU the way a trained scene would."""
+    import tempfile
     import paper_2311_02542_b200 as L
     g = L.HashGridConfig(spec.levels, spec.features_per_level, spec.base_resolution,
                          spec.per_level_scale, spec.table_size)
     field = L.RadianceField.synthetic(L.FieldConfig(grid=g), spec.seed, spec.amplitude)
-    if spec.dense_occupancy:
-        grid = L.OccupancyGrid(spec.occ_res)
-    else:
-        z = np.load(os.path.join(ROOT, "tests", "golden",
-                                 f"occ_{spec.name.replace('-dense', '')}.npz"))
-        res = int(z["res"])
-        grid = L.OccupancyGrid(res, np.unpackbits(z["bits"])[: res ** 3])
-    return field, grid
+    res, bits = occupancy_bits(spec)
+    grid = L.OccupancyGrid(res, bits)
+    if not via_checkpoint:
+        return field, grid
+    with tempfile.TemporaryDirectory(prefix="lumi_bench_") as d:
+        path = os.path.join(d, f"{spec.name}.lumickpt")
+        L.save_checkpoint(path, field, grid, samples_per_ray=256)
+        field2, grid2, _ = L.load_checkpoint(path)
+    return field2, grid2
 
 
 class ClockSampler:
@@ -136,28 +181,54 @@ def gather_roofline(achieved, table_log2: int):
             "peak_source": "profiles/r01_bench_gather.json (tools/bench_gather.py, coherent points)"}
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per launch from the committed ncu --set full capture, if any."""
+def ncu_kernel(kernel: str):
+    """The render kernel's entry of the committed ncu --set full summary (profiles/), if any."""
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        k = prof["kernels"].get(kernel)
-        return None if k is None else k.get("dram_bytes_per_launch")
+        k = dict(prof["kernels"].get(kernel) or {})
+        k["_source"] = f"profiles/{prof.get('source', 'ncu_summary.json')}"
+        return k
     except Exception:
+        return {}
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch from the committed ncu --set full capture, if any."""
+    return ncu_kernel(kernel).get("dram_bytes_per_launch")
+
+
+def issue_roofline(kernel: str, ms_per_launch: float, sm_mhz):
+    """The binding limit of the render kernel: warp-instruction issue.  ncu's executed warp
+    instructions per launch of the same kernel and workload (one C3 eye) over the live
+    per-launch time, against 4 issue slots per SM per clock x 148 SMs."""
+    k = ncu_kernel(kernel)
+    wi = k.get("warp_instructions")
+    if not wi or not ms_per_launch or not sm_mhz:
         return None
+    achieved = wi / (ms_per_launch / 1e3) / 1e9
+    peak = 4 * 148 * float(sm_mhz) / 1e3
+    return {"bound": "issue", "achieved": round(achieved, 1), "peak": round(peak, 1),
+            "unit": "G warp-instructions/s", "frac": round(achieved / peak, 4),
+            "ncu_issue_active": k.get("issue_active_pct"),
+            "source": f"{k['_source']}: {wi:.4g} warp instructions per launch; peak = 4 issue "
+                      f"slots/SM/clk x 148 SMs x {float(sm_mhz):.0f} MHz (sampled under load)"}
 
 
 # --------------------------------------------------------------------------- reference
 
 def reference_model(spec):
+    """The same scene for the reference's own renderer (oracle/_ref): its own init_random +
+    grid overwrite (ref_wrap.cpp ref_synth_params, bit-identical to the product's) and the same
+    occupancy bits -- the reference arm loads nothing from the product library."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     ref = O.Reference()
     cfg = O.field_config(spec.levels, spec.features_per_level, spec.base_resolution,
                          spec.per_level_scale, spec.table_size, spec.hidden_width,
                          spec.bottleneck, 0)
-    field, grid = load_scene(spec)  # host-only parts of the product: params + occupancy bits
-    p = O.Params(cfg, field.grid_params, field.density_params, field.color_params)
-    return O, ref, ref.model(p, grid.bits, grid.res)
+    p = ref.synth_params(cfg, spec.seed, spec.amplitude)
+    res, bits = occupancy_bits(spec)
+    return O, ref, ref.model(p, bits, res)
 
 
 SAMPLE_BANDS = 8
@@ -220,7 +291,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(mrays, 6), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(wall * 1000 / max(args.steps, 1), 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64 geometry / f32 field",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64 geometry / f32 field / f64 compositing",
         "data": "synthetic (seeded init_random + reference-baked occupancy)",
         "config": {"workload": f"{args.config}: {cfg.description}", "eye_size": cfg.eye_size,
                    "eyes": cfg.eyes, "table_size": cfg.model.table_size,
@@ -267,7 +338,7 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = scenes.CONFIGS[args.config]
     spec = cfg.model
-    field, grid = load_scene(spec)
+    field, grid = load_scene(spec, via_checkpoint=not args.no_checkpoint)
     dm = L.DeviceModel(field, grid, local)
     opts = L.RenderOptions()
     drv = StereoFrameDriver(torch, dm, cfg.eye_size, opts, rank, world, dist=dist if world > 1 else None,
@@ -359,12 +430,13 @@ def run_ours(args):
 
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
+    mlp_peak = peaks.get("bf16_tflops_sustained", 1398.6)
+    clocks = clk.summary()
     evals, level_samples, candidates, rays = (float(x) for x in counters)
     # the tensor-core kernel gathers the fp16 copy of the table (32 B per level-sample), the
     # SIMT cross-check the reference fp32 layout (64 B)
     bytes_per_ls = GATHER_BYTES_PER_LEVEL_SAMPLE // (1 if dm.kernel == "simt" else 2)
-    kname = {"tc": "k_render_tc", "packet": "k_render_pk", "simt": "k_render_simt",
-             "ws": "k_render_ws"}[dm.kernel]
+    kname = {"simt": "k_render_simt", "ws": "k_render_ws"}[dm.kernel]
     gather_bytes = level_samples * bytes_per_ls
     # the render kernel's own launches on rank 0 (CUDA events on the launch stream around
     # each launch, march pass excluded); counters are summed over ranks, so scale by 1/world
@@ -395,7 +467,10 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(elapsed / args.steps, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64 geometry / f32 field", "data": "synthetic (seeded init_random + reference-baked occupancy)",
+        "dtype": DTYPE,
+        "data": "synthetic (seeded init_random + reference-baked occupancy, through a LUMICKPT "
+                "checkpoint round trip)" if not args.no_checkpoint else
+                "synthetic (seeded init_random + reference-baked occupancy)",
         "config": {"workload": f"{args.config}: {cfg.description}", "eye_size": cfg.eye_size,
                    "eyes": 2, "table_size": spec.table_size, "rays_per_frame": rays_frame,
                    "samples_per_ray": opts.samples_per_ray, "parallelism": f"rows{world}", "gather": drv.gather or "none",
@@ -429,9 +504,14 @@ def run_ours(args):
                                     f"(CUDA events on the launch stream)"},
         "roofline_gather": gather_roofline(achieved, spec.table_log2),
         "roofline_mlp": {"bound": "tensor", "achieved": None if mlp_tflops is None else round(mlp_tflops, 2),
-                         "peak": peaks.get("bf16_tflops_sustained", 1398.6), "unit": "TFLOP/s",
-                         "algorithmic": "18,944 FLOP per evaluated sample"},
-        "clocks": clk.summary(),
+                         "peak": mlp_peak, "unit": "TFLOP/s",
+                         "frac": None if mlp_tflops is None else round(mlp_tflops / mlp_peak, 4),
+                         "algorithmic": "18,944 FLOP per evaluated sample (fp16 operands; "
+                                        "peak = MEASURED_PEAKS bf16 sustained, the kernel runs "
+                                        "inside a long step)"},
+        "roofline_issue": issue_roofline(kname, render_ms / max(render_launches, 1),
+                                         clocks.get("sm_mhz") or peaks.get("sm_max_mhz")),
+        "clocks": clocks,
         "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "path": "lumi_render_rows (C ABI) into pinned host buffers: the kernel stores the pixels over PCIe (zero-copy)" if world == 1 else
@@ -446,6 +526,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:

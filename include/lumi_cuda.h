@@ -25,6 +25,12 @@
  *                               field.h:141-179, network.h:115-136, grid.h:118-137
  *   lumi_model_device_params, lumi_model_params_updated
  *                               in-place parameter access for a device-side optimizer
+ *   lumi_frame_driver_create / _render[_host] / _assignment / _set_assignment / _destroy
+ *                               run_frame + next_assignment with GPUs as the workers: one
+ *                               host thread per GPU, bands stored into one device frame
+ *                               over NVLink peer access  proj/src/scheduler.cpp:114-162
+ *   lumi_checkpoint_read, lumi_checkpoint_write
+ *                               load_checkpoint / save_checkpoint   proj/src/scene.cpp:320-394
  *   lumi_ipc_export, lumi_ipc_open, lumi_ipc_close
  *                               the frame gather of run_frame (results gathered by row
  *                               index into one shared Image, proj/src/scheduler.cpp:114-152)
@@ -170,6 +176,8 @@ int lumi_model_set_timing(LumiModel* m, int enable);
 int lumi_model_take_timing(LumiModel* m, double* march_ms, double* render_ms, int* launches);
 /* Device-side memory footprint of the model in bytes. */
 int lumi_model_bytes(const LumiModel* m, uint64_t* bytes);
+/* The CUDA device the model lives on. */
+int lumi_model_device(const LumiModel* m, int* device);
 
 /* ---- rendering ------------------------------------------------------------------ */
 /* Drop-in for render_rows (renderer.h:252-278): host planar buffers of the camera's
@@ -198,6 +206,14 @@ int lumi_march_kept_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRen
 int lumi_mlp_batch_async(LumiModel* m, const void* features, const float* dirs, int n, float* out,
                          void* stream);
 
+/* MultiResHashGrid::encode (grid.h:90-114) through the renderer's production gather (fp16 table
+   copy, fp16 trilinear weights, packed-fp16 accumulation): n contracted positions pos [n][3]
+   fp32, LOD weights as the renderer carries them, lod [n] = fl with w_l = clamp(fl - l, 0, 1)
+   (fl = 1e-4 is the reference's L_eff < 0 case, only w_0 = 1e-4) -> out [n][2 * levels] fp32,
+   zeros where w_l = 0.  Device pointers, enqueued on `stream`.  Parity tooling for the gather. */
+int lumi_encode_async(LumiModel* m, int n, const float* pos, const float* lod, float* out,
+                      void* stream);
+
 /* The hash-grid gather alone (benchmark of the attainable gather rate): n points, every level
    of each through the renderer's gather (fp16 table); coherent != 0 gives each warp an 8x4
    patch of neighbouring points (like a ray packet), 0 uniform random points.  out: device
@@ -222,6 +238,13 @@ typedef struct LumiCheckpointInfo {
    color[color_params], occupancy[occ_res^3]). */
 int lumi_checkpoint_read(const char* path, LumiCheckpointInfo* info, float* table,
                          float* density_params, float* color_params, uint8_t* occupancy);
+/* save_checkpoint (scene.cpp:320-351) of a rendering model: info->field / samples_per_ray /
+   contraction / background / occ_res / n_cameras, the parameter arrays in the
+   lumi_field_layout sizes, alpha_v [n_cameras] (NULL = zeros), occupancy [occ_res^3]
+   (nonzero = occupied).  The occupancy grid's training trackers are written as zeros. */
+int lumi_checkpoint_write(const char* path, const LumiCheckpointInfo* info, const float* table,
+                          const float* density_params, const float* color_params,
+                          const double* alpha_v, const uint8_t* occupancy);
 
 /* ---- occupancy bake (GPU) ------------------------------------------------------- */
 /* OccupancyGrid::probe(k) with the density head + prune(alpha), zero history, no
@@ -289,6 +312,35 @@ int lumi_train_backward(LumiModel* m, const LumiTrainRay* rays, int nrays, const
    fused density-L2/colour-L1 layer).  Synchronous. */
 int lumi_model_device_params(LumiModel* m, float** table, float** density, float** color);
 int lumi_model_params_updated(LumiModel* m);
+
+/* ---- native multi-GPU frame driver -------------------------------------
+   run_frame (scheduler.cpp:114-152) with GPUs as the workers.  models[i] is worker i's replica
+   (one per GPU; the same model may appear several times to run several workers on one GPU,
+   each on its own stream).  One persistent host thread per worker renders its contiguous band
+   of the stacked image (eyes x eye_height rows of `width`; eye e's camera row y is stacked row
+   e * eye_height + y) with lumi_render_rows_async; a band crossing the eye seam becomes one
+   launch per eye.  The frame target is device memory on any GPU: workers on other GPUs store
+   their pixels straight into it over NVLink (peer access enabled on first use) -- the gather
+   is the render kernel's epilogue.  After each frame the per-worker CUDA-event ms drive
+   next_assignment (scheduler.cpp:154-162, dampening lambda) for the next frame; the first frame
+   uses equal_assignment.  lumi_frame_driver_render is synchronous; wall_ms is the host time of
+   the frame, worker_ms / worker_rays ([workers], optional) the FrameStats fields.  A failing
+   worker fails the frame with "run_frame: worker i failed: ..." (scheduler.cpp:137-139). */
+typedef struct LumiFrameDriver LumiFrameDriver;
+int lumi_frame_driver_create(LumiModel* const* models, int workers, int width, int eye_height,
+                             int eyes, double dampening, LumiFrameDriver** out);
+int lumi_frame_driver_render(LumiFrameDriver* d, const LumiCameraDesc* cams /* [eyes] */,
+                             const LumiRenderOptions* opts, const LumiFrameTarget* target,
+                             double* wall_ms, double* worker_ms, int64_t* worker_rays);
+/* The same into a host planar image [3][eyes * eye_height][width] (the reference's shared
+   Image<float>): the frame is rendered into a device frame on worker 0's GPU, then copied. */
+int lumi_frame_driver_render_host(LumiFrameDriver* d, const LumiCameraDesc* cams,
+                                  const LumiRenderOptions* opts, float* out, double* wall_ms,
+                                  double* worker_ms, int64_t* worker_rays);
+/* the assignment the NEXT frame will use: rows per worker (contiguous in worker order) */
+int lumi_frame_driver_assignment(const LumiFrameDriver* d, int32_t* rows, double* shares);
+int lumi_frame_driver_set_assignment(LumiFrameDriver* d, const int32_t* rows);
+int lumi_frame_driver_destroy(LumiFrameDriver* d);
 
 /* ---- peer-memory frame gather ------------------------------------------
    lumi_ipc_export: an inter-process handle (LUMI_IPC_HANDLE_BYTES opaque bytes) for the

@@ -470,6 +470,7 @@ class Reference(Oracle):
             getattr(L, fn).argtypes = [d]
             getattr(L, fn).restype = d
         L.ref_save_checkpoint.argtypes = [vp, C.c_char_p, i32, vp, i32]
+        L.ref_write_pfm.argtypes = [C.c_char_p, vp, i32, i32, i32]
         L.ref_equal_assignment.argtypes = [i32, i32, vp, vp]
         L.ref_assign_rows.argtypes = [i32, i32, vp, vp, vp, d, vp, vp]
         L.ref_aggregate_stats.argtypes = [vp, i32, vp]
@@ -563,6 +564,12 @@ class Reference(Oracle):
         self._check(self.lib.ref_probe_prune(model.h, arr, len(cams), spp, k, res, alpha, _p(pm),
                                              _p(occ)))
         return pm, occ
+
+    def write_pfm(self, path, planar):
+        """The reference write_pfm (image.cpp:20-35) of a float32 [C, H, W] image."""
+        a = np.ascontiguousarray(planar, np.float32)
+        c, h, w = a.shape
+        self._check(self.lib.ref_write_pfm(str(path).encode(), _p(a), w, h, c))
 
     def save_checkpoint(self, model, path, spp=256, background=(0.0, 0.0, 0.0), contraction=1):
         """The reference save_checkpoint (scene.cpp:320-351) of a model."""

@@ -18,6 +18,7 @@
 #include "lumi/color.h"
 #include "lumi/field.h"
 #include "lumi/grid.h"
+#include "lumi/image.h"
 #include "lumi/occupancy.h"
 #include "lumi/renderer.h"
 #include "lumi/scene.h"
@@ -349,6 +350,15 @@ int ref_save_checkpoint(void* h, const char* path, int spp, const double* backgr
     Checkpoint ck{m.cfg, m.field, m.grid, {0.01, 0.02}, {background[0], background[1], background[2]},
                   contraction ? ContractionMode::kLInfCubic : ContractionMode::kNone, spp};
     save_checkpoint(ck, path);
+  });
+}
+
+// write_pfm (image.cpp:20-35) of a planar float image, for the PFM writer parity test.
+int ref_write_pfm(const char* path, const float* planar, int w, int h, int c) {
+  return guarded([&] {
+    Image<float> img(w, h, c);
+    std::memcpy(img.data.data(), planar, sizeof(float) * static_cast<size_t>(w) * h * c);
+    write_pfm(path, img);
   });
 }
 

@@ -3,7 +3,8 @@ rendering path.  See DESIGN.md.  The CUDA library is required (no CPU fallback).
 from ._abi import Error  # noqa: F401
 from .renderer import (CameraModel, ColorSpaceMode, ContractionMode, DeviceModel,  # noqa: F401
                        FieldConfig, HashGridConfig, Image, OccupancyGrid, RadianceField,
-                       RenderOptions, RowStats, device_info, load_checkpoint, render_rows)
+                       RenderOptions, RowStats, device_info, load_checkpoint, render_rows,
+                       save_checkpoint)
 from .scheduler import (FrameStats, RowRange, StatsSummary, WorkerAssignment,  # noqa: F401
                         aggregate_stats, assign_rows, equal_assignment, next_assignment,
                         run_frame)

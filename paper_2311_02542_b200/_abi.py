@@ -101,20 +101,29 @@ SIGNATURES = {
     "lumi_model_set_kernel": ([_vp, _i], C.c_int),
     "lumi_model_destroy": ([_vp], C.c_int),
     "lumi_model_bytes": ([_vp, _vp], C.c_int),
+    "lumi_model_device": ([_vp, _vp], C.c_int),
     "lumi_model_set_timing": ([_vp, _i], C.c_int),
     "lumi_model_take_timing": ([_vp, _vp, _vp, _vp], C.c_int),
     "lumi_render_rows": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp], C.c_int),
     "lumi_render_rows_async": ([_vp, _vp, _vp, _i, _i, _vp, _vp], C.c_int),
     "lumi_march_kept_async": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp], C.c_int),
+    "lumi_encode_async": ([_vp, _i, _vp, _vp, _vp, _vp], C.c_int),
     "lumi_gather_bench_async": ([_vp, _i, _i, _vp, _vp], C.c_int),
     "lumi_mlp_batch_async": ([_vp, _vp, _vp, _i, _vp, _vp], C.c_int),
     "lumi_checkpoint_read": ([C.c_char_p, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "lumi_checkpoint_write": ([C.c_char_p, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "lumi_bake_occupancy": ([_vp, _vp, _i, _i, _i, _i, _f, _vp, _vp], C.c_int),
     "lumi_train_backward_async": ([_vp, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp],
                                   C.c_int),
     "lumi_train_backward": ([_vp, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "lumi_model_device_params": ([_vp, _vp, _vp, _vp], C.c_int),
     "lumi_model_params_updated": ([_vp], C.c_int),
+    "lumi_frame_driver_create": ([_vp, _i, _i, _i, _i, _d, _vp], C.c_int),
+    "lumi_frame_driver_render": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "lumi_frame_driver_render_host": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "lumi_frame_driver_assignment": ([_vp, _vp, _vp], C.c_int),
+    "lumi_frame_driver_set_assignment": ([_vp, _vp], C.c_int),
+    "lumi_frame_driver_destroy": ([_vp], C.c_int),
     "lumi_ipc_export": ([_vp, _vp, _vp], C.c_int),
     "lumi_ipc_open": ([_i, _vp, _u64, _vp], C.c_int),
     "lumi_ipc_close": ([_i, _vp], C.c_int),

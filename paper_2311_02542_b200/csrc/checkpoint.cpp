@@ -1,5 +1,5 @@
-// checkpoint.cpp -- LUMICKPT v1 ingest (the on-disk model format feeding the render path):
-// proj/src/scene.cpp:286-394 (header, config, grid table, density / colour parameters,
+// checkpoint.cpp -- LUMICKPT v1 ingest and export (the on-disk model format feeding the render
+// path): proj/src/scene.cpp:286-394 (header, config, grid table, density / colour parameters,
 // per-camera vignetting) and proj/src/occupancy.cpp:200-243 (RLE occupancy bits + trackers).
 // Host-only; the parsed arrays go straight to lumi_model_create.
 #include <cstdint>
@@ -106,5 +106,76 @@ extern "C" int lumi_checkpoint_read(const char* path, LumiCheckpointInfo* info, 
   r.is.read(rest.data(), static_cast<std::streamsize>(rest.size()));
   if (!r.is) return err("occupancy: truncated stream");
   *info = ci;
+  return LUMI_OK;
+}
+
+namespace {
+struct Writer {
+  std::ofstream os;
+  template <typename T>
+  void put(const T& v) {
+    os.write(reinterpret_cast<const char*>(&v), sizeof(T));
+  }
+  void floats(const float* p, uint64_t n) {  // put_floats (scene.cpp:309-312)
+    put(n);
+    os.write(reinterpret_cast<const char*>(p), static_cast<std::streamsize>(n * sizeof(float)));
+  }
+};
+}  // namespace
+
+// save_checkpoint (scene.cpp:320-351) + OccupancyGrid::save (occupancy.cpp:200-222) of a
+// rendering model: training trackers (carved bytes, history, probe maxima) are written as zeros.
+extern "C" int lumi_checkpoint_write(const char* path, const LumiCheckpointInfo* info,
+                                     const float* table, const float* dparams, const float* cparams,
+                                     const double* alpha_v, const uint8_t* occupancy) {
+  if (!path || !info || !table || !dparams || !cparams || !occupancy)
+    return err("checkpoint: null argument");
+  LumiGridLayout lay;
+  int rc = lumi_field_layout(&info->field, &lay);
+  if (rc) return rc;
+  if (info->occ_res < 1 || info->occ_res > 1024) return err("occupancy: bad resolution");
+  if (info->n_cameras < 0) return err("checkpoint: bad camera count");
+  Writer w;
+  w.os.open(path, std::ios::binary);
+  if (!w.os.good()) return err(std::string("checkpoint: cannot write ") + path);
+  w.os.write("LUMICKPT", 8);
+  w.put<uint32_t>(1);
+  const LumiFieldDesc& f = info->field;
+  w.put<int32_t>(f.levels);
+  w.put<int32_t>(f.features_per_level);
+  w.put<int32_t>(f.base_resolution);
+  w.put<double>(f.per_level_scale);
+  w.put<uint32_t>(f.table_size);
+  w.put<int32_t>(f.hidden_width);
+  w.put<int32_t>(f.bottleneck);
+  w.put<uint8_t>(f.color_space == 0 ? 0 : 1);
+  w.put<uint8_t>(info->contraction == 1 ? 0 : 1);  // 0 = kLInfCubic in the file
+  w.put<int32_t>(info->samples_per_ray);
+  for (int k = 0; k < 3; ++k) w.put<double>(info->background[k]);
+  w.floats(table, lay.total_floats);
+  w.floats(dparams, lay.density_params);
+  w.floats(cparams, lay.color_params);
+  w.put<uint64_t>(static_cast<uint64_t>(info->n_cameras));
+  for (int k = 0; k < info->n_cameras; ++k) w.put<double>(alpha_v ? alpha_v[k] : 0.0);
+  const int32_t res = info->occ_res;
+  const uint64_t n = static_cast<uint64_t>(res) * res * res;
+  w.put<int32_t>(res);
+  std::vector<std::pair<uint8_t, uint64_t>> rle;
+  for (uint64_t i = 0; i < n;) {
+    const uint8_t v = occupancy[i] ? 1 : 0;
+    uint64_t len = 1;
+    while (i + len < n && (occupancy[i + len] ? 1 : 0) == v) ++len;
+    rle.emplace_back(v, len);
+    i += len;
+  }
+  w.put<uint64_t>(rle.size());
+  for (const auto& r : rle) {
+    w.put<uint8_t>(r.first);
+    w.put<uint64_t>(r.second);
+  }
+  const std::vector<char> zeros(n * (1 + 2 * sizeof(float)), 0);
+  w.os.write(zeros.data(), static_cast<std::streamsize>(zeros.size()));
+  w.os.flush();
+  if (!w.os.good()) return err(std::string("checkpoint: write failed ") + path);
   return LUMI_OK;
 }

@@ -115,6 +115,8 @@ cudaError_t launch_march_mask(const lumi_dev::RenderParams& p, cudaStream_t s);
 // public [pixel][word] kept mask through the production (filtered) march pass
 cudaError_t launch_march_public(lumi_dev::RenderParams p, uint32_t* mask, int32_t* counts,
                                 cudaStream_t s);
+cudaError_t launch_encode(const lumi_dev::GridDev& g, int n, const float* pos, const float* fl,
+                          float* out, cudaStream_t s);
 cudaError_t launch_gather_bench(const lumi_dev::GridDev& g, int n, int coherent, float* out,
                                 cudaStream_t s);
 cudaError_t launch_mlp_batch(const lumi_dev::MlpDev& mlp, const void* feat, const float* dirs, int n,

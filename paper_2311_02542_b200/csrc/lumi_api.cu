@@ -503,6 +503,12 @@ int lumi_model_bytes(const LumiModel* m, uint64_t* bytes) {
   return LUMI_OK;
 }
 
+int lumi_model_device(const LumiModel* m, int* device) {
+  if (!m || !device) return fail(LUMI_ERR_INVALID, "null argument");
+  *device = m->device;
+  return LUMI_OK;
+}
+
 int lumi_render_rows_async(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions* o,
                            int b, int e, const LumiFrameTarget* t, void* stream) {
   if (!m) return fail(LUMI_ERR_INVALID, "null model");
@@ -790,6 +796,28 @@ int lumi_gather_bench_async(LumiModel* m, int n, int coherent, float* out, void*
   if (rc) return rc;
   cudaError_t e = launch_gather_bench(rp.grid, n, coherent, out, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(LUMI_ERR_CUDA, std::string("gather_bench: ") + cudaGetErrorString(e));
+  return LUMI_OK;
+}
+
+int lumi_encode_async(LumiModel* m, int n, const float* pos, const float* lod, float* out,
+                      void* stream) {
+  if (!m) return fail(LUMI_ERR_INVALID, "null model");
+  if (n < 0 || (n > 0 && (!pos || !lod || !out))) return fail(LUMI_ERR_INVALID, "encode: bad buffers");
+  DeviceGuard dg(m->device);
+  RenderParams rp;
+  LumiCameraDesc dummy{};
+  dummy.rot[0] = dummy.rot[4] = dummy.rot[8] = 1.0;
+  dummy.fx = dummy.fy = 1.0;
+  dummy.width = dummy.height = 1;
+  dummy.t_near = 0.05;
+  dummy.t_far = 10.0;
+  LumiRenderOptions o{};
+  o.samples_per_ray = 2;
+  o.chunk_size = 32;
+  int rc = make_params(m, &dummy, &o, 0, 0, &rp);
+  if (rc) return rc;
+  cudaError_t e = launch_encode(rp.grid, n, pos, lod, out, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(LUMI_ERR_CUDA, std::string("encode: ") + cudaGetErrorString(e));
   return LUMI_OK;
 }
 

@@ -238,8 +238,44 @@ __global__ void __launch_bounds__(256) k_gather_bench(GridDev g, int n, int cohe
   out[i] = acc;
 }
 
+// The production encoding of n given samples (parity of the renderer's gather, grid.h:90-114):
+// contracted positions [n][3] -> u = saturate((c + 2) / 4) as the render kernel computes it,
+// LOD weights carried as fl (w_l = saturate(fl - l), the kernel's representation), every
+// active level through pk::gather_level -> features [n][2 * levels] fp32 (zeros for w_l = 0).
+__global__ void __launch_bounds__(256) k_encode(GridDev g, int n, const float* __restrict__ pos,
+                                                const float* __restrict__ fl,
+                                                float* __restrict__ out) {
+  __shared__ uint4 lvl[kMaxLevels];
+  for (int l = threadIdx.x; l < kMaxLevels; l += blockDim.x) {
+    const int res = l < g.levels ? g.res[l] : 1;
+    const unsigned long long base =
+        reinterpret_cast<unsigned long long>(g.table16 + (l < g.levels ? g.offset2[l] : 0));
+    lvl[l] = make_uint4((uint32_t)res, ((g.dense_mask >> l) & 1u) ? 0u : g.hash_mask[l],
+                        (uint32_t)base, (uint32_t)(base >> 32));
+  }
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float u = __saturatef((pos[3 * i] + 2.f) * 0.25f), v = __saturatef((pos[3 * i + 1] + 2.f) * 0.25f),
+              w = __saturatef((pos[3 * i + 2] + 2.f) * 0.25f);
+  const float f = fl[i];
+  for (int l = 0; l < g.levels; ++l) {
+    const float wl = __saturatef(f - (float)l);
+    const float2 r = wl > 0.f ? pk::gather_level(lvl[l], u, v, w, wl) : make_float2(0.f, 0.f);
+    out[(size_t)i * 2 * g.levels + 2 * l] = r.x;
+    out[(size_t)i * 2 * g.levels + 2 * l + 1] = r.y;
+  }
+}
+
 }  // namespace mb
 }  // namespace lumi_dev
+
+cudaError_t launch_encode(const lumi_dev::GridDev& g, int n, const float* pos, const float* fl,
+                          float* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  lumi_dev::mb::k_encode<<<(n + 255) / 256, 256, 0, s>>>(g, n, pos, fl, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gather_bench(const lumi_dev::GridDev& g, int n, int coherent, float* out,
                                 cudaStream_t s) {

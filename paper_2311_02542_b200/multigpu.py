@@ -14,16 +14,22 @@ the bands gathered to rank 0 over NVLink one of two ways:
   transfers (the bands are unequal, so an all-gather does not fit).
 
 With world size 1 the same driver renders the whole frame on one GPU with no collective.
+
+`NativeFrameDriver` is the single-process form behind the C ABI (lumi_frame_driver_*): one
+host thread per GPU inside liblumi_cuda.so, exactly the reference's run_frame shape
+(scheduler.cpp:114-162), for callers of the drop-in that do not run one process per GPU.
 """
 from __future__ import annotations
 
-from typing import List, Optional
+import ctypes as C
+from typing import List, Optional, Sequence
 
 import numpy as np
 
 from . import _abi, scenes
 from .renderer import CameraModel, DeviceModel, RenderOptions
-from .scheduler import FrameStats, WorkerAssignment, equal_assignment, next_assignment
+from .scheduler import (FrameStats, WorkerAssignment, _from_rows, equal_assignment,
+                        next_assignment)
 
 
 def eye_bands(begin: int, end: int, eye_size: int):
@@ -192,3 +198,64 @@ class StereoFrameDriver:
 
     def counters(self) -> Optional[np.ndarray]:
         return None if self.stats is None else self.stats.cpu().numpy()
+
+
+class NativeFrameDriver:
+    """run_frame + next_assignment inside the native library (lumi_frame_driver_*): worker i
+    renders with models[i] (one replica per GPU; a model may repeat to run several workers on
+    one GPU), one host thread per worker, every band stored straight into the device frame
+    target (over NVLink peer access from other GPUs).  `render` returns the FrameStats of the
+    frame and moves the assignment for the next one."""
+
+    def __init__(self, models: Sequence[DeviceModel], eye_size: int, eyes: int = 2,
+                 dampening: float = 0.5, width: Optional[int] = None):
+        L = _abi.lib()
+        self.models = list(models)  # keeps the replicas alive
+        self.n = len(self.models)
+        self.W = int(width or eye_size)
+        self.S, self.eyes = int(eye_size), int(eyes)
+        self.H = self.S * self.eyes
+        arr = (C.c_void_p * self.n)(*[m.h.value for m in self.models])
+        h = C.c_void_p()
+        _abi.check(L.lumi_frame_driver_create(arr, self.n, self.W, self.S, self.eyes,
+                                              float(dampening), C.byref(h)))
+        self.h = h
+
+    def assignment(self) -> WorkerAssignment:
+        import numpy as np
+        rows = np.zeros(self.n, np.int32)
+        shares = np.zeros(self.n, np.float64)
+        _abi.check(_abi.lib().lumi_frame_driver_assignment(self.h, rows.ctypes.data,
+                                                           shares.ctypes.data))
+        return _from_rows(rows, shares, self.H)
+
+    def set_assignment(self, rows: Sequence[int]) -> None:
+        import numpy as np
+        r = np.ascontiguousarray(rows, np.int32)
+        _abi.check(_abi.lib().lumi_frame_driver_set_assignment(self.h, r.ctypes.data))
+
+    def render(self, cams: Sequence[CameraModel], opts: RenderOptions,
+               target: _abi.FrameTarget) -> FrameStats:
+        import numpy as np
+        cd = (_abi.CameraDesc * self.eyes)(*[c.desc() for c in cams])
+        od = opts.desc()
+        wall = C.c_double()
+        ms = np.zeros(self.n, np.float64)
+        rays = np.zeros(self.n, np.int64)
+        rows_before = self.assignment()
+        _abi.check(_abi.lib().lumi_frame_driver_render(self.h, cd, C.byref(od), C.byref(target),
+                                                       C.byref(wall), ms.ctypes.data,
+                                                       rays.ctypes.data))
+        return FrameStats(wall_ms=float(wall.value), rays=rows_before.height * self.W,
+                          worker_ms=ms.tolist(), worker_rays=rays.tolist())
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            _abi.lib().lumi_frame_driver_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -371,6 +371,12 @@ class DeviceModel:
                                               C.c_void_p(dirs_ptr), int(n),
                                               C.c_void_p(out_ptr), C.c_void_p(stream)))
 
+    def encode_async(self, n: int, pos_ptr: int, lod_ptr: int, out_ptr: int, stream: int = 0) -> None:
+        """MultiResHashGrid::encode (grid.h:90-114) through the production gather: contracted
+        positions [n][3] fp32 and LOD fl [n] (w_l = clamp(fl - l, 0, 1)) -> [n][2*levels]."""
+        check(_abi.lib().lumi_encode_async(self.h, int(n), C.c_void_p(pos_ptr), C.c_void_p(lod_ptr),
+                                           C.c_void_p(out_ptr), C.c_void_p(stream)))
+
     def gather_bench_async(self, n: int, coherent: bool, out_ptr: int, stream: int = 0) -> None:
         """The renderer's hash-grid gather alone over n points x all levels (benchmark)."""
         check(_abi.lib().lumi_gather_bench_async(self.h, int(n), 1 if coherent else 0,
@@ -486,3 +492,22 @@ def load_checkpoint(path: str):
     meta = dict(samples_per_ray=info.samples_per_ray, background=tuple(info.background),
                 contraction=ContractionMode(info.contraction), n_cameras=info.n_cameras)
     return field, grid, meta
+
+
+def save_checkpoint(path: str, field: RadianceField, grid: OccupancyGrid,
+                    samples_per_ray: int = 256, background=(0.0, 0.0, 0.0),
+                    contraction: "ContractionMode" = ContractionMode.kLInfCubic,
+                    camera_alpha_v=()) -> None:
+    """save_checkpoint (proj/src/scene.cpp:320-351) of a rendering model in the reference's
+    LUMICKPT v1 format (the occupancy grid's training trackers are written as zeros)."""
+    info = _abi.CheckpointInfo()
+    info.field = field.cfg.desc()
+    info.samples_per_ray = int(samples_per_ray)
+    info.contraction = int(contraction)
+    info.background[:] = [float(v) for v in background]
+    info.occ_res = grid.res
+    av = np.ascontiguousarray(camera_alpha_v, np.float64)
+    info.n_cameras = int(av.size)
+    check(_abi.lib().lumi_checkpoint_write(str(path).encode(), C.byref(info), _p(field.grid_params),
+                                           _p(field.density_params), _p(field.color_params),
+                                           _p(av) if av.size else None, _p(grid.bits)))

@@ -13,6 +13,7 @@
 #include <sstream>
 #include <vector>
 
+#include "lumi/cuda_frame.h"
 #include "lumi/cuda_renderer.h"
 #include "lumi/scheduler.h"
 
@@ -130,6 +131,43 @@ int main(int argc, char** argv) {
     render_rows(field, grid, cam, opts, r.begin, r.end, &frame, nullptr, nullptr, nullptr);
   }, nullptr);
   CHECK(frame.data == gpu.data);
+
+  // the native multi-GPU frame driver (include/lumi/cuda_frame.h): three workers sharing this
+  // box's GPU render stereo frames; each frame equals the per-eye overload renders bit for
+  // bit, and the partition follows next_assignment on the measured per-worker times
+  {
+    const int S = 128;
+    CameraModel eye[2];
+    for (int e = 0; e < 2; ++e) {
+      eye[e] = cam;
+      eye[e].width = eye[e].height = S;
+      eye[e].fx = eye[e].fy = 0.6 * S;
+      eye[e].cx = eye[e].cy = S / 2.0;
+      eye[e].pose.origin.x += (e ? 0.032 : -0.032);
+    }
+    cuda::GpuFrameDriver drv(field, grid, {0, 0, 0}, S, S, 2);
+    for (int f = 0; f < 3; ++f) {
+      WorkerAssignment before = drv.assignment();
+      Image<float> stacked(S, 2 * S, 3);
+      FrameStats st = drv.render({eye[0], eye[1]}, opts, &stacked);
+      CHECK(st.worker_ms.size() == 3 && st.rays == 2 * S * S);
+      for (int e = 0; e < 2; ++e) {
+        Image<float> one(S, S, 3);
+        render_rows(field, grid, eye[e], opts, 0, S, &one, nullptr, nullptr, nullptr);
+        bool same = true;
+        for (int c = 0; c < 3; ++c)
+          for (int y = 0; y < S; ++y)
+            for (int x = 0; x < S; ++x) same &= one.at(x, y, c) == stacked.at(x, e * S + y, c);
+        CHECK(same);
+      }
+      WorkerAssignment want = next_assignment(before, st, 0.5);
+      WorkerAssignment got = drv.assignment();
+      for (int i = 0; i < 3; ++i) CHECK(got.ranges[i].begin == want.ranges[i].begin && got.ranges[i].end == want.ranges[i].end);
+      std::printf("frame driver frame %d: rows %d/%d/%d, worker ms %.3f/%.3f/%.3f\n", f,
+                  before.ranges[0].count(), before.ranges[1].count(), before.ranges[2].count(),
+                  st.worker_ms[0], st.worker_ms[1], st.worker_ms[2]);
+    }
+  }
 
   // error behaviour: lumi::Error on a bad row range, like the reference's require()
   bool threw = false;

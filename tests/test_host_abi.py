@@ -117,3 +117,39 @@ def test_checkpoint_ingest_matches_reference_writer(reference, tmp_path):
     bad.write_bytes(raw[: len(raw) - 100])
     with pytest.raises(L.Error, match="truncated"):
         L.load_checkpoint(bad)
+
+
+def test_checkpoint_writer_byte_identical_to_reference(reference, tmp_path):
+    """lumi_checkpoint_write (the product's save_checkpoint) produces the same bytes as the
+    reference's save_checkpoint (scene.cpp:320-351) for a rendering model (zero trackers)."""
+    cfg = O.field_config(table_size=1 << 12, base=16)
+    p = reference.synth_params(cfg, 9, 0.7)
+    rng = np.random.default_rng(4)
+    occ = (rng.random(24 ** 3) < 0.4).astype(np.uint8)
+    m = reference.model(p, occ, 24)
+    ref_path = tmp_path / "ref.lumickpt"
+    reference.save_checkpoint(m, ref_path, spp=128, background=(0.25, 0.5, 0.75), contraction=1)
+    f = L.RadianceField(L.FieldConfig(grid=L.HashGridConfig(table_size=1 << 12, base_resolution=16)))
+    f.grid_params[:] = p.table
+    f.density_params[:] = p.dparams
+    f.color_params[:] = p.cparams
+    ours = tmp_path / "ours.lumickpt"
+    L.save_checkpoint(ours, f, L.OccupancyGrid(24, occ), samples_per_ray=128,
+                      background=(0.25, 0.5, 0.75), camera_alpha_v=(0.01, 0.02))
+    assert ours.read_bytes() == ref_path.read_bytes()
+
+
+def test_pfm_writer_byte_identical_to_reference(reference, tmp_path):
+    """§8f row 3: the parity-artefact PFM writer (image.cpp:20-35) -- same bytes as the
+    reference's write_pfm, and read_pfm (image.cpp:36-66) round-trips them."""
+    from paper_2311_02542_b200.image_io import read_pfm, write_pfm
+    rng = np.random.default_rng(6)
+    for shape in ((3, 17, 23), (1, 8, 5)):
+        img = rng.standard_normal(shape).astype(np.float32)
+        ours, ref = tmp_path / "ours.pfm", tmp_path / "ref.pfm"
+        write_pfm(ours, img)
+        reference.write_pfm(ref, img)
+        assert ours.read_bytes() == ref.read_bytes()
+        assert np.array_equal(read_pfm(ours), img)
+    with pytest.raises(L.Error, match="1 or 3 channels"):
+        write_pfm(tmp_path / "x.pfm", np.zeros((2, 4, 4), np.float32))
