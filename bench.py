@@ -491,7 +491,7 @@ def run_ours(args):
                     "render_share_of_step": round(render_ms / max(elapsed, 1e-9), 4)},
         "work": {"evals_per_ray": round(evals / max(rays, 1), 3),
                  "active_levels_per_eval": round(level_samples / max(evals, 1), 3),
-                 "candidates_per_ray": round(candidates / max(rays, 1), 3)},
+                 "candidates_tested_per_ray": round(candidates / max(rays, 1), 3)},
         "roofline": {"bound": "hbm", "achieved": None if achieved is None else round(achieved, 1),
                      "peak": hbm, "unit": "GB/s",
                      "frac": None if achieved is None else round(achieved / hbm, 4),

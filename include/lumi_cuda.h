@@ -129,7 +129,8 @@ typedef struct LumiFrameTarget {
   int64_t* row_evals;
   uint8_t* srgb8; /* optional interleaved RGB8 display buffer (PQ -> sRGB epilogue) */
   /* optional device counters, accumulated (not reset): [0] network evaluations actually
-     executed, [1] active (w_l > 0) level-samples gathered, [2] candidates marched,
+     executed, [1] active (w_l > 0) level-samples gathered, [2] candidates the march pass
+     tested (empty-space skipping jumps the rest),
      [3] rays.  Used for the algorithmic-bytes roofline. */
   uint64_t* work_stats;
   double exposure_bias_stops;

@@ -172,18 +172,185 @@ __global__ void __launch_bounds__(128) k_march_mask_fast(RenderParams p) {
   if (idx < p.total_rays) p.kept_count[idx] = (uint16_t)count;
   add_work_stats(p, 0, 0, valid ? (unsigned long long)p.n : 0ull, 0);
 }
+
+// ---- empty-space skipping ------------------------------------------------------------------
+// The skip pass (production): the same certified per-candidate test, but a candidate decided
+// EMPTY lets the ray jump over every following candidate that provably lands in empty space.
+// occ_dist holds per voxel the Chebyshev voxel distance D to the nearest occupied voxel.  If
+// candidate i's exact voxel coordinate g_i lies in a voxel with distance D, every point whose
+// exact g is within L-inf distance < D - 1 of g_i lies in a voxel at most D - 1 away -- empty
+// (or outside the grid: free).  Along the ray |x_j - x_i|_inf <= |d|_inf (t_j - t_i); the
+// contraction (camera.cpp:34-49) is the identity inside the unit cube and 2/m-Lipschitz in L-inf
+// outside it (|x|_inf = m >= 1), so |g_j - g_i|_inf <= q Lip |d|_inf (t_j - t_i) with q = res/4,
+// Lip = 1 while the segment stays inside the cube, 2 / m_i once the ray has left it (m grows
+// along the ray after the exit: |o + d t|_inf is convex), 2 otherwise.  Candidates j with
+//   t_j < t_i + (D - 1) / (q Lip |d|_inf)      (shrunk by a relative 1e-3 + fp32 rounding slack)
+// are therefore empty and are not tested.  Decisions stay exact: the jump only skips
+// candidates the reference would also find empty; every tested candidate goes through the
+// certified fp32 test and, if undecided, the exact double re-test.
+__global__ void __launch_bounds__(128) k_march_skip(RenderParams p) {
+  extern __shared__ uint32_t s_bits[];  // [mask_words][128]: this CTA's kept bits
+  __shared__ double s_ts[kMaxSamples];
+  __shared__ float s_tf[kMaxSamples];
+  __shared__ double s_dir[4][32][3];  // per lane: exact direction (undecided re-tests)
+  constexpr int kQueue = 256;
+  __shared__ uint16_t s_queue[4][kQueue];  // per warp: undecided (lane, candidate)
+  __shared__ int s_qn[4];
+  for (int i = threadIdx.x; i < p.n; i += blockDim.x) {
+    s_ts[i] = p.ts[i];
+    s_tf[i] = (float)p.ts[i];
+  }
+  for (int i = threadIdx.x; i < p.mask_words * 128; i += blockDim.x) s_bits[i] = 0u;
+  if (threadIdx.x < 4) s_qn[threadIdx.x] = 0;
+  __syncthreads();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long idx = (long long)blockIdx.x * blockDim.x + tid;
+  int x = 0, y = 0;
+  const bool valid = idx < p.total_rays && ray_pixel(p, idx, x, y);
+  const d3 o{p.cam.origin[0], p.cam.origin[1], p.cam.origin[2]};
+  const d3 d = valid ? ray_dir(p.cam, (double)x + 0.5, (double)y + 0.5) : d3{0, 0, 1};
+  if (p.ray_dirs && idx < p.total_rays) store_ray_dirs(p, idx, valid, x, y, d);
+  s_dir[warp][lane][0] = d.x;
+  s_dir[warp][lane][1] = d.y;
+  s_dir[warp][lane][2] = d.z;
+  const float3 of = make_float3((float)o.x, (float)o.y, (float)o.z);
+  const float3 df = make_float3((float)d.x, (float)d.y, (float)d.z);
+  const float onorm = fabsf(of.x) + fabsf(of.y) + fabsf(of.z);
+  const InsideMarch im = inside_march_setup(p, of, df);
+  const float om = fmaxf(fabsf(of.x), fmaxf(fabsf(of.y), fabsf(of.z)));
+  // the ray's exit from the unit cube (origin inside): t_exit_hi bounds it from above (the
+  // inside fast path is pointless beyond), t_exit_lo from below (Lip = 1 before it)
+  float t_exit_hi = 3.4e38f, t_exit_lo = 0.f;
+  if (om < 1.f) {
+    float te = 3.4e38f;
+    const float dd[3] = {df.x, df.y, df.z}, oo[3] = {of.x, of.y, of.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (dd[a] != 0.f) te = fminf(te, ((dd[a] > 0.f ? 1.f : -1.f) - oo[a]) / dd[a]);
+    t_exit_hi = te * 1.001f + 1e-3f;
+    t_exit_lo = te * 0.999f - 1e-3f;
+  }
+  const float q = 0.25f * (float)p.occ_res;
+  const float dinf = fmaxf(fabsf(df.x), fmaxf(fabsf(df.y), fabsf(df.z))) * 1.0001f;
+  const bool contracted = p.contraction != 0;
+  // candidate index of a distance: k = (n - 1) log(t / t_near) / log(t_far / t_near)
+  const float k_scale = (float)(p.n - 1) / __logf(s_tf[p.n - 1] / s_tf[0]);
+  const float inv_tn = 1.f / s_tf[0];
+  int i = 0;
+  uint32_t tested = 0;
+  if (valid) {
+    while (i < p.n) {
+      const float tf = s_tf[i];
+      float m = 0.f;
+      int vi = tf < t_exit_hi ? voxel_inside(p, im, tf) : -2;
+      if (vi == -2) vi = voxel_filtered(p, of, df, onorm, tf, &m);
+      else m = om;  // inside the cube: |x| < 1
+      ++tested;
+      int D = 1;
+      if (vi >= 0) {
+        D = __ldg(p.occ_dist + vi);
+        if (D == 0) atomicOr(&s_bits[(i >> 5) * 128 + tid], 1u << (i & 31));
+      } else if (vi == -2) {  // undecided: the warp re-tests it exactly below
+        const int at = atomicAdd(&s_qn[warp], 1);
+        if (at < kQueue) {
+          s_queue[warp][at] = (uint16_t)(lane << 10 | i);
+        } else if (occupied(p, contract(ray_at(o, d, s_ts[i]), p.contraction))) {
+          atomicOr(&s_bits[(i >> 5) * 128 + tid], 1u << (i & 31));
+        }
+      }
+      int nxt = i + 1;
+      if (D >= 2) {
+        // Lipschitz bound of the contraction over [t_i, t_j] (see above)
+        float lip = 1.f;
+        if (contracted) lip = (om < 1.f && tf >= t_exit_hi && m >= 1.f) ? 2.f / m : 2.f;
+        float span = (float)(D - 1) / (q * dinf);
+        if (contracted && om < 1.f && tf + span < t_exit_lo) lip = 1.f;  // stays inside
+        span = span / lip * 0.999f;
+        const float t_lim = tf + span - 2.4e-7f * tf;
+        int j = (int)(__logf(t_lim * inv_tn) * k_scale);  // ~ the last candidate below t_lim
+        j = min(j, p.n - 1);
+        while (j > i && !(s_tf[j] < t_lim)) --j;
+        while (j + 1 < p.n && s_tf[j + 1] < t_lim) ++j;
+        nxt = max(i + 1, j + 1);
+      }
+      i = nxt;
+    }
+  }
+  __syncwarp();
+  // undecided candidates of the whole warp, re-tested in exact double one per lane
+  const int qn = min(s_qn[warp], kQueue);
+  for (int k = lane; k < qn; k += 32) {
+    const int e = s_queue[warp][k], ol = e >> 10, c = e & 1023;
+    const d3 od{s_dir[warp][ol][0], s_dir[warp][ol][1], s_dir[warp][ol][2]};
+    if (occupied(p, contract(ray_at(o, od, s_ts[c]), p.contraction)))
+      atomicOr(&s_bits[(c >> 5) * 128 + warp * 32 + ol], 1u << (c & 31));
+  }
+  __syncwarp();
+  if (idx < p.total_rays) {
+    int count = 0;
+    for (int w0 = 0; w0 < p.mask_words; ++w0) {
+      const uint32_t bits = s_bits[w0 * 128 + tid];
+      count += __popc(bits);
+      p.kept_mask[(size_t)w0 * p.total_rays + idx] = bits;
+    }
+    p.kept_count[idx] = (uint16_t)count;
+  }
+  add_work_stats(p, 0, 0, valid ? (unsigned long long)tested : 0ull, 0);
+}
+
+// Chebyshev distance transform of the occupancy grid, one axis per pass (separable:
+// min_o max_k |x_k - o_k| = min over o_1 of max(|x_1 - o_1|, min over o_2 of max(...))).
+// src: pass 0 the occupancy bytes (0 / nonzero), later passes the previous distances.
+__global__ void k_occ_distance(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int res,
+                               int axis, int first) {
+  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = (long long)res * res * res;
+  if (v >= n) return;
+  const long long stride = axis == 0 ? 1 : (axis == 1 ? res : (long long)res * res);
+  const int c = (int)((v / stride) % res);
+  const long long base = v - (long long)c * stride;
+  int best = 255;
+  for (int o = 0; o < res; ++o) {
+    const int dc = abs(o - c);
+    if (dc >= best) {
+      if (o > c) break;
+      continue;
+    }
+    const uint8_t s = __ldg(src + base + (long long)o * stride);
+    const int f = first ? (s ? 0 : 255) : (int)s;
+    best = min(best, max(dc, f));
+  }
+  dst[v] = (uint8_t)best;
+}
+
 }  // namespace march
 }  // namespace lumi_dev
 
 using namespace lumi_dev;
+
+cudaError_t launch_occ_distance(const uint8_t* occ, uint8_t* dist, uint8_t* scratch, int res,
+                                cudaStream_t s) {
+  const long long n = (long long)res * res * res;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  march::k_occ_distance<<<blocks, 256, 0, s>>>(occ, dist, res, 2, 1);
+  march::k_occ_distance<<<blocks, 256, 0, s>>>(dist, scratch, res, 1, 0);
+  march::k_occ_distance<<<blocks, 256, 0, s>>>(scratch, dist, res, 0, 0);
+  return cudaGetLastError();
+}
 // The exact march pass (k_march_mask) over p.total_rays tile-ordered ray ids
 // (p.tile_w x p.tile_h tiles) into p.kept_mask / p.kept_count.
 cudaError_t launch_march_mask(const RenderParams& p, cudaStream_t s) {
-  static const bool exact = std::getenv("LUMI_MARCH_EXACT") != nullptr;  // A/B and tests
+  // LUMI_MARCH_EXACT=1: the double-precision pass; LUMI_MARCH_NOSKIP=1: the certified fp32
+  // pass without empty-space skipping (A/B and tests)
+  static const bool exact = std::getenv("LUMI_MARCH_EXACT") != nullptr;
+  static const bool noskip = std::getenv("LUMI_MARCH_NOSKIP") != nullptr;
+  const unsigned blocks = (unsigned)((p.total_rays + 127) / 128);
   if (exact)
-    march::k_march_mask<<<(unsigned)((p.total_rays + 127) / 128), 128, 0, s>>>(p);
+    march::k_march_mask<<<blocks, 128, 0, s>>>(p);
+  else if (noskip || !p.occ_dist)
+    march::k_march_mask_fast<<<blocks, 128, 0, s>>>(p);
   else
-    march::k_march_mask_fast<<<(unsigned)((p.total_rays + 127) / 128), 128, 0, s>>>(p);
+    march::k_march_skip<<<blocks, 128, (size_t)p.mask_words * 128 * sizeof(uint32_t), s>>>(p);
   return cudaGetLastError();
 }
 

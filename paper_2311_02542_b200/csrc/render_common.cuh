@@ -14,6 +14,9 @@ struct RenderParams {
   GridDev grid;
   MlpDev mlp;
   const uint8_t* occ;  // occ_res^3 bytes
+  // per voxel the Chebyshev (L-inf) voxel distance to the nearest occupied voxel, clamped at
+  // 255 (0 = occupied): the march pass's empty-space skip
+  const uint8_t* occ_dist;
   int occ_res;
   const double* ts;    // host-computed exponential distances (renderer.h:135-141)
   double ratio;        // host-computed pow(t_far/t_near, 1/(n-1)) (renderer.h:142)
@@ -162,11 +165,14 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-__device__ __forceinline__ int occupied_filtered(const RenderParams& p, float3 of, float3 df,
-                                                 float onorm, float tf) {
+// The certified fp32 voxel of one candidate (see above): its voxel index (>= 0), -1 when it is
+// certainly outside the grid's domain (free), -2 when fp32 cannot decide.  *m_out gets |x|_inf.
+__device__ __forceinline__ int voxel_filtered(const RenderParams& p, float3 of, float3 df, float onorm,
+                                              float tf, float* m_out = nullptr) {
   const float x = fmaf(df.x, tf, of.x), y = fmaf(df.y, tf, of.y), z = fmaf(df.z, tf, of.z);
   const float ax = fabsf(x), ay = fabsf(y), az = fabsf(z);
   const float m = fmaxf(ax, fmaxf(ay, az));
+  if (m_out) *m_out = m;
   const float ex = 4.76837158e-07f * (onorm + tf);  // 8 * 2^-24 * (|o| + t)
   const bool contract = p.contraction != 0 && m > 1.f;
   const float inv = contract ? rcp_approx(m) : 1.f;  // ~1 ulp, inside the 2^-21 term
@@ -188,13 +194,21 @@ __device__ __forceinline__ int occupied_filtered(const RenderParams& p, float3 o
   const float rx = __fsub_rn(__fadd_rn(gx, kMagic), kMagic), ry = __fsub_rn(__fadd_rn(gy, kMagic), kMagic),
               rz = __fsub_rn(__fadd_rn(gz, kMagic), kMagic);
   const float dmin = fminf(fabsf(gx - rx), fminf(fabsf(gy - ry), fabsf(gz - rz)));
-  if (dmin <= eps || (contract && m - m2 <= 4.f * ex)) return 2;
-  if (fminf(gx, fminf(gy, gz)) < 0.f || fmaxf(gx, fmaxf(gy, gz)) > res) return 0;
+  if (dmin <= eps || (contract && m - m2 <= 4.f * ex)) return -2;
+  if (fminf(gx, fminf(gy, gz)) < 0.f || fmaxf(gx, fmaxf(gy, gz)) > res) return -1;
   const uint32_t r = (uint32_t)p.occ_res;  // res^3 < 2^32 (checked on the host)
   const uint32_t ix = (uint32_t)(__float_as_int(__fadd_rn(gx - 0.5f, kMagic)) - 0x4B400000),
                  iy = (uint32_t)(__float_as_int(__fadd_rn(gy - 0.5f, kMagic)) - 0x4B400000),
                  iz = (uint32_t)(__float_as_int(__fadd_rn(gz - 0.5f, kMagic)) - 0x4B400000);
-  return __ldg(p.occ + ((iz * r + iy) * r + ix)) != 0 ? 1 : 0;
+  return (int)((iz * r + iy) * r + ix);
+}
+
+// Returns 0 (empty), 1 (occupied) or 2 (undecided in fp32).
+__device__ __forceinline__ int occupied_filtered(const RenderParams& p, float3 of, float3 df,
+                                                 float onorm, float tf) {
+  const int vi = voxel_filtered(p, of, df, onorm, tf);
+  if (vi == -2) return 2;
+  return vi >= 0 && __ldg(p.occ + vi) != 0 ? 1 : 0;
 }
 
 
@@ -226,8 +240,8 @@ __device__ __forceinline__ InsideMarch inside_march_setup(const RenderParams& p,
   return m;
 }
 
-// 0 / 1: decided (empty / occupied); -1: use occupied_filtered
-__device__ __forceinline__ int occupied_inside(const RenderParams& p, const InsideMarch& m, float tf) {
+// voxel index (>= 0) when certified strictly inside the unit cube; -2: use voxel_filtered
+__device__ __forceinline__ int voxel_inside(const RenderParams& p, const InsideMarch& m, float tf) {
   const float gx = fmaf(m.g1.x, tf, m.g0.x), gy = fmaf(m.g1.y, tf, m.g0.y), gz = fmaf(m.g1.z, tf, m.g0.z);
   const float eps = fmaf(m.e1, tf, m.e0);
   constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: rint on the FMA pipe
@@ -235,12 +249,18 @@ __device__ __forceinline__ int occupied_inside(const RenderParams& p, const Insi
               rz = __fsub_rn(__fadd_rn(gz, kMagic), kMagic);
   const float dmin = fminf(fabsf(gx - rx), fminf(fabsf(gy - ry), fabsf(gz - rz)));
   const float gmin = fminf(gx, fminf(gy, gz)), gmax = fmaxf(gx, fmaxf(gy, gz));
-  if (!(dmin > eps && gmin - eps > m.qlo && gmax + eps < m.qhi)) return -1;
+  if (!(dmin > eps && gmin - eps > m.qlo && gmax + eps < m.qhi)) return -2;
   const uint32_t r = (uint32_t)p.occ_res;
   const uint32_t ix = (uint32_t)(__float_as_int(__fadd_rn(gx - 0.5f, kMagic)) - 0x4B400000),
                  iy = (uint32_t)(__float_as_int(__fadd_rn(gy - 0.5f, kMagic)) - 0x4B400000),
                  iz = (uint32_t)(__float_as_int(__fadd_rn(gz - 0.5f, kMagic)) - 0x4B400000);
-  return __ldg(p.occ + ((iz * r + iy) * r + ix)) != 0 ? 1 : 0;
+  return (int)((iz * r + iy) * r + ix);
+}
+
+// 0 / 1: decided (empty / occupied); -1: use occupied_filtered
+__device__ __forceinline__ int occupied_inside(const RenderParams& p, const InsideMarch& m, float tf) {
+  const int vi = voxel_inside(p, m, tf);
+  return vi < 0 ? -1 : (__ldg(p.occ + vi) != 0 ? 1 : 0);
 }
 
 }  // namespace lumi_dev

@@ -388,7 +388,6 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
             r.nd = make_float3((float)nn.x, (float)nn.y, (float)nn.z);
 #endif
             ++cnt.rays;
-            cnt.marched += p.n;
           }
           r.contributing = 0;
           r.term = false;
@@ -709,8 +708,7 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
   // streams never share it)
   if ((e = cudaMallocAsync(&p.work_counter, 256, s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(p.work_counter, 0, sizeof(unsigned int), s)) != cudaSuccess) return e;
-  RenderParams pm = p;
-  pm.work_stats = nullptr;
+  RenderParams pm = p;  // the march pass counts the candidates it tests (work_stats[2])
   if (ev) cudaEventRecord(ev[0], s);
   if ((e = launch_march_mask(pm, s)) != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[1], s);
