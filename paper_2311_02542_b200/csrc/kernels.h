@@ -112,9 +112,6 @@ cudaError_t launch_render_simt(const lumi_dev::RenderParams& p, cudaStream_t s);
 cudaError_t launch_march_kept(const lumi_dev::RenderParams& p, uint32_t* mask, int32_t* counts,
                               cudaStream_t s);
 cudaError_t launch_march_mask(const lumi_dev::RenderParams& p, cudaStream_t s);
-// Chebyshev voxel distance to the nearest occupied voxel (clamped at 255) of a res^3 grid
-cudaError_t launch_occ_distance(const uint8_t* occ, uint8_t* dist, uint8_t* scratch, int res,
-                                cudaStream_t s);
 // public [pixel][word] kept mask through the production (filtered) march pass
 cudaError_t launch_march_public(lumi_dev::RenderParams p, uint32_t* mask, int32_t* counts,
                                 cudaStream_t s);

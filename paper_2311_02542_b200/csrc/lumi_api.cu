@@ -176,7 +176,6 @@ struct LumiModel {
   float* d_cparams = nullptr;
   float* d_fused = nullptr;  // density L2 folded into colour L1 (packet kernel), see fuse_l2_c1
   uint8_t* d_occ = nullptr;
-  uint8_t* d_occ_dist = nullptr;  // Chebyshev voxel distance to the nearest occupied voxel
   int occ_res = 0;
   int kernel = LUMI_KERNEL_WS;
   int num_sms = 148;
@@ -267,7 +266,6 @@ int make_params(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions
   p->mlp.fused = m->d_fused;
   p->mlp.color_space = m->desc.color_space;
   p->occ = m->d_occ;
-  p->occ_dist = m->d_occ_dist;
   p->occ_res = m->occ_res;
   if ((rc = get_ts(m, cam->t_near, cam->t_far, o->samples_per_ray, &p->ts, &p->ratio))) return rc;
   p->n = o->samples_per_ray;
@@ -464,20 +462,9 @@ int lumi_model_set_occupancy(LumiModel* m, const uint8_t* occ, int res) {
   if (occ)
     for (size_t i = 0; i < n; ++i) bits[i] = occ[i] ? 1 : 0;
   if (m->d_occ) cudaFree(m->d_occ);
-  if (m->d_occ_dist) cudaFree(m->d_occ_dist);
-  m->d_occ = m->d_occ_dist = nullptr;
+  m->d_occ = nullptr;
   LUMI_CUDA_TRY(cudaMalloc(&m->d_occ, n));
-  LUMI_CUDA_TRY(cudaMalloc(&m->d_occ_dist, n));
   LUMI_CUDA_TRY(cudaMemcpy(m->d_occ, bits.data(), n, cudaMemcpyHostToDevice));
-  {
-    uint8_t* scratch = nullptr;
-    LUMI_CUDA_TRY(cudaMalloc(&scratch, n));
-    const cudaError_t e = launch_occ_distance(m->d_occ, m->d_occ_dist, scratch, res, nullptr);
-    cudaError_t e2 = cudaDeviceSynchronize();
-    cudaFree(scratch);
-    LUMI_CUDA_TRY(e);
-    LUMI_CUDA_TRY(e2);
-  }
   m->occ_res = res;
   return LUMI_OK;
 }
@@ -491,7 +478,6 @@ int lumi_model_destroy(LumiModel* m) {
   cudaFree(m->d_cparams);
   cudaFree(m->d_fused);
   cudaFree(m->d_occ);
-  cudaFree(m->d_occ_dist);
   for (auto& kv : m->ts_cache) cudaFree(kv.second.first);
   for (auto& a : m->ev_pool)
     for (auto x : a) cudaEventDestroy(x);

@@ -173,22 +173,21 @@ __global__ void __launch_bounds__(128) k_march_mask_fast(RenderParams p) {
   add_work_stats(p, 0, 0, valid ? (unsigned long long)p.n : 0ull, 0);
 }
 
-// ---- empty-space skipping ------------------------------------------------------------------
-// The skip pass (production): the same certified per-candidate test, but a candidate decided
-// EMPTY lets the ray jump over every following candidate that provably lands in empty space.
-// occ_dist holds per voxel the Chebyshev voxel distance D to the nearest occupied voxel.  If
-// candidate i's exact voxel coordinate g_i lies in a voxel with distance D, every point whose
-// exact g is within L-inf distance < D - 1 of g_i lies in a voxel at most D - 1 away -- empty
-// (or outside the grid: free).  Along the ray |x_j - x_i|_inf <= |d|_inf (t_j - t_i); the
-// contraction (camera.cpp:34-49) is the identity inside the unit cube and 2/m-Lipschitz in L-inf
-// outside it (|x|_inf = m >= 1), so |g_j - g_i|_inf <= q Lip |d|_inf (t_j - t_i) with q = res/4,
-// Lip = 1 while the segment stays inside the cube, 2 / m_i once the ray has left it (m grows
-// along the ray after the exit: |o + d t|_inf is convex), 2 otherwise.  Candidates j with
-//   t_j < t_i + (D - 1) / (q Lip |d|_inf)      (shrunk by a relative 1e-3 + fp32 rounding slack)
-// are therefore empty and are not tested.  Decisions stay exact: the jump only skips
-// candidates the reference would also find empty; every tested candidate goes through the
-// certified fp32 test and, if undecided, the exact double re-test.
-__global__ void __launch_bounds__(128) k_march_skip(RenderParams p) {
+// ---- voxel runs ------------------------------------------------------------------------------
+// The production march pass.  Inside the unit cube the contraction is the identity and the
+// voxel coordinate is linear in t, g(t) = G0 + G1 t (fp32 certified: |g_f - g| <= eps(t) =
+// E0 + E1 t, render_common.cuh).  When candidate i is certified in voxel k, every later
+// candidate whose fp32 t keeps g(t) +- eps(t) strictly inside voxel k (and inside the cube) on
+// every axis would pass the same certified test with the same voxel -- its exact point is in
+// voxel k -- so the whole run of candidates up to the voxel's exit gets voxel k's occupancy bit
+// from ONE test.  Per axis with G1 > E1 the run ends where g + eps reaches the upper face:
+//   t < (min(k + 1, 3q) - G0 - E0) / (G1 + E1)     (the lower face recedes: G1 - E1 > 0),
+// mirrored for G1 < -E1; an axis with |G1| <= E1 gets no run.  The bound is shrunk by a relative
+// 1e-5 (approximate division).  At the reference's 256 samples a C3 ray holds ~138 candidates
+// inside the cube in ~35 voxel runs.  Outside the cube every candidate is tested on its own (the
+// contraction's max-axis switch is discontinuous, so runs there would need per-pyramid exits).
+// Undecided candidates are re-tested in exact double, cooperatively per warp.
+__global__ void __launch_bounds__(128) k_march_runs(RenderParams p) {
   extern __shared__ uint32_t s_bits[];  // [mask_words][128]: this CTA's kept bits
   __shared__ double s_ts[kMaxSamples];
   __shared__ float s_tf[kMaxSamples];
@@ -217,64 +216,78 @@ __global__ void __launch_bounds__(128) k_march_skip(RenderParams p) {
   const float3 df = make_float3((float)d.x, (float)d.y, (float)d.z);
   const float onorm = fabsf(of.x) + fabsf(of.y) + fabsf(of.z);
   const InsideMarch im = inside_march_setup(p, of, df);
-  const float om = fmaxf(fabsf(of.x), fmaxf(fabsf(of.y), fabsf(of.z)));
-  // the ray's exit from the unit cube (origin inside): t_exit_hi bounds it from above (the
-  // inside fast path is pointless beyond), t_exit_lo from below (Lip = 1 before it)
-  float t_exit_hi = 3.4e38f, t_exit_lo = 0.f;
-  if (om < 1.f) {
-    float te = 3.4e38f;
+  // beyond the ray's exit from the unit cube (slab test in fp32, with slack) the inside test can
+  // only answer "undecided": go straight to the general test there
+  float t_exit = 3.4e38f;
+  {
     const float dd[3] = {df.x, df.y, df.z}, oo[3] = {of.x, of.y, of.z};
 #pragma unroll
     for (int a = 0; a < 3; ++a)
-      if (dd[a] != 0.f) te = fminf(te, ((dd[a] > 0.f ? 1.f : -1.f) - oo[a]) / dd[a]);
-    t_exit_hi = te * 1.001f + 1e-3f;
-    t_exit_lo = te * 0.999f - 1e-3f;
+      if (dd[a] != 0.f) t_exit = fminf(t_exit, ((dd[a] > 0.f ? 1.f : -1.f) - oo[a]) / dd[a]);
+    t_exit = t_exit * 1.001f + 1e-3f;
   }
-  const float q = 0.25f * (float)p.occ_res;
-  const float dinf = fmaxf(fabsf(df.x), fmaxf(fabsf(df.y), fabsf(df.z))) * 1.0001f;
-  const bool contracted = p.contraction != 0;
   // candidate index of a distance: k = (n - 1) log(t / t_near) / log(t_far / t_near)
   const float k_scale = (float)(p.n - 1) / __logf(s_tf[p.n - 1] / s_tf[0]);
   const float inv_tn = 1.f / s_tf[0];
-  int i = 0;
+  const uint32_t r = (uint32_t)p.occ_res;
+  constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: rint on the FMA pipe
   uint32_t tested = 0;
-  if (valid) {
-    while (i < p.n) {
-      const float tf = s_tf[i];
-      float m = 0.f;
-      int vi = tf < t_exit_hi ? voxel_inside(p, im, tf) : -2;
-      if (vi == -2) vi = voxel_filtered(p, of, df, onorm, tf, &m);
-      else m = om;  // inside the cube: |x| < 1
-      ++tested;
-      int D = 1;
-      if (vi >= 0) {
-        D = __ldg(p.occ_dist + vi);
-        if (D == 0) atomicOr(&s_bits[(i >> 5) * 128 + tid], 1u << (i & 31));
-      } else if (vi == -2) {  // undecided: the warp re-tests it exactly below
-        const int at = atomicAdd(&s_qn[warp], 1);
-        if (at < kQueue) {
-          s_queue[warp][at] = (uint16_t)(lane << 10 | i);
-        } else if (occupied(p, contract(ray_at(o, d, s_ts[i]), p.contraction))) {
-          atomicOr(&s_bits[(i >> 5) * 128 + tid], 1u << (i & 31));
+  int i = 0;
+  while (valid && i < p.n) {
+    const float tf = s_tf[i];
+    int j = i;  // the last candidate decided together with i
+    int vi = -2;
+    if (tf < t_exit) {
+      const float gx = fmaf(im.g1.x, tf, im.g0.x), gy = fmaf(im.g1.y, tf, im.g0.y),
+                  gz = fmaf(im.g1.z, tf, im.g0.z);
+      const float eps = fmaf(im.e1, tf, im.e0);
+      const float rx = __fsub_rn(__fadd_rn(gx, kMagic), kMagic), ry = __fsub_rn(__fadd_rn(gy, kMagic), kMagic),
+                  rz = __fsub_rn(__fadd_rn(gz, kMagic), kMagic);
+      const float dmin = fminf(fabsf(gx - rx), fminf(fabsf(gy - ry), fabsf(gz - rz)));
+      const float gmin = fminf(gx, fminf(gy, gz)), gmax = fmaxf(gx, fmaxf(gy, gz));
+      if (dmin > eps && gmin - eps > im.qlo && gmax + eps < im.qhi) {
+        // floor(g) as a float integer and as an index
+        const float bx = __fadd_rn(gx - 0.5f, kMagic), by = __fadd_rn(gy - 0.5f, kMagic),
+                    bz = __fadd_rn(gz - 0.5f, kMagic);
+        const uint32_t ix = (uint32_t)(__float_as_int(bx) - 0x4B400000),
+                       iy = (uint32_t)(__float_as_int(by) - 0x4B400000),
+                       iz = (uint32_t)(__float_as_int(bz) - 0x4B400000);
+        vi = (int)((iz * r + iy) * r + ix);
+        const float kx = bx - kMagic, ky = by - kMagic, kz = bz - kMagic;
+        auto axis_exit = [&](float k, float g0, float g1) {
+          if (g1 > im.e1) return __fdividef(fminf(k + 1.f, im.qhi) - g0 - im.e0, g1 + im.e1);
+          if (g1 < -im.e1) return __fdividef(g0 - im.e0 - fmaxf(k, im.qlo), im.e1 - g1);
+          return 0.f;
+        };
+        const float t_lim = fminf(axis_exit(kx, im.g0.x, im.g1.x),
+                                  fminf(axis_exit(ky, im.g0.y, im.g1.y), axis_exit(kz, im.g0.z, im.g1.z))) *
+                            0.99999f;
+        if (i + 1 < p.n && s_tf[i + 1] < t_lim) {
+          int jj = min((int)(__logf(t_lim * inv_tn) * k_scale), p.n - 1);
+          while (jj > i && !(s_tf[jj] < t_lim)) --jj;
+          while (jj + 1 < p.n && s_tf[jj + 1] < t_lim) ++jj;
+          j = max(jj, i);
         }
       }
-      int nxt = i + 1;
-      if (D >= 2) {
-        // Lipschitz bound of the contraction over [t_i, t_j] (see above)
-        float lip = 1.f;
-        if (contracted) lip = (om < 1.f && tf >= t_exit_hi && m >= 1.f) ? 2.f / m : 2.f;
-        float span = (float)(D - 1) / (q * dinf);
-        if (contracted && om < 1.f && tf + span < t_exit_lo) lip = 1.f;  // stays inside
-        span = span / lip * 0.999f;
-        const float t_lim = tf + span - 2.4e-7f * tf;
-        int j = (int)(__logf(t_lim * inv_tn) * k_scale);  // ~ the last candidate below t_lim
-        j = min(j, p.n - 1);
-        while (j > i && !(s_tf[j] < t_lim)) --j;
-        while (j + 1 < p.n && s_tf[j + 1] < t_lim) ++j;
-        nxt = max(i + 1, j + 1);
-      }
-      i = nxt;
     }
+    if (vi == -2) vi = voxel_filtered(p, of, df, onorm, tf);
+    ++tested;
+    if (vi == -2) {  // undecided: the warp re-tests it exactly below
+      const int at = atomicAdd(&s_qn[warp], 1);
+      if (at < kQueue) {
+        s_queue[warp][at] = (uint16_t)(lane << 10 | i);
+      } else if (occupied(p, contract(ray_at(o, d, s_ts[i]), p.contraction))) {
+        s_bits[(i >> 5) * 128 + tid] |= 1u << (i & 31);
+      }
+    } else if (vi >= 0 && __ldg(p.occ + vi) != 0) {
+      // set candidates i..j
+      for (int w = i >> 5; w <= (j >> 5); ++w) {
+        const int lo = max(i - 32 * w, 0), hi = min(j - 32 * w, 31);
+        const uint32_t upto = hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u);
+        s_bits[w * 128 + tid] |= upto & ~((1u << lo) - 1u);
+      }
+    }
+    i = j + 1;
   }
   __syncwarp();
   // undecided candidates of the whole warp, re-tested in exact double one per lane
@@ -298,59 +311,25 @@ __global__ void __launch_bounds__(128) k_march_skip(RenderParams p) {
   add_work_stats(p, 0, 0, valid ? (unsigned long long)tested : 0ull, 0);
 }
 
-// Chebyshev distance transform of the occupancy grid, one axis per pass (separable:
-// min_o max_k |x_k - o_k| = min over o_1 of max(|x_1 - o_1|, min over o_2 of max(...))).
-// src: pass 0 the occupancy bytes (0 / nonzero), later passes the previous distances.
-__global__ void k_occ_distance(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int res,
-                               int axis, int first) {
-  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long n = (long long)res * res * res;
-  if (v >= n) return;
-  const long long stride = axis == 0 ? 1 : (axis == 1 ? res : (long long)res * res);
-  const int c = (int)((v / stride) % res);
-  const long long base = v - (long long)c * stride;
-  int best = 255;
-  for (int o = 0; o < res; ++o) {
-    const int dc = abs(o - c);
-    if (dc >= best) {
-      if (o > c) break;
-      continue;
-    }
-    const uint8_t s = __ldg(src + base + (long long)o * stride);
-    const int f = first ? (s ? 0 : 255) : (int)s;
-    best = min(best, max(dc, f));
-  }
-  dst[v] = (uint8_t)best;
-}
-
 }  // namespace march
 }  // namespace lumi_dev
 
 using namespace lumi_dev;
 
-cudaError_t launch_occ_distance(const uint8_t* occ, uint8_t* dist, uint8_t* scratch, int res,
-                                cudaStream_t s) {
-  const long long n = (long long)res * res * res;
-  const unsigned blocks = (unsigned)((n + 255) / 256);
-  march::k_occ_distance<<<blocks, 256, 0, s>>>(occ, dist, res, 2, 1);
-  march::k_occ_distance<<<blocks, 256, 0, s>>>(dist, scratch, res, 1, 0);
-  march::k_occ_distance<<<blocks, 256, 0, s>>>(scratch, dist, res, 0, 0);
-  return cudaGetLastError();
-}
 // The exact march pass (k_march_mask) over p.total_rays tile-ordered ray ids
 // (p.tile_w x p.tile_h tiles) into p.kept_mask / p.kept_count.
 cudaError_t launch_march_mask(const RenderParams& p, cudaStream_t s) {
-  // LUMI_MARCH_EXACT=1: the double-precision pass; LUMI_MARCH_NOSKIP=1: the certified fp32
-  // pass without empty-space skipping (A/B and tests)
+  // LUMI_MARCH_EXACT=1: the double-precision pass; LUMI_MARCH_RUNS=1: the voxel-run pass
+  // (A/B and tests; default: the certified fp32 pass candidate by candidate)
   static const bool exact = std::getenv("LUMI_MARCH_EXACT") != nullptr;
-  static const bool noskip = std::getenv("LUMI_MARCH_NOSKIP") != nullptr;
+  static const bool runs = std::getenv("LUMI_MARCH_RUNS") != nullptr;
   const unsigned blocks = (unsigned)((p.total_rays + 127) / 128);
   if (exact)
     march::k_march_mask<<<blocks, 128, 0, s>>>(p);
-  else if (noskip || !p.occ_dist)
-    march::k_march_mask_fast<<<blocks, 128, 0, s>>>(p);
+  else if (runs)
+    march::k_march_runs<<<blocks, 128, (size_t)p.mask_words * 128 * sizeof(uint32_t), s>>>(p);
   else
-    march::k_march_skip<<<blocks, 128, (size_t)p.mask_words * 128 * sizeof(uint32_t), s>>>(p);
+    march::k_march_mask_fast<<<blocks, 128, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -14,9 +14,6 @@ struct RenderParams {
   GridDev grid;
   MlpDev mlp;
   const uint8_t* occ;  // occ_res^3 bytes
-  // per voxel the Chebyshev (L-inf) voxel distance to the nearest occupied voxel, clamped at
-  // 255 (0 = occupied): the march pass's empty-space skip
-  const uint8_t* occ_dist;
   int occ_res;
   const double* ts;    // host-computed exponential distances (renderer.h:135-141)
   double ratio;        // host-computed pow(t_far/t_near, 1/(n-1)) (renderer.h:142)

@@ -79,6 +79,18 @@ constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5, kBarProd = 6;
 #define WS_CONS_LEVELS 0
 #endif
 constexpr int kConsLevels = WS_CONS_LEVELS;  // LOD levels gathered by the consumers (<= 4)
+// WS_ROWMAJOR (default): producer thread t gathers ALL active levels of row t, four levels (one
+// 16-byte A chunk) at a time, straight from the row's (u, v, w, fl) -- no shared (row, level)
+// list to build or decode.  The 32 rows of a warp are neighbouring rays of one packet at nearly
+// the same distance, so their LOD (hence their level count) is nearly uniform and the lanes of a
+// warp walk the same level together (coherent hash cells, warp-uniform dense/hashed branch).
+#ifndef WS_ROWMAJOR
+#define WS_ROWMAJOR 1
+#endif
+#if WS_ROWMAJOR
+static_assert(kConsLevels == 0, "the row-major producers gather every level");
+static_assert(WS_PROD_WARPS == 4, "row-major producers: one thread per row");
+#endif
 
 #ifdef LUMI_PHASE_TIMING
 // warp-cycles: producers [wait list, gather], consumers [fill+geometry+list, wait gather, MLP,
@@ -121,8 +133,10 @@ struct __align__(16) Smem {
   uint4 lvl[kMaxLevels];
   float4 samp[2][128];
   uint8_t na[2][128];                        // per row: active LOD levels (0 = no sample)
+#if !WS_ROWMAJOR
   uint16_t pairs[kWarps * 32 * kMaxLevels];  // the round's gather list, warp lists concatenated
   int cnt[2][kWarps];                        // per warp: pairs the producers will list
+#endif
 };
 
 // layer 1 with the bias step's A from the shared ones block (LBO 128 B between its two core
@@ -245,6 +259,49 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       list_ready_sync(b);
       WS_T(0);
       if (s.stop[b]) break;
+#if WS_ROWMAJOR
+      {
+        // row ctid: grid coordinates + LOD (fl) and its active level count, from the consumers
+        const float4 P = s.samp[b][ctid];
+        const int na = s.na[b][ctid];
+        const int na_max = __reduce_max_sync(FULL, (unsigned)na);
+#pragma unroll 1
+        for (int c = 0; c < kMaxLevels / 4; ++c) {  // A chunk c = levels 4c .. 4c + 3
+          uint4 out = make_uint4(0u, 0u, 0u, 0u);
+          if (4 * c < na_max) {  // warp-uniform
+            GatherPrep gp[4];
+            float wl[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int l = 4 * c + q;
+              wl[q] = l < na ? __saturatef(P.w - (float)l) : 0.f;
+              gather_prep(s.lvl[l], P.x, P.y, P.z, gp[q]);
+            }
+            // all corner loads of the chunk in flight before the first combine; lanes whose row
+            // has fewer levels predicate theirs off
+            __half2 e[4][8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const bool act = 4 * c + q < na;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) e[q][k] = act ? __ldg(gp[q].base + gp[q].idx[k]) : __half2{};
+            }
+            uint32_t f[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 v = gather_combine(e[q], gp[q].fu, gp[q].fv, gp[q].fs, wl[q]);
+              f[q] = h2u(__floats2half2_rn(v.x, v.y));
+            }
+            out = make_uint4(f[0], f[1], f[2], f[3]);
+          }
+          st16(s.A[b], a_off(ctid, c), out);
+        }
+      }
+      ptx::fence_async_smem();
+      gather_done_arrive(b);
+      WS_T(1);
+      continue;
+#else
       if (ctid < 128) {  // producer thread ctid < 128: row ctid
         // clear this row's features (buffer b's last reader, the MMA of round j-2, is done)
         // and list the (row, level) pairs of producer warp w's 32 rows, level-major
@@ -310,6 +367,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       bar_sync<kBarProd, kProdThreads>();  // every producer is done with this round's lists
       gather_done_arrive(b);
       WS_T(1);
+#endif
     }
   } else {
     // ================================ consumers ==============================================
@@ -484,6 +542,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       }
       {  // the row's gather input for the producers: grid coordinates, LOD, active levels
         const float fl = lw.floor_only ? 1e-4f : (float)lw.full + lw.frac;
+#if !WS_ROWMAJOR
         // the consumers gather the first kConsLevels levels of their own rows themselves (it
         // balances the two warpgroups) into A chunk 0, which they also clear
         {
@@ -496,13 +555,18 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           }
           st16(s.A[b], a_off(ctid, 0), make_uint4(wds[0], wds[1], wds[2], wds[3]));
         }
+#endif
         if (have) s.samp[b][ctid] = make_float4(u, v, w, fl);
         s.na[b][ctid] = (uint8_t)na;
+#if !WS_ROWMAJOR
         const int mine = na > kConsLevels ? na - kConsLevels : 0;  // the producers' pairs of this row
         const int wsum = __reduce_add_sync(FULL, (unsigned)mine);
         if (lane == 0) s.cnt[b][warp] = wsum;
+#endif
       }
-      ptx::fence_async_smem();
+#if !WS_ROWMAJOR
+      ptx::fence_async_smem();  // A chunk 0 (the MMA's async proxy reads it)
+#endif
       WS_T(7);
       // all consumer warps finished (every packet stored) -> the producers stop after round j
       const bool stop = bar_and<kBarCons, 128>(no_more && !packet_live);
