@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(128) k_march_mask(RenderParams p) {
         if (occupied(p, contract(ray_at(o, d, s_ts[w0 * 32 + b]), p.contraction))) bits |= 1u << b;
     }
     count += __popc(bits);
-    p.kept_mask[(size_t)w0 * p.total_rays + idx] = bits;
+    p.kept_mask[(size_t)w0 * p.total_rays + idx] = p.mask_transposed ? warp_transpose32(bits) : bits;
   }
   p.kept_count[idx] = (uint16_t)count;
   add_work_stats(p, 0, 0, valid ? (unsigned long long)p.n : 0ull, 0);
@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(128) k_march_mask_fast(RenderParams p) {
       __syncwarp();
     }
     count += __popc(bits);
-    if (idx < p.total_rays) p.kept_mask[(size_t)w0 * p.total_rays + idx] = bits;
+    const uint32_t out = p.mask_transposed ? warp_transpose32(bits) : bits;  // warp-uniform
+    if (idx < p.total_rays) p.kept_mask[(size_t)w0 * p.total_rays + idx] = out;
   }
   if (idx < p.total_rays) p.kept_count[idx] = (uint16_t)count;
   add_work_stats(p, 0, 0, valid ? (unsigned long long)p.n : 0ull, 0);
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(128) k_march_runs(RenderParams p) {
     for (int w0 = 0; w0 < p.mask_words; ++w0) {
       const uint32_t bits = s_bits[w0 * 128 + tid];
       count += __popc(bits);
-      p.kept_mask[(size_t)w0 * p.total_rays + idx] = bits;
+      p.kept_mask[(size_t)w0 * p.total_rays + idx] = p.mask_transposed ? warp_transpose32(bits) : bits;
     }
     p.kept_count[idx] = (uint16_t)count;
   }
@@ -358,6 +359,7 @@ cudaError_t launch_march_public(RenderParams p, uint32_t* mask, int32_t* counts,
   p.total_rays = rays;
   p.mask_words = (p.n + 31) / 32;
   p.work_stats = nullptr;
+  p.mask_transposed = 0;
   cudaError_t e;
   if ((e = cudaMallocAsync(&p.kept_mask, (size_t)rays * p.mask_words * 4, s)) != cudaSuccess) return e;
   if ((e = cudaMallocAsync(&p.kept_count, (size_t)rays * 2, s)) != cudaSuccess) return e;

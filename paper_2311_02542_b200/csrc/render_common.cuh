@@ -43,6 +43,10 @@ struct RenderParams {
   // kept_mask[word * total_rays + id], kept_count[id]
   uint32_t* kept_mask;
   uint16_t* kept_count;
+  // 1: kept_mask is stored transposed per 32-ray packet (ray ids packet-major, 32 per packet):
+  // word w of id pkt * 32 + c is the bitmask of the packet's rays (bit = ray lane) that keep
+  // candidate w * 32 + c -- the candidate-major view the packet renderer streams
+  int mask_transposed;
   // optional, written by the march pass for the packet renderer: fp32 direction of each ray id
   // and of its right neighbour (x + 1.5), SoA [6][total_rays], so a warp starting a packet
   // loads its rays instead of running the double-precision ray generation on its critical path
@@ -50,6 +54,20 @@ struct RenderParams {
   int mask_words;
   long long total_rays;
 };
+
+// 32x32 bit-matrix transpose across a warp (lane = row, bit = column in; lane = column, bit =
+// row out): five butterfly stages swapping the off-diagonal blocks.  All 32 lanes must call it.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
+                     : s == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y << s) & ~m));
+  }
+  return x;
+}
 
 // color.cpp:17-44 constants (scene-linear 1.0 = 100 cd/m^2)
 __device__ __forceinline__ double pq_decode_dev(double v) {

@@ -72,9 +72,9 @@ constexpr int kCtasPerSm = (kProdWarps == 4 || WS_REGSPLIT) ? 3 : 2;  // (regist
 #define WS_PROD_PAIRS 3
 #endif
 constexpr int kProdPairs = WS_PROD_PAIRS;  // pairs per producer thread per gather step
-// named barriers: 0 = __syncthreads (setup / teardown), LIST_READY 1 + b, GATHER_DONE 3 + b,
-// 5 = consumer warpgroup only, 6 = producer warpgroup only
-constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5, kBarProd = 6;
+// named barriers: 0 = __syncthreads (setup / teardown), LIST_READY 1 + b, GATHER_DONE 4 + b
+// (b < kStages), 7 = consumer warpgroup only, 8 = producer warpgroup only
+constexpr int kBarList = 1, kBarGather = 4, kBarCons = 7, kBarProd = 8;
 #ifndef WS_CONS_LEVELS
 #define WS_CONS_LEVELS 0
 #endif
@@ -86,6 +86,22 @@ constexpr int kConsLevels = WS_CONS_LEVELS;  // LOD levels gathered by the consu
 // warp walk the same level together (coherent hash cells, warp-uniform dense/hashed branch).
 #ifndef WS_ROWMAJOR
 #define WS_ROWMAJOR 1
+#endif
+#ifndef WS_F32_ALPHA
+#define WS_F32_ALPHA 1
+#endif
+// WS_STAGES: rounds in flight between the two warpgroups (2 = double-buffered, 3 = the
+// consumers fill two rounds ahead of the MLP, so a slow round on either side is absorbed)
+#ifndef WS_STAGES
+#define WS_STAGES 2
+#endif
+constexpr int kStages = WS_STAGES;
+static_assert(kStages == 2 || kStages == 3, "2 or 3 pipeline stages");
+// WS_TMASK: the march pass stores each packet's mask words transposed (candidate-major), so a
+// warp starting a word scans 32 counts instead of transposing the word with 32 ballots, and
+// expands it once into a (candidate, ray) sample stream its rows index directly
+#ifndef WS_TMASK
+#define WS_TMASK 0
 #endif
 #if WS_ROWMAJOR
 static_assert(kConsLevels == 0, "the row-major producers gather every level");
@@ -112,27 +128,31 @@ struct __align__(16) Smem {
 #if WS_SHARED_ONES
   // double-buffered layer-1 A tiles, features only (chunk-major, a_off); the bias step's
   // [1 0 ... 0] block is one shared pair of core matrices read with SBO = 0 by every row group
-  uint8_t A[2][128 * 32 * 2];
+  uint8_t A[kStages][128 * 32 * 2];
   uint8_t ones[2 * 128];
 #else
-  uint8_t A[2][128 * (32 + kKb) * 2];  // double-buffered layer-1 A tiles (chunk-major, a_off)
+  uint8_t A[kStages][128 * (32 + kKb) * 2];  // layer-1 A tiles per stage (chunk-major, a_off)
 #endif
   uint8_t W1[64 * (32 + kKb) * 2];
   uint8_t F[80 * (80 + kKb) * 2];
   uint8_t C2[64 * (64 + kKb) * 2];
   uint8_t C3[16 * (64 + kKb) * 2];
   float4 res[128];
+#if WS_TMASK
+  uint16_t stream[kWarps][32 * 32];  // per warp: the current mask word's (candidate, ray) samples
+#else
   uint32_t ballot[kWarps][32];
   uint16_t prefix[kWarps][33];
-  uint32_t own[2][kWarps][32];
-  uint16_t rowcand[2][kWarps][32];
-  uint8_t rowlane[2][128];
+#endif
+  uint32_t own[kStages][kWarps][32];
+  uint16_t rowcand[kStages][kWarps][32];
+  uint8_t rowlane[kStages][128];
   uint64_t mbar;
   uint32_t tmem_base;
-  int stop[2];
+  int stop[kStages];
   uint4 lvl[kMaxLevels];
-  float4 samp[2][128];
-  uint8_t na[2][128];                        // per row: active LOD levels (0 = no sample)
+  float4 samp[kStages][128];
+  uint8_t na[kStages][128];                  // per row: active LOD levels (0 = no sample)
 #if !WS_ROWMAJOR
   uint16_t pairs[kWarps * 32 * kMaxLevels];  // the round's gather list, warp lists concatenated
   int cnt[2][kWarps];                        // per warp: pairs the producers will list
@@ -174,18 +194,26 @@ __device__ __forceinline__ bool bar_and(bool v) {
       : "memory");
   return r != 0;
 }
-// buffer-indexed barriers: b is 0 or 1
+// stage-indexed barriers: b < kStages
 __device__ __forceinline__ void list_ready_sync(int b) {
-  if (b) bar_sync<kBarList + 1, kCtaThreads>(); else bar_sync<kBarList, kCtaThreads>();
+  if (b == 0) bar_sync<kBarList, kCtaThreads>();
+  else if (b == 1) bar_sync<kBarList + 1, kCtaThreads>();
+  else bar_sync<kBarList + 2, kCtaThreads>();
 }
 __device__ __forceinline__ void list_ready_arrive(int b) {
-  if (b) bar_arrive<kBarList + 1, kCtaThreads>(); else bar_arrive<kBarList, kCtaThreads>();
+  if (b == 0) bar_arrive<kBarList, kCtaThreads>();
+  else if (b == 1) bar_arrive<kBarList + 1, kCtaThreads>();
+  else bar_arrive<kBarList + 2, kCtaThreads>();
 }
 __device__ __forceinline__ void gather_done_sync(int b) {
-  if (b) bar_sync<kBarGather + 1, kCtaThreads>(); else bar_sync<kBarGather, kCtaThreads>();
+  if (b == 0) bar_sync<kBarGather, kCtaThreads>();
+  else if (b == 1) bar_sync<kBarGather + 1, kCtaThreads>();
+  else bar_sync<kBarGather + 2, kCtaThreads>();
 }
 __device__ __forceinline__ void gather_done_arrive(int b) {
-  if (b) bar_arrive<kBarGather + 1, kCtaThreads>(); else bar_arrive<kBarGather, kCtaThreads>();
+  if (b == 0) bar_arrive<kBarGather, kCtaThreads>();
+  else if (b == 1) bar_arrive<kBarGather + 1, kCtaThreads>();
+  else bar_arrive<kBarGather + 2, kCtaThreads>();
 }
 
 __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderParams p) {
@@ -253,9 +281,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
 
   if (wg == 1) {
     // ================================ producers ==============================================
+    int b = 0;  // j % kStages
 #pragma unroll 1
-    for (int j = 0;; ++j) {
-      const int b = j & 1;
+    for (int j = 0;; ++j, b = b + 1 == kStages ? 0 : b + 1) {
       list_ready_sync(b);
       WS_T(0);
       if (s.stop[b]) break;
@@ -404,9 +432,10 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
 #endif
     uint32_t phase = 0;
 
+    int b = 0, stop_round = -1;  // b = j % kStages; stop_round: the first round with no rows
 #pragma unroll 1
-    for (int j = 0;; ++j) {
-      const int b = j & 1;
+    for (int j = 0;; ++j, b = b + 1 == kStages ? 0 : b + 1) {
+      if (stop_round < 0) {
       // ---- F(j): this warp's rows of round j from its packet stream -----------------------
       int take = 0, rl = lane, cand = 0;
       while (take < 32 && !no_more && !pending) {
@@ -454,7 +483,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           packet_live = true;
           word = -1;
           g_next = word_total = 0;
-#if WS_PREFETCH
+#if WS_TMASK
+          next_bits = __ldg(p.kept_mask + r.id);  // lane = candidate of word 0: its rays
+#elif WS_PREFETCH
           next_bits = r.valid ? __ldg(p.kept_mask + r.id) : 0u;
 #endif
         }
@@ -462,12 +493,18 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           const int n = min(32 - take, word_total - g_next);
           if (lane >= take && lane < take + n) {
             const int g = g_next + (lane - take);
+#if WS_TMASK
+            const uint32_t e = s.stream[warp][g];
+            rl = (int)(e & 31u);
+            cand = word * 32 + (int)(e >> 5);
+#else
             int lo = 0;
 #pragma unroll
             for (int st = 16; st > 0; st >>= 1)
               if (s.prefix[warp][lo + st] <= g) lo += st;
             rl = nth_set_bit(s.ballot[warp][lo], g - s.prefix[warp][lo]);
             cand = word * 32 + lo;
+#endif
           }
           take += n;
           g_next += n;
@@ -480,6 +517,29 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           break;
         }
         ++word;
+#if WS_TMASK
+        {
+          // the march pass stored the packet's words transposed: lane c holds the rays keeping
+          // candidate word * 32 + c.  Drop terminated rays, scan the per-candidate counts and
+          // expand the word into the candidate-major sample stream (candidate, ray) of the warp
+          const uint32_t alive_m = __ballot_sync(FULL, r.alive);
+          const uint32_t col = next_bits & alive_m;
+          if (word + 1 < p.mask_words && alive_m != 0u)
+            next_bits = __ldg(p.kept_mask + (size_t)(word + 1) * p.total_rays + r.id);
+          const int c = __popc(col);
+          int incl = c;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, off);
+            if (lane >= off) incl += v;
+          }
+          int pos = incl - c;
+          for (uint32_t m = col; m; m &= m - 1u) s.stream[warp][pos++] = (uint16_t)((lane << 5) | (__ffs(m) - 1));
+          __syncwarp();
+          g_next = 0;
+          word_total = __shfl_sync(FULL, incl, 31);
+        }
+#else
 #if WS_PREFETCH
         const uint32_t bits = r.alive ? next_bits : 0u;
         if (word + 1 < p.mask_words && r.alive)
@@ -500,6 +560,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         __syncwarp();
         g_next = 0;
         word_total = run;
+#endif
       }
       WS_T(6);
       const bool have = lane < take;
@@ -568,15 +629,19 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       ptx::fence_async_smem();  // A chunk 0 (the MMA's async proxy reads it)
 #endif
       WS_T(7);
-      // all consumer warps finished (every packet stored) -> the producers stop after round j
+      // all consumer warps finished (every packet stored) -> the producers stop at round j
       const bool stop = bar_and<kBarCons, 128>(no_more && !packet_live);
       if (ctid == 0) s.stop[b] = stop ? 1 : 0;
       list_ready_arrive(b);
+      if (stop) stop_round = j;
       WS_T(2);
+      }
 
-      if (j > 0) {
-        // ---- M(j-1): the tcgen05 MLP over round j-1's 128 rows (field.h:106-137) ----------
-        const int bp = (j - 1) & 1;
+      // the round whose MLP and compositing run now: kStages - 1 rounds behind the fill
+      const int jm = j - (kStages - 1);
+      if (jm >= 0 && (stop_round < 0 || jm < stop_round)) {
+        // ---- M(jm): the tcgen05 MLP over round jm's 128 rows (field.h:106-137) -------------
+        const int bp = b + 1 == kStages ? 0 : b + 1;  // jm % kStages
         gather_done_sync(bp);
         WS_T(3);
         const int rlp = s.rowlane[bp][ctid];
@@ -654,7 +719,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         }
         __syncwarp();
         WS_T(4);
-        // ---- C(j-1): owners composite their samples of round j-1 in order ----------------
+        // ---- C(jm): owners composite their samples of round jm in order ------------------
         uint32_t mine = s.own[bp][warp][lane];
         while (mine && r.alive) {
           const int jj = __ffs(mine) - 1;
@@ -663,6 +728,18 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           const int cnd = s.rowcand[bp][warp][jj];
           const double t = __ldg(p.ts + cnd);
           const double delta = (cnd + 1 < p.n) ? dsub(__ldg(p.ts + cnd + 1), t) : dmul(t, dsub(p.ratio, 1.0));
+#if WS_F32_ALPHA
+          // alpha and the sample's weight in fp32 (the MUFU exp: ~2 ulp, far below the fp16 sigma's
+          // error); the transmittance that decides the cut keeps accumulating in double
+          const float ef = __expf(-e.x * (float)delta);
+          const float wgt = (float)r.trans * (1.f - ef);
+          r.px += wgt * e.y;
+          r.py += wgt * e.z;
+          r.pz += wgt * e.w;
+          r.depth += wgt * (float)t;
+          r.opac += wgt;
+          r.trans = dmul(r.trans, (double)ef);
+#else
           const double a = dsub(1.0, exp(dmul(-(double)e.x, delta)));
           const double wgt = dmul(r.trans, a);
           r.px = dadd(r.px, dmul(wgt, (double)e.y));
@@ -671,6 +748,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           r.depth = dadd(r.depth, dmul(wgt, t));
           r.opac = dadd(r.opac, wgt);
           r.trans = dmul(r.trans, dsub(1.0, a));
+#endif
           ++r.contributing;
           if (p.t_cut > 0 && r.trans < p.t_cut) {
             r.term = true;
@@ -680,7 +758,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       }
       WS_T(5);
       // a finished packet is stored once its last round is composited (renderer.h:233-236)
-      if (pending && j - 1 >= last_round) {
+      if (pending && jm >= last_round) {
         if (r.valid) {
           const long long pk_ = r.id >> 5;
           const int px_ = (int)(pk_ % packets_x) * kPW + (lane % kPW);
@@ -693,7 +771,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         pending = false;
         packet_live = false;
       }
-      if (stop) break;
+      if (stop_round >= 0 && jm + 1 >= stop_round) break;  // every round with rows composited
     }
     ptx::tc_fence_before();
     bar_sync<kBarCons, 128>();
@@ -761,6 +839,7 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
   p.total_rays = packets * 32;
   if (p.total_rays >= (1ll << 31)) return cudaErrorInvalidValue;
   p.mask_words = (p.n + 31) / 32;
+  p.mask_transposed = WS_TMASK;
   if ((e = cudaMallocAsync(&p.kept_mask, (size_t)p.total_rays * p.mask_words * 4, s)) != cudaSuccess)
     return e;
   if ((e = cudaMallocAsync(&p.kept_count, (size_t)p.total_rays * 2, s)) != cudaSuccess) return e;
