@@ -220,6 +220,9 @@ struct MlpDev {
   const float* cparams;
   const float* fused;  // [65 x 80] + [65]: density L2 folded into colour L1 (lumi_api.cu)
   int color_space;
+  // the packed-renderer's fp16 UMMA weight tiles (W1 | fused | C2 | C3), the exact shared-memory
+  // image k_render_ws stages with one TMA bulk copy per CTA; built by launch_pack_weight_tiles
+  const void* wtiles;
 };
 
 }  // namespace lumi_dev

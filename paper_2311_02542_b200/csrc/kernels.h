@@ -121,6 +121,9 @@ cudaError_t launch_gather_bench(const lumi_dev::GridDev& g, int n, int coherent,
                                 cudaStream_t s);
 cudaError_t launch_mlp_batch(const lumi_dev::MlpDev& mlp, const void* feat, const float* dirs, int n,
                              float* out, int num_sms, cudaStream_t s);
+// the packed fp16 weight-tile image k_render_ws stages by TMA (bytes; build with the launcher)
+size_t render_ws_weight_tile_bytes();
+cudaError_t launch_pack_weight_tiles(const lumi_dev::MlpDev& mlp, void* img, cudaStream_t s);
 // ev (optional): 3 events recorded before the march pass, between march and render, after render
 cudaError_t launch_render_ws(lumi_dev::RenderParams p, cudaStream_t s, int num_sms,
                              cudaEvent_t* ev = nullptr);

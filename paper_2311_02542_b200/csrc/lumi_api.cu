@@ -175,6 +175,7 @@ struct LumiModel {
   float* d_dparams = nullptr;
   float* d_cparams = nullptr;
   float* d_fused = nullptr;  // density L2 folded into colour L1 (packet kernel), see fuse_l2_c1
+  void* d_wtiles = nullptr;  // the packet kernel's fp16 weight-tile image (TMA-staged per CTA)
   uint8_t* d_occ = nullptr;
   int occ_res = 0;
   int kernel = LUMI_KERNEL_WS;
@@ -264,6 +265,12 @@ int make_params(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions
   p->mlp.dparams = m->d_dparams;
   p->mlp.cparams = m->d_cparams;
   p->mlp.fused = m->d_fused;
+  // LUMI_WS_TMA=0 (A/B): each CTA converts the fp32 parameters itself instead of the TMA copy
+  static const bool tma = [] {
+    const char* e = std::getenv("LUMI_WS_TMA");
+    return !(e && e[0] == '0');
+  }();
+  p->mlp.wtiles = tma ? m->d_wtiles : nullptr;
   p->mlp.color_space = m->desc.color_space;
   p->occ = m->d_occ;
   p->occ_res = m->occ_res;
@@ -444,6 +451,12 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
                         cudaMemcpyHostToDevice)) != cudaSuccess)
       return cleanup(fail(LUMI_ERR_CUDA, std::string("model upload: ") + cudaGetErrorString(e)));
   }
+  if ((e = cudaMalloc(&m->d_wtiles, render_ws_weight_tile_bytes())) != cudaSuccess ||
+      (e = launch_pack_weight_tiles(lumi_dev::MlpDev{m->d_dparams, m->d_cparams, m->d_fused,
+                                                      m->desc.color_space, nullptr},
+                                    m->d_wtiles, nullptr)) != cudaSuccess ||
+      (e = cudaDeviceSynchronize()) != cudaSuccess)
+    return cleanup(fail(LUMI_ERR_CUDA, std::string("model upload: ") + cudaGetErrorString(e)));
   if ((rc = lumi_model_set_occupancy(m, occ, occ_res))) return cleanup(rc);
   if (const char* k = std::getenv("LUMI_KERNEL")) {
     const std::string ks(k);
@@ -477,6 +490,7 @@ int lumi_model_destroy(LumiModel* m) {
   cudaFree(m->d_dparams);
   cudaFree(m->d_cparams);
   cudaFree(m->d_fused);
+  cudaFree(m->d_wtiles);
   cudaFree(m->d_occ);
   for (auto& kv : m->ts_cache) cudaFree(kv.second.first);
   for (auto& a : m->ev_pool)
@@ -828,7 +842,7 @@ int lumi_mlp_batch_async(LumiModel* m, const void* features, const float* dirs, 
   if ((reinterpret_cast<uintptr_t>(features) & 15) != 0)
     return fail(LUMI_ERR_INVALID, "mlp_batch: features must be 16-byte aligned");
   DeviceGuard dg(m->device);
-  lumi_dev::MlpDev mlp{m->d_dparams, m->d_cparams, m->d_fused, m->desc.color_space};
+  lumi_dev::MlpDev mlp{m->d_dparams, m->d_cparams, m->d_fused, m->desc.color_space, nullptr};
   cudaError_t e = launch_mlp_batch(mlp, features, dirs, n, out, m->num_sms, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(LUMI_ERR_CUDA, std::string("mlp_batch: ") + cudaGetErrorString(e));
   return LUMI_OK;
@@ -987,6 +1001,9 @@ int lumi_model_params_updated(LumiModel* m) {
   LUMI_CUDA_TRY(cudaMemcpy(cp.data(), m->d_cparams, cp.size() * sizeof(float), cudaMemcpyDeviceToHost));
   const std::vector<float> fused = fuse_l2_c1(dp.data(), cp.data());
   LUMI_CUDA_TRY(cudaMemcpy(m->d_fused, fused.data(), fused.size() * sizeof(float), cudaMemcpyHostToDevice));
+  LUMI_CUDA_TRY(launch_pack_weight_tiles(lumi_dev::MlpDev{m->d_dparams, m->d_cparams, m->d_fused,
+                                                         m->desc.color_space, nullptr},
+                                         m->d_wtiles, nullptr));
   LUMI_CUDA_TRY(cudaDeviceSynchronize());
   return LUMI_OK;
 }

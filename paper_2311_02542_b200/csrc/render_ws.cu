@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -148,6 +149,7 @@ struct __align__(16) Smem {
   uint16_t rowcand[kStages][kWarps][32];
   uint8_t rowlane[kStages][128];
   uint64_t mbar;
+  uint64_t wbar;  // the weight tiles' TMA bulk copy
   uint32_t tmem_base;
   int stop[kStages];
   uint4 lvl[kMaxLevels];
@@ -158,6 +160,31 @@ struct __align__(16) Smem {
   int cnt[2][kWarps];                        // per warp: pairs the producers will list
 #endif
 };
+
+// the four weight tiles are consecutive in Smem: one contiguous image, one bulk copy
+constexpr size_t kWeightTileBytes = sizeof(Smem::W1) + sizeof(Smem::F) + sizeof(Smem::C2) + sizeof(Smem::C3);
+static_assert(offsetof(Smem, F) == offsetof(Smem, W1) + sizeof(Smem::W1) &&
+                  offsetof(Smem, C2) == offsetof(Smem, F) + sizeof(Smem::F) &&
+                  offsetof(Smem, C3) == offsetof(Smem, C2) + sizeof(Smem::C2),
+              "weight tiles must be contiguous");
+static_assert(kWeightTileBytes % 16 == 0 && offsetof(Smem, W1) % 16 == 0, "bulk copy alignment");
+
+// the weight tiles' shared-memory image in global memory (the same load_weight_tile code,
+// storing through a generic pointer), built once per model / parameter update
+__global__ void k_pack_weight_tiles(MlpDev mlp, uint8_t* img) {
+  const float* dp = mlp.dparams;
+  const float* cp = mlp.cparams;
+  const float* c2 = cp + 64 * 32 + 64;
+  const float* c3 = c2 + 64 * 64 + 64;
+  uint8_t* W1 = img;
+  uint8_t* F = W1 + sizeof(Smem::W1);
+  uint8_t* C2 = F + sizeof(Smem::F);
+  uint8_t* C3 = C2 + sizeof(Smem::C2);
+  load_weight_tile(W1, dp, 64, 64, 32);
+  load_weight_tile(F, mlp.fused, kHidden + 1, 80, 80);
+  load_weight_tile(C2, c2, 64, 64, 64);
+  load_weight_tile(C3, c3, 3, 16, 64);
+}
 
 // layer 1 with the bias step's A from the shared ones block (LBO 128 B between its two core
 // matrices, SBO 0: every 8-row group reads the same [1 0 ... 0] rows)
@@ -224,14 +251,26 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
   const unsigned FULL = 0xffffffffu;
 
   // ---- setup (all 256 threads) -------------------------------------------------------------
-  const float* dp = p.mlp.dparams;
-  const float* cp = p.mlp.cparams;
-  const float* c2 = cp + 64 * 32 + 64;
-  const float* c3 = c2 + 64 * 64 + 64;
-  load_weight_tile(s.W1, dp, 64, 64, 32);
-  load_weight_tile(s.F, p.mlp.fused, kHidden + 1, 80, 80);
-  load_weight_tile(s.C2, c2, 64, 64, 64);
-  load_weight_tile(s.C3, c3, 3, 16, 64);
+  // the four fp16 UMMA weight tiles: one TMA bulk copy of their packed image (built once per
+  // model, launch_pack_weight_tiles), or converted from the fp32 parameters here
+  const bool tma_weights = p.mlp.wtiles != nullptr;
+  if (tma_weights) {
+    if (tid == 0) {
+      ptx::mbar_init(&s.wbar, 1);
+      ptx::fence_mbar_init();
+      ptx::mbar_arrive_expect_tx(&s.wbar, (uint32_t)kWeightTileBytes);
+      ptx::tma_bulk_g2s(s.W1, p.mlp.wtiles, (uint32_t)kWeightTileBytes, &s.wbar);
+    }
+  } else {
+    const float* dp = p.mlp.dparams;
+    const float* cp = p.mlp.cparams;
+    const float* c2 = cp + 64 * 32 + 64;
+    const float* c3 = c2 + 64 * 64 + 64;
+    load_weight_tile(s.W1, dp, 64, 64, 32);
+    load_weight_tile(s.F, p.mlp.fused, kHidden + 1, 80, 80);
+    load_weight_tile(s.C2, c2, 64, 64, 64);
+    load_weight_tile(s.C3, c3, 3, 16, 64);
+  }
 #if WS_SHARED_ONES
   if (tid < 16) st16(s.ones, (uint32_t)tid * 16u, make_uint4(tid < 8 ? 0x3C00u : 0u, 0u, 0u, 0u));
 #else
@@ -399,6 +438,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
     }
   } else {
     // ================================ consumers ==============================================
+    if (tma_weights) ptx::mbar_wait(&s.wbar, 0);  // the weight tiles have landed
     const uint32_t t_lane = tmem + ((uint32_t)(warp * 32) << 16);
     {
       const uint32_t ones[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -787,6 +827,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
 using namespace lumi_dev;
 
 size_t render_ws_smem_bytes() { return sizeof(ws::Smem); }
+size_t render_ws_weight_tile_bytes() { return ws::kWeightTileBytes; }
+
+cudaError_t launch_pack_weight_tiles(const MlpDev& mlp, void* img, cudaStream_t s) {
+  ws::k_pack_weight_tiles<<<1, 256, 0, s>>>(mlp, static_cast<uint8_t*>(img));
+  return cudaGetLastError();
+}
 
 // march pass over packet-ordered ray ids + the warp-specialised kernel
 cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEvent_t* ev) {
