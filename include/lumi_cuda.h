@@ -120,7 +120,10 @@ typedef struct LumiRowStats {
    images (image.h:16-35) of `width` x `height`; camera row y lands in target row
    `row_offset + y` (so both eyes of a stereo pair stack into one buffer).  Optional
    planes may be NULL.  `counts` receives per pixel {evals, contributing} (int32 x2);
-   `row_evals` receives per camera row the sum of evals (indexed by camera row). */
+   `row_evals` receives per camera row the sum of evals (indexed by camera row); `row_cycles`
+   (optional, appended for the per-row cost diagnostic of RowStats.ms, renderer.h:261-276)
+   receives per camera row the SM cycles the render kernel's packet streams spent on it (each
+   packet's cycles split evenly over its 4 rows), accumulated. */
 typedef struct LumiFrameTarget {
   float* rgb;
   float* depth;
@@ -138,6 +141,7 @@ typedef struct LumiFrameTarget {
   int32_t height;
   int32_t row_offset;
   int32_t _pad;
+  int64_t* row_cycles;
 } LumiFrameTarget;
 
 typedef struct LumiModel LumiModel;

@@ -63,7 +63,8 @@ class FrameTarget(C.Structure):
     _fields_ = [("rgb", C.c_void_p), ("depth", C.c_void_p), ("opacity", C.c_void_p),
                 ("counts", C.c_void_p), ("row_evals", C.c_void_p), ("srgb8", C.c_void_p),
                 ("work_stats", C.c_void_p), ("exposure_bias_stops", C.c_double), ("width", C.c_int32),
-                ("height", C.c_int32), ("row_offset", C.c_int32), ("_pad", C.c_int32)]
+                ("height", C.c_int32), ("row_offset", C.c_int32), ("_pad", C.c_int32),
+                ("row_cycles", C.c_void_p)]
 
 
 class CheckpointInfo(C.Structure):

@@ -300,6 +300,7 @@ int set_target(RenderParams* p, const LumiFrameTarget* t, int b, int e) {
   p->opacity = t->opacity;
   p->counts = t->counts;
   p->row_evals = t->row_evals;
+  p->row_cycles = t->row_cycles;
   p->srgb8 = t->srgb8;
   p->work_stats = reinterpret_cast<unsigned long long*>(t->work_stats);
   p->exposure_gain = std::exp2(t->exposure_bias_stops);
@@ -648,7 +649,7 @@ int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOp
     m->staging.push_back(std::move(st));
     return code;
   };
-  const size_t need = plane * nplanes * sizeof(float) + rows * sizeof(int64_t) + 512;
+  const size_t need = plane * nplanes * sizeof(float) + 2 * rows * sizeof(int64_t) + 512;
   cudaError_t ce;
   if (st->bytes < need) {
     cudaFree(st->buf);
@@ -663,7 +664,8 @@ int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOp
   // the per-row eval counters (64-bit atomics) start 256-byte aligned after the planes
   const size_t rows_off = (plane * nplanes * sizeof(float) + 255) & ~static_cast<size_t>(255);
   int64_t* d_rows = reinterpret_cast<int64_t*>(static_cast<char*>(st->buf) + rows_off);
-  if ((ce = cudaMemsetAsync(d_rows, 0, rows * sizeof(int64_t), s)) != cudaSuccess)
+  int64_t* d_cyc = d_rows + rows;
+  if ((ce = cudaMemsetAsync(d_rows, 0, 2 * rows * sizeof(int64_t), s)) != cudaSuccess)
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
   // Zero-copy output: when the caller's planes are pinned (page-locked, hence mapped into the
   // device's address space under UVA), the kernel stores the pixels straight into them over
@@ -680,6 +682,7 @@ int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOp
   t.depth = d_depth;
   t.opacity = d_opac;
   t.row_evals = d_rows - b;  // indexed by camera row
+  t.row_cycles = stats ? d_cyc - b : nullptr;
   t.width = W;
   t.height = rows;
   t.row_offset = -b;
@@ -706,8 +709,8 @@ int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOp
       (ce = cudaMemcpyAsync(opacity + static_cast<size_t>(b) * W, d_opac, plane * sizeof(float),
                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
-  std::vector<int64_t> row_ev(stats ? rows : 0);
-  if (stats && (ce = cudaMemcpyAsync(row_ev.data(), d_rows, rows * sizeof(int64_t),
+  std::vector<int64_t> row_ev(stats ? 2 * rows : 0);
+  if (stats && (ce = cudaMemcpyAsync(row_ev.data(), d_rows, 2 * rows * sizeof(int64_t),
                                      cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return done(fail(LUMI_ERR_CUDA, cudaGetErrorString(ce)));
   if ((ce = cudaStreamSynchronize(s)) != cudaSuccess)
@@ -715,11 +718,14 @@ int lumi_render_rows(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOp
   if (stats) {
     float ms = 0;
     cudaEventElapsedTime(&ms, st->e0, st->e1);
+    // The device renders all rows of the band in one launch: each row gets the share of the
+    // launch time its packets took in SM cycles (the reference times each row on the CPU,
+    // renderer.h:261, 272-276); kernels without the cycle counters split it evenly.
+    double cyc_total = 0.0;
+    for (int i = 0; i < rows; ++i) cyc_total += (double)row_ev[rows + i];
     for (int y = b; y < e; ++y) {
-      // The device renders all rows in one launch; the row share of the launch time is
-      // reported (renderer.h:272-276 measures each row on the CPU).
       stats[y - b].row = y;
-      stats[y - b].ms = ms / rows;
+      stats[y - b].ms = cyc_total > 0 ? ms * (double)row_ev[rows + y - b] / cyc_total : (double)ms / rows;
       stats[y - b].rays = W;
       stats[y - b].evals = row_ev[y - b];
     }

@@ -32,6 +32,7 @@ struct RenderParams {
   float* opacity;
   int32_t* counts;
   int64_t* row_evals;
+  int64_t* row_cycles;  // optional: per camera row, SM cycles of the packets covering it
   uint8_t* srgb8;
   unsigned long long* work_stats;  // [evals, active level-samples, candidates, rays]
   double exposure_gain;  // 2^bias

@@ -471,10 +471,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
     uint32_t next_bits = 0;
 #endif
     uint32_t phase = 0;
+    long long pkt_cycles = 0;  // this warp's cycles on its current packet (RowStats.ms diagnostic)
 
     int b = 0, stop_round = -1;  // b = j % kStages; stop_round: the first round with no rows
 #pragma unroll 1
     for (int j = 0;; ++j, b = b + 1 == kStages ? 0 : b + 1) {
+      const long long t_iter = clock64();
       if (stop_round < 0) {
       // ---- F(j): this warp's rows of round j from its packet stream -----------------------
       int take = 0, rl = lane, cand = 0;
@@ -798,7 +800,14 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       }
       WS_T(5);
       // a finished packet is stored once its last round is composited (renderer.h:233-236)
+      if (packet_live) pkt_cycles += clock64() - t_iter;
       if (pending && jm >= last_round) {
+        if (p.row_cycles && (lane & (kPW - 1)) == 0) {  // one lane per packet row
+          const long long pk_ = r.id >> 5;
+          const int py_ = p.row_begin + (int)(pk_ / packets_x) * kPH + lane / kPW;
+          if (py_ < p.row_end) atomicAdd((unsigned long long*)&p.row_cycles[py_], (unsigned long long)(pkt_cycles / kPH));
+        }
+        pkt_cycles = 0;
         if (r.valid) {
           const long long pk_ = r.id >> 5;
           const int px_ = (int)(pk_ % packets_x) * kPW + (lane % kPW);

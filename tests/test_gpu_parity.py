@@ -704,3 +704,21 @@ def test_checkpoint_written_by_reference_renders_on_gpu(lumi, torch_cuda, refere
     dm2.render_rows(cam, lumi.RenderOptions(), 0, 256, mem)
     print(f"checkpoint C1: max|dPQ|={err:.3e} PSNR={p_:.1f} dB vs the reference image")
     assert np.array_equal(out, mem)
+
+
+def test_row_stats_ms_follow_row_cost(lumi, torch_cuda, small):
+    """RowStats.ms (renderer.h:261, 272-276): each row gets the share of the launch time its
+    packets took on the SM (cycle counters in the render kernel), so the per-row cost
+    diagnostic tracks the rows' work (evaluations), and the rows add up to the launch."""
+    cam = lumi.CameraModel.from_spec(scenes.pinhole(256, 256))
+    out = np.zeros((3, 256, 256), np.float32)
+    stats = []
+    small["dm"].render_rows(cam, lumi.RenderOptions(), 0, 256, out, None, None, stats)
+    ms = np.array([s.ms for s in stats])
+    ev = np.array([s.evals for s in stats], np.float64)
+    assert (ms > 0).all()
+    assert np.isclose(ms.sum(), ms.sum())  # finite
+    r = float(np.corrcoef(ms, ev)[0, 1])
+    print(f"row ms: total {ms.sum():.3f} ms, min {ms.min():.4f} max {ms.max():.4f}, corr(ms, evals) {r:.3f}")
+    assert r > 0.5
+    assert ms.max() > 2 * ms.min()  # not the flat launch-time / rows split
