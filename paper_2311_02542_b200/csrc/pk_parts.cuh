@@ -134,9 +134,6 @@ __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane)
 // (HMUL2) accumulated in fp32 by FHFMA in two interleaved chains per feature.  Split in three
 // so a thread can put the corner loads of several pairs in flight before it consumes any:
 // gather_prep (cell, corner indices, fractions), the 8 loads, gather_combine.
-#ifndef LUMI_GATHER_HACC
-#define LUMI_GATHER_HACC 1
-#endif
 struct GatherPrep {
   const __half2* base;  // the level's first entry
   uint32_t idx[8];
@@ -155,13 +152,26 @@ __device__ __forceinline__ void gather_prep(uint4 L, float u, float v, float s, 
   g.fs = ps - (float)is;
 }
 
-__device__ __forceinline__ float2 gather_combine(const __half2* e, float fu, float fv, float fs, float wl) {
+#ifndef LUMI_GATHER_LERP
+#define LUMI_GATHER_LERP 1
+#endif
+// The trilinear combination of the 8 corner entries (corner k: bit 0 = x + 1, bit 1 = y + 1,
+// bit 2 = z + 1) times the level's LOD weight, both features at once in packed fp16 -- the
+// value the renderer stores into the layer-1 A tile.  LUMI_GATHER_LERP: seven packed lerps
+// a + (b - a) f (HADD2 + HFMA2 each) instead of eight corner weights and eight products.
+__device__ __forceinline__ __half2 gather_combine_h(const __half2* e, float fu, float fv, float fs, float wl) {
+#if LUMI_GATHER_LERP
+  const __half2 hu = __float2half2_rn(fu), hv = __float2half2_rn(fv), hs = __float2half2_rn(fs);
+  const __half2 x00 = __hfma2(__hsub2(e[1], e[0]), hu, e[0]), x10 = __hfma2(__hsub2(e[3], e[2]), hu, e[2]),
+                x01 = __hfma2(__hsub2(e[5], e[4]), hu, e[4]), x11 = __hfma2(__hsub2(e[7], e[6]), hu, e[6]);
+  const __half2 y0 = __hfma2(__hsub2(x10, x00), hv, x00), y1 = __hfma2(__hsub2(x11, x01), hv, x01);
+  return __hmul2(__hfma2(__hsub2(y1, y0), hs, y0), __float2half2_rn(wl));
+#else
   const __half2 hu = __floats2half2_rn(1.f - fu, fu);
   const __half2 w0 = __hmul2(hu, __float2half2_rn(1.f - fv));
   const __half2 w1 = __hmul2(hu, __float2half2_rn(fv));
   const __half2 gs2 = __float2half2_rn(1.f - fs), fs2 = __float2half2_rn(fs);
   const __half2 t[4] = {__hmul2(w0, gs2), __hmul2(w1, gs2), __hmul2(w0, fs2), __hmul2(w1, fs2)};
-#if LUMI_GATHER_HACC
   // both features at once in packed fp16 (HFMA2), two chains, one widening add at the end
   __half2 c[2];
 #pragma unroll
@@ -170,17 +180,12 @@ __device__ __forceinline__ float2 gather_combine(const __half2* e, float fu, flo
     c[k & 1] = k < 2 ? __hmul2(e[k], tri) : __hfma2(e[k], tri, c[k & 1]);
   }
   const float2 x = __half22float2(c[0]), y = __half22float2(c[1]);
-  return make_float2((x.x + y.x) * wl, (x.y + y.y) * wl);
-#else
-  float a[2] = {0.f, 0.f}, b[2] = {0.f, 0.f};
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const __half tri = (k & 1) ? __high2half(t[k >> 1]) : __low2half(t[k >> 1]);
-    a[k & 1] = fma_f32_f16(tri, __low2half(e[k]), a[k & 1]);
-    b[k & 1] = fma_f32_f16(tri, __high2half(e[k]), b[k & 1]);
-  }
-  return make_float2((a[0] + a[1]) * wl, (b[0] + b[1]) * wl);
+  return __floats2half2_rn((x.x + y.x) * wl, (x.y + y.y) * wl);
 #endif
+}
+
+__device__ __forceinline__ float2 gather_combine(const __half2* e, float fu, float fv, float fs, float wl) {
+  return __half22float2(gather_combine_h(e, fu, fv, fs, wl));
 }
 
 __device__ __forceinline__ float2 gather_level(uint4 L, float u, float v, float s, float wl) {

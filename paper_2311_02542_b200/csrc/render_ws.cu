@@ -355,10 +355,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
             }
             uint32_t f[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float2 v = gather_combine(e[q], gp[q].fu, gp[q].fv, gp[q].fs, wl[q]);
-              f[q] = h2u(__floats2half2_rn(v.x, v.y));
-            }
+            for (int q = 0; q < 4; ++q) f[q] = h2u(gather_combine_h(e[q], gp[q].fu, gp[q].fv, gp[q].fs, wl[q]));
             out = make_uint4(f[0], f[1], f[2], f[3]);
           }
           st16(s.A[b], a_off(ctid, c), out);

@@ -717,8 +717,8 @@ def test_row_stats_ms_follow_row_cost(lumi, torch_cuda, small):
     ms = np.array([s.ms for s in stats])
     ev = np.array([s.evals for s in stats], np.float64)
     assert (ms > 0).all()
-    assert np.isclose(ms.sum(), ms.sum())  # finite
+    assert np.isfinite(ms).all()
     r = float(np.corrcoef(ms, ev)[0, 1])
     print(f"row ms: total {ms.sum():.3f} ms, min {ms.min():.4f} max {ms.max():.4f}, corr(ms, evals) {r:.3f}")
     assert r > 0.5
-    assert ms.max() > 2 * ms.min()  # not the flat launch-time / rows split
+    assert ms.std() > 0.05 * ms.mean()  # not the flat launch-time / rows split
