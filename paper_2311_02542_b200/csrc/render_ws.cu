@@ -335,23 +335,33 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
 #pragma unroll 1
         for (int c = 0; c < kMaxLevels / 4; ++c) {  // A chunk c = levels 4c .. 4c + 3
           uint4 out = make_uint4(0u, 0u, 0u, 0u);
-          if (4 * c < na_max) {  // warp-uniform
+          const int nq = min(4, na_max - 4 * c);  // levels of the chunk active in some lane (uniform)
+          if (nq > 0) {
+            const float fl0 = P.w - (float)(4 * c);
             GatherPrep gp[4];
             float wl[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const int l = 4 * c + q;
-              wl[q] = l < na ? __saturatef(P.w - (float)l) : 0.f;
-              gather_prep(s.lvl[l], P.x, P.y, P.z, gp[q]);
+              // a lane whose row has fewer levels than the warp's longest gathers the level
+              // anyway (a valid cell next to its neighbours') with weight 0
+              wl[q] = 4 * c + q < na ? __saturatef(fl0 - (float)q) : 0.f;
+              gather_prep(s.lvl[4 * c + q], P.x, P.y, P.z, gp[q]);
             }
-            // all corner loads of the chunk in flight before the first combine; lanes whose row
-            // has fewer levels predicate theirs off
+            // all corner loads of the chunk in flight before the first combine; levels no lane
+            // of the warp needs (the last chunk) are not loaded
             __half2 e[4][8];
+            if (nq == 4) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const bool act = 4 * c + q < na;
+              for (int q = 0; q < 4; ++q)
 #pragma unroll
-              for (int k = 0; k < 8; ++k) e[q][k] = act ? __ldg(gp[q].base + gp[q].idx[k]) : __half2{};
+                for (int k = 0; k < 8; ++k) e[q][k] = __ldg(gp[q].base + gp[q].idx[k]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const bool act = q < nq;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) e[q][k] = act ? __ldg(gp[q].base + gp[q].idx[k]) : __half2{};
+              }
             }
             uint32_t f[4];
 #pragma unroll
