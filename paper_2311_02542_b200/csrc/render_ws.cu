@@ -73,9 +73,23 @@ constexpr int kCtasPerSm = (kProdWarps == 4 || WS_REGSPLIT) ? 3 : 2;  // (regist
 #define WS_PROD_PAIRS 3
 #endif
 constexpr int kProdPairs = WS_PROD_PAIRS;  // pairs per producer thread per gather step
+// WS_PAIRS: producer warp w gathers exactly consumer warp w's 32 rows, so the list handoff is a
+// per-warp-pair barrier (64 threads): a producer warp starts as soon as ITS consumer warp has
+// filled its rows instead of waiting for the slowest of the four.  The round's MMA still waits
+// for all four producer warps (GATHER_DONE).  Stop: producers cannot see the consumers' stop
+// decision before they start, so they gather the final (empty) round too; the consumers then
+// drain its GATHER_DONE, raise `halt` and wake each producer warp one last time.
+#ifndef WS_PAIRS
+#define WS_PAIRS 0
+#endif
 // named barriers: 0 = __syncthreads (setup / teardown), LIST_READY 1 + b, GATHER_DONE 4 + b
 // (b < kStages), 7 = consumer warpgroup only, 8 = producer warpgroup only
-constexpr int kBarList = 1, kBarGather = 4, kBarCons = 7, kBarProd = 8;
+#if WS_PAIRS
+// LIST_READY of (warp w, stage b) = kBarPair + 2 w + b (1 .. 8), GATHER_DONE 9 + b
+constexpr int kBarPair = 1, kBarList = 0, kBarGather = 9, kBarCons = 11, kBarProd = 12;
+#else
+constexpr int kBarList = 1, kBarGather = 4, kBarCons = 7, kBarProd = 8, kBarPair = 0;
+#endif
 #ifndef WS_CONS_LEVELS
 #define WS_CONS_LEVELS 0
 #endif
@@ -97,6 +111,10 @@ constexpr int kConsLevels = WS_CONS_LEVELS;  // LOD levels gathered by the consu
 #define WS_STAGES 2
 #endif
 constexpr int kStages = WS_STAGES;
+#if WS_PAIRS
+static_assert(kStages == 2 && WS_ROWMAJOR, "the per-pair handoff is built for the 2-stage row-major kernel");
+#endif
+
 static_assert(kStages == 2 || kStages == 3, "2 or 3 pipeline stages");
 // WS_TMASK: the march pass stores each packet's mask words transposed (candidate-major), so a
 // warp starting a word scans 32 counts instead of transposing the word with 32 ballots, and
@@ -152,6 +170,7 @@ struct __align__(16) Smem {
   uint64_t wbar;  // the weight tiles' TMA bulk copy
   uint32_t tmem_base;
   int stop[kStages];
+  int halt;  // WS_PAIRS: the consumers have stopped (no further round)
   uint4 lvl[kMaxLevels];
   float4 samp[kStages][128];
   uint8_t na[kStages][128];                  // per row: active LOD levels (0 = no sample)
@@ -221,6 +240,24 @@ __device__ __forceinline__ bool bar_and(bool v) {
       : "memory");
   return r != 0;
 }
+// per-warp-pair list handoff (WS_PAIRS): 64 threads, consumer warp w + producer warp w
+template <int ID>
+__device__ __forceinline__ void pair_bar(bool arrive) {
+  if (arrive) bar_arrive<ID, 64>(); else bar_sync<ID, 64>();
+}
+__device__ __forceinline__ void pair_ready(int w, int b, bool arrive) {
+  switch (2 * w + b) {
+    case 0: pair_bar<kBarPair + 0>(arrive); break;
+    case 1: pair_bar<kBarPair + 1>(arrive); break;
+    case 2: pair_bar<kBarPair + 2>(arrive); break;
+    case 3: pair_bar<kBarPair + 3>(arrive); break;
+    case 4: pair_bar<kBarPair + 4>(arrive); break;
+    case 5: pair_bar<kBarPair + 5>(arrive); break;
+    case 6: pair_bar<kBarPair + 6>(arrive); break;
+    default: pair_bar<kBarPair + 7>(arrive); break;
+  }
+}
+
 // stage-indexed barriers: b < kStages
 __device__ __forceinline__ void list_ready_sync(int b) {
   if (b == 0) bar_sync<kBarList, kCtaThreads>();
@@ -289,6 +326,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
                           (uint32_t)(base >> 32));
   }
   if (tid == 0) {
+    s.halt = 0;
     ptx::mbar_init(&s.mbar, 1);
     ptx::fence_mbar_init();
   }
@@ -323,9 +361,15 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
     int b = 0;  // j % kStages
 #pragma unroll 1
     for (int j = 0;; ++j, b = b + 1 == kStages ? 0 : b + 1) {
+#if WS_PAIRS
+      pair_ready(warp, b, false);
+      WS_T(0);
+      if (s.halt) break;
+#else
       list_ready_sync(b);
       WS_T(0);
       if (s.stop[b]) break;
+#endif
 #if WS_ROWMAJOR
       {
         // row ctid: grid coordinates + LOD (fl) and its active level count, from the consumers
@@ -678,10 +722,16 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       ptx::fence_async_smem();  // A chunk 0 (the MMA's async proxy reads it)
 #endif
       WS_T(7);
+#if WS_PAIRS
+      pair_ready(warp, b, true);  // this warp's rows are ready: its producer warp may start
+      // all consumer warps finished (every packet stored) -> no round j
+      const bool stop = bar_and<kBarCons, 128>(no_more && !packet_live);
+#else
       // all consumer warps finished (every packet stored) -> the producers stop at round j
       const bool stop = bar_and<kBarCons, 128>(no_more && !packet_live);
       if (ctid == 0) s.stop[b] = stop ? 1 : 0;
       list_ready_arrive(b);
+#endif
       if (stop) stop_round = j;
       WS_T(2);
       }
@@ -829,6 +879,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       }
       if (stop_round >= 0 && jm + 1 >= stop_round) break;  // every round with rows composited
     }
+#if WS_PAIRS
+    // the producers gathered the (empty) stop round: drain it, then wake every producer warp
+    // once more with `halt` raised (written by each consumer thread before its own arrive)
+    gather_done_sync(b);
+    s.halt = 1;
+    pair_ready(warp, b + 1 == kStages ? 0 : b + 1, true);
+#endif
     ptx::tc_fence_before();
     bar_sync<kBarCons, 128>();
     ptx::tc_fence_after();
