@@ -167,18 +167,24 @@ def measured_peaks():
 
 def gather_roofline(achieved, table_log2: int):
     """The gather rate against the MEASURED rate of the same gather code in isolation
-    (tools/bench_gather.py -> profiles/r01_bench_gather.json: all 16 levels of packet-coherent
+    (tools/bench_gather.py -> profiles/r02_bench_gather.json: all 16 levels of packet-coherent
     points on this table), the attainable ceiling of an irregular fp16 gather on this GPU."""
-    try:
-        g = json.load(open(os.path.join(ROOT, "profiles", "r01_bench_gather.json")))
-        peak = g["results"][f"T2^{table_log2}_coherent"]["gather_GBs"]
-    except Exception:
+    src = None
+    for name in ("r02_bench_gather.json", "r01_bench_gather.json"):
+        try:
+            g = json.load(open(os.path.join(ROOT, "profiles", name)))
+            peak = g["results"][f"T2^{table_log2}_coherent"]["gather_GBs"]
+            src = name
+            break
+        except Exception:
+            continue
+    if src is None:
         return None
     if achieved is None:
         return None
     return {"bound": "gather", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4),
-            "peak_source": "profiles/r01_bench_gather.json (tools/bench_gather.py, coherent points)"}
+            "peak_source": f"profiles/{src} (tools/bench_gather.py, coherent points)"}
 
 
 def ncu_kernel(kernel: str):
