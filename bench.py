@@ -165,26 +165,25 @@ def measured_peaks():
         return {}
 
 
-def gather_roofline(achieved, table_log2: int):
-    """The gather rate against the MEASURED rate of the same gather code in isolation
-    (tools/bench_gather.py -> profiles/r02_bench_gather.json: all 16 levels of packet-coherent
-    points on this table), the attainable ceiling of an irregular fp16 gather on this GPU."""
+def gather_isolated(achieved, table_log2: int):
+    """The in-frame gather rate next to the same gather code run alone (tools/bench_gather.py ->
+    profiles/r02_bench_gather.json, all 16 levels of synthetic packet-coherent points on this
+    table).  A comparison, not a ceiling: real ray packets are more coherent than the synthetic
+    points, so the frame can gather faster than the isolated benchmark."""
     src = None
     for name in ("r02_bench_gather.json", "r01_bench_gather.json"):
         try:
             g = json.load(open(os.path.join(ROOT, "profiles", name)))
-            peak = g["results"][f"T2^{table_log2}_coherent"]["gather_GBs"]
+            iso = g["results"][f"T2^{table_log2}_coherent"]["gather_GBs"]
             src = name
             break
         except Exception:
             continue
-    if src is None:
+    if src is None or achieved is None:
         return None
-    if achieved is None:
-        return None
-    return {"bound": "gather", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4),
-            "peak_source": f"profiles/{src} (tools/bench_gather.py, coherent points)"}
+    return {"in_frame_GBs": round(achieved, 1), "isolated_coherent_GBs": iso,
+            "ratio": round(achieved / iso, 4), "source": f"profiles/{src}",
+            "note": "comparison with the isolated gather benchmark, not a hardware ceiling"}
 
 
 def ncu_kernel(kernel: str):
@@ -508,7 +507,7 @@ def run_ours(args):
                                     f"{level_samples / max(world, 1):.3e} level-samples in "
                                     f"{render_launches} {kname} launches, {render_ms:.1f} ms "
                                     f"(CUDA events on the launch stream)"},
-        "roofline_gather": gather_roofline(achieved, spec.table_log2),
+        "gather_isolated": gather_isolated(achieved, spec.table_log2),
         "roofline_mlp": {"bound": "tensor", "achieved": None if mlp_tflops is None else round(mlp_tflops, 2),
                          "peak": mlp_peak, "unit": "TFLOP/s",
                          "frac": None if mlp_tflops is None else round(mlp_tflops / mlp_peak, 4),
