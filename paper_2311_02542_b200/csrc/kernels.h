@@ -112,6 +112,7 @@ cudaError_t launch_render_simt(const lumi_dev::RenderParams& p, cudaStream_t s);
 cudaError_t launch_march_kept(const lumi_dev::RenderParams& p, uint32_t* mask, int32_t* counts,
                               cudaStream_t s);
 cudaError_t launch_march_mask(const lumi_dev::RenderParams& p, cudaStream_t s);
+uint32_t march_occ_bias(int res);  // RenderParams::occ_bias
 // public [pixel][word] kept mask through the production (filtered) march pass
 cudaError_t launch_march_public(lumi_dev::RenderParams p, uint32_t* mask, int32_t* counts,
                                 cudaStream_t s);

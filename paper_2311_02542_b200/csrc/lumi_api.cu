@@ -274,6 +274,7 @@ int make_params(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions
   p->mlp.color_space = m->desc.color_space;
   p->occ = m->d_occ;
   p->occ_res = m->occ_res;
+  p->occ_bias = march_occ_bias(m->occ_res);
   if ((rc = get_ts(m, cam->t_near, cam->t_far, o->samples_per_ray, &p->ts, &p->ratio))) return rc;
   p->n = o->samples_per_ray;
   p->lod_enabled = o->lod_enabled ? 1 : 0;

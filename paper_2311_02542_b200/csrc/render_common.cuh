@@ -15,6 +15,9 @@ struct RenderParams {
   MlpDev mlp;
   const uint8_t* occ;  // occ_res^3 bytes
   int occ_res;
+  uint32_t occ_bias;   // march_occ_bias(occ_res): the segment march pass's biased voxel index
+  uint32_t zero;       // always 0 (a value the compiler cannot prove uniform: keeps per-thread
+                       // copies of uniform 64-bit bases in registers)
   const double* ts;    // host-computed exponential distances (renderer.h:135-141)
   double ratio;        // host-computed pow(t_far/t_near, 1/(n-1)) (renderer.h:142)
   int n;               // samples_per_ray

@@ -150,6 +150,47 @@ def test_filtered_march_equals_exact_full_eye(lumi, torch_cuda, small, frame, co
     assert np.array_equal(fm, em)
 
 
+def _look_rot(fwd, up=(0.0, 0.0, 1.0)):
+    """Row-major world<-camera rotation whose camera z looks along `fwd`."""
+    f = np.asarray(fwd, float)
+    f /= np.linalg.norm(f)
+    x = np.cross(up, f)
+    if np.linalg.norm(x) < 1e-6:
+        x = np.cross((0.0, 1.0, 0.0), f)
+    x /= np.linalg.norm(x)
+    y = np.cross(f, x)
+    return tuple(np.stack([x, y, f], axis=1).reshape(-1).tolist())
+
+
+@pytest.mark.parametrize("pose", ["diagonal", "corner", "outside", "outside_far", "axis_tie", "nocontract_out"])
+def test_segment_march_equals_exact_off_axis(lumi, torch_cuda, small, pose):
+    """The segment march pass (inside-cube and final-pyramid segments, general test elsewhere)
+    against the exact double march on poses that stress its segment logic: diagonal views
+    (max-axis ties between |d| components), a camera near a cube corner, cameras outside the
+    cube looking in (no inside segment, late final pyramids), no contraction from outside."""
+    fwd, org, contraction = {
+        "diagonal": ((1.0, 1.0, 1.0), (0.1, -0.2, 0.05), 1),
+        "corner": ((-1.0, -0.8, -0.6), (0.93, 0.9, 0.95), 1),
+        "outside": ((-1.0, 0.3, 0.1), (1.7, -0.2, 0.3), 1),
+        "outside_far": ((-1.0, -1.0, 0.2), (3.5, 2.5, -0.4), 1),
+        "axis_tie": ((1.0, 1.0, 0.0), (0.0, 0.0, 0.0), 1),
+        "nocontract_out": ((0.0, -1.0, 0.2), (0.3, 1.6, -0.1), 0),
+    }[pose]
+    spec = scenes.pinhole(512, 512, _look_rot(fwd), org)
+    cam = lumi.CameraModel.from_spec(spec)
+    opts = lumi.RenderOptions(contraction=contraction)
+    dm = small["dm"]
+    dm.set_kernel("simt")
+    try:
+        em, ec = march_kept_gpu(torch_cuda, lumi, dm, cam, opts, 0, 512)
+    finally:
+        dm.set_kernel("ws")
+    fm, fc = march_kept_gpu(torch_cuda, lumi, dm, cam, opts, 0, 512)
+    assert ec.sum() > 0
+    assert np.array_equal(fc, ec)
+    assert np.array_equal(fm, em)
+
+
 def _render(lumi, dm, cam, opts, b=0, e=None):
     e = cam.height if e is None else e
     out = np.zeros((3, cam.height, cam.width), np.float32)
