@@ -245,25 +245,30 @@ __global__ void __launch_bounds__(256) k_gather_bench(GridDev g, int n, int cohe
 __global__ void __launch_bounds__(256) k_encode(GridDev g, int n, const float* __restrict__ pos,
                                                 const float* __restrict__ fl,
                                                 float* __restrict__ out) {
-  __shared__ uint4 lvl[kMaxLevels];
-  for (int l = threadIdx.x; l < kMaxLevels; l += blockDim.x) {
-    const int res = l < g.levels ? g.res[l] : 1;
-    const unsigned long long base =
-        reinterpret_cast<unsigned long long>(g.table16 + (l < g.levels ? g.offset2[l] : 0));
-    lvl[l] = make_uint4((uint32_t)res, ((g.dense_mask >> l) & 1u) ? 0u : g.hash_mask[l],
-                        (uint32_t)base, (uint32_t)(base >> 32));
-  }
+  __shared__ pk::LevelTab lt;
+  pk::level_tab_init(lt, g, threadIdx.x, blockDim.x);
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const float u = __saturatef((pos[3 * i] + 2.f) * 0.25f), v = __saturatef((pos[3 * i + 1] + 2.f) * 0.25f),
-              w = __saturatef((pos[3 * i + 2] + 2.f) * 0.25f);
+  const float u = pk::unit_below1((pos[3 * i] + 2.f) * 0.25f), v = pk::unit_below1((pos[3 * i + 1] + 2.f) * 0.25f),
+              w = pk::unit_below1((pos[3 * i + 2] + 2.f) * 0.25f);
   const float f = fl[i];
-  for (int l = 0; l < g.levels; ++l) {
-    const float wl = __saturatef(f - (float)l);
-    const float2 r = wl > 0.f ? pk::gather_level(lvl[l], u, v, w, wl) : make_float2(0.f, 0.f);
-    out[(size_t)i * 2 * g.levels + 2 * l] = r.x;
-    out[(size_t)i * 2 * g.levels + 2 * l + 1] = r.y;
+  // the renderer's producer code: chunks of four levels, the levels past this sample's last
+  // active one not loaded (weight 0 either way)
+  int na = 0;
+  for (int l = 0; l < g.levels; ++l)
+    if (__saturatef(f - (float)l) > 0.f) na = l + 1;
+  for (int c = 0; c < kMaxLevels / 4; ++c) {
+    const int nq = min(4, na - 4 * c);
+    const uint4 q4 = nq > 0 ? pk::gather_chunk4(lt, 4 * c, nq, u, v, w, f) : make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t qs[4] = {q4.x, q4.y, q4.z, q4.w};
+    for (int q = 0; q < 4; ++q) {
+      const int l = 4 * c + q;
+      if (l >= g.levels) break;
+      const float2 r = __half22float2(*reinterpret_cast<const __half2*>(&qs[q]));
+      out[(size_t)i * 2 * g.levels + 2 * l] = r.x;
+      out[(size_t)i * 2 * g.levels + 2 * l + 1] = r.y;
+    }
   }
 }
 

@@ -197,6 +197,159 @@ __device__ __forceinline__ float2 gather_level(uint4 L, float u, float v, float 
   return gather_combine(e, g.fu, g.fv, g.fs, wl);
 }
 
+// ---- the production gather: four levels (one 16-byte A chunk) of one sample -----------------
+// MultiResHashGrid::corners + encode (grid.h:96-113, 144-167) restated for the fp16 table:
+//  * cell and fractions of TWO levels at once in packed f32x2: p = u r rounded down (u < 1, so
+//    p < r and no clamp to res - 1 is needed), b = p + 2^23 rounded down holds floor(p) in its
+//    low mantissa bits (b = 0x4B000000 + floor(p) as an integer), f = p - (b - 2^23);
+//  * corner indices straight off those biased bits: the bias is folded into per-level addends
+//    (dense: idx = x + y V + z V^2; hashed: (x ^ y P1 ^ z P2) & mask, where the mask < 2^24
+//    strips the bias bits of x), dense corners x+1 as a +4-byte load offset;
+//  * the trilinear value as seven packed-fp16 lerps with the (fu, fv) and (fs, w_l) pairs
+//    converted once each (operand swizzles select the halves).
+struct LevelTab {
+  float res[kMaxLevels];       // resolution as float
+  uint32_t mask[kMaxLevels];   // hashed: table entries - 1; dense: 0
+  uint32_t m1[kMaxLevels];     // y multiplier: dense V = res + 1, hashed 2654435761
+  uint32_t m2[kMaxLevels];     // z multiplier: dense V^2, hashed 805459861
+  uint32_t k1[kMaxLevels];     // y addend folding the bias (and, dense, x's bias)
+  uint32_t k2[kMaxLevels];     // z addend folding the bias
+  unsigned long long base[kMaxLevels];  // the level's first fp16 entry pair (byte address)
+};
+
+constexpr uint32_t kFloorBias = 0x4B000000u;  // bits of 2^23
+
+// fill one CTA's table (any thread count; call before a barrier)
+__device__ __forceinline__ void level_tab_init(LevelTab& t, const GridDev& g, int tid, int nthreads) {
+  for (int l = tid; l < kMaxLevels; l += nthreads) {
+    const bool live = l < g.levels;
+    const uint32_t res = live ? (uint32_t)g.res[l] : 1u;
+    const bool dense = live && ((g.dense_mask >> l) & 1u);
+    const uint32_t V = res + 1u;
+    t.res[l] = (float)res;
+    t.mask[l] = dense ? 0u : (live ? g.hash_mask[l] : 0u);
+    t.m1[l] = dense ? V : 2654435761u;
+    t.m2[l] = dense ? V * V : 805459861u;
+    // dense: y_b V + k1 = y V - C (y_b = C + y, so k1 = -C (V + 1)): x's bias cancels in the sum
+    t.k1[l] = dense ? 0u - kFloorBias * (V + 1u) : 0u - kFloorBias * 2654435761u;
+    t.k2[l] = dense ? 0u - kFloorBias * (V * V) : 0u - kFloorBias * 805459861u;
+    t.base[l] = reinterpret_cast<unsigned long long>(g.table16 + (live ? g.offset2[l] : 0));
+  }
+}
+
+__device__ __forceinline__ uint64_t f2pk(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2upk(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+
+// floor bits and fractions of coordinate a at the two resolutions r2 (levels l, l + 1)
+__device__ __forceinline__ void cell2(float a, uint64_t r2, uint32_t& b0, uint32_t& b1, float& f0, float& f1) {
+  uint64_t p, b, fl, f;
+  asm("mul.rm.f32x2 %0, %1, %2;" : "=l"(p) : "l"(f2pk(a, a)), "l"(r2));
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(b) : "l"(p), "l"(f2pk(8388608.f, 8388608.f)));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(fl) : "l"(b), "l"(f2pk(-8388608.f, -8388608.f)));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f) : "l"(p), "l"(fl));
+  const float2 bb = f2upk(b), ff = f2upk(f);
+  b0 = __float_as_uint(bb.x);
+  b1 = __float_as_uint(bb.y);
+  f0 = ff.x;
+  f1 = ff.y;
+}
+
+__device__ __forceinline__ __half2 lerp7(const __half2* e, __half2 huv, __half2 hsw) {
+  const __half2 hu = __low2half2(huv), hv = __high2half2(huv), hs = __low2half2(hsw);
+  const __half2 x00 = __hfma2(__hsub2(e[1], e[0]), hu, e[0]), x10 = __hfma2(__hsub2(e[3], e[2]), hu, e[2]),
+                x01 = __hfma2(__hsub2(e[5], e[4]), hu, e[4]), x11 = __hfma2(__hsub2(e[7], e[6]), hu, e[6]);
+  const __half2 y0 = __hfma2(__hsub2(x10, x00), hv, x00), y1 = __hfma2(__hsub2(x11, x01), hv, x01);
+  return __hmul2(__hfma2(__hsub2(y1, y0), hs, y0), __high2half2(hsw));
+}
+
+// (a ^ b) & c in one LOP3 (immediate 0x28: (0xF0 ^ 0xCC) & 0xAA)
+__device__ __forceinline__ uint32_t xor_and(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// the 8 corner entries of one level (biased cell bits xb, yb, zb)
+__device__ __forceinline__ void corners8(const LevelTab& t, int l, uint32_t xb, uint32_t yb, uint32_t zb,
+                                         __half2* e) {
+  const uint32_t m1 = t.m1[l], m2 = t.m2[l], mask = t.mask[l];
+  const uint32_t hy0 = yb * m1 + t.k1[l], hy1 = hy0 + m1;
+  const uint32_t hz0 = zb * m2 + t.k2[l], hz1 = hz0 + m2;
+  const __half2* base = reinterpret_cast<const __half2*>(t.base[l]);
+  if (mask == 0u) {  // dense: x + y V + z V^2, x + 1 one entry on
+    const uint32_t i0 = xb + hy0 + hz0, i2 = xb + hy1 + hz0, i4 = xb + hy0 + hz1, i6 = xb + hy1 + hz1;
+    const __half2 *p0 = base + i0, *p2 = base + i2, *p4 = base + i4, *p6 = base + i6;
+    e[0] = __ldg(p0);
+    e[1] = __ldg(p0 + 1);
+    e[2] = __ldg(p2);
+    e[3] = __ldg(p2 + 1);
+    e[4] = __ldg(p4);
+    e[5] = __ldg(p4 + 1);
+    e[6] = __ldg(p6);
+    e[7] = __ldg(p6 + 1);
+  } else {  // hashed (grid.h:50-52): (x ^ yz) & mask as ONE three-input LOP3 per corner
+    const uint32_t xb1 = xb + 1u;
+    const uint32_t yz00 = hy0 ^ hz0, yz10 = hy1 ^ hz0, yz01 = hy0 ^ hz1, yz11 = hy1 ^ hz1;
+    e[0] = __ldg(base + xor_and(xb, yz00, mask));
+    e[1] = __ldg(base + xor_and(xb1, yz00, mask));
+    e[2] = __ldg(base + xor_and(xb, yz10, mask));
+    e[3] = __ldg(base + xor_and(xb1, yz10, mask));
+    e[4] = __ldg(base + xor_and(xb, yz01, mask));
+    e[5] = __ldg(base + xor_and(xb1, yz01, mask));
+    e[6] = __ldg(base + xor_and(xb, yz11, mask));
+    e[7] = __ldg(base + xor_and(xb1, yz11, mask));
+  }
+}
+
+// Levels l0 .. l0 + 3 of one sample: (u, v, w) in [0, 1) (the caller clamps below 1), fl the LOD
+// as w_l = saturate(fl - l); nq (warp-uniform) = how many of the four levels any lane needs --
+// the others are not loaded and come out zero.  Returns the four half2 features.
+__device__ __forceinline__ uint4 gather_chunk4(const LevelTab& t, int l0, int nq, float u, float v, float w,
+                                               float fl) {
+  uint32_t xb[4], yb[4], zb[4];
+  float fu[4], fv[4], fs[4];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const uint64_t r2 = *reinterpret_cast<const uint64_t*>(&t.res[l0 + 2 * j]);
+    cell2(u, r2, xb[2 * j], xb[2 * j + 1], fu[2 * j], fu[2 * j + 1]);
+    cell2(v, r2, yb[2 * j], yb[2 * j + 1], fv[2 * j], fv[2 * j + 1]);
+    cell2(w, r2, zb[2 * j], zb[2 * j + 1], fs[2 * j], fs[2 * j + 1]);
+  }
+  __half2 e[4][8];
+  if (nq == 4) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) corners8(t, l0 + q, xb[q], yb[q], zb[q], e[q]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < nq) {
+        corners8(t, l0 + q, xb[q], yb[q], zb[q], e[q]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) e[q][k] = __half2{};
+      }
+    }
+  }
+  uint32_t f[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float wl = __saturatef(fl - (float)(l0 + q));
+    f[q] = h2u(lerp7(e[q], __floats2half2_rn(fu[q], fv[q]), __floats2half2_rn(fs[q], wl)));
+  }
+  return make_uint4(f[0], f[1], f[2], f[3]);
+}
+
+// the clamp every caller of gather_chunk4 applies: [0, 1] -> [0, 1 - 2^-24]
+__device__ __forceinline__ float unit_below1(float x) { return fminf(__saturatef(x), 0.99999994f); }
+
 // trunc_exp / sigmoid (network.h:41-57) with the MUFU exp2 / reciprocal: ~2 ulp, far below the
 // fp16 MLP operands' 1.6e-4 (oracle-measured)
 __device__ __forceinline__ float trunc_exp_fast(float x) {

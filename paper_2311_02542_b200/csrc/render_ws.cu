@@ -102,6 +102,11 @@ constexpr int kConsLevels = WS_CONS_LEVELS;  // LOD levels gathered by the consu
 #ifndef WS_ROWMAJOR
 #define WS_ROWMAJOR 1
 #endif
+// WS_GATHER2: the producers run pk::gather_chunk4 (packed-f32x2 cells off biased float bits,
+// bias-folded corner indices, dense x+1 as a load offset); 0 = the round-1/2 gather_prep path
+#ifndef WS_GATHER2
+#define WS_GATHER2 1
+#endif
 #ifndef WS_F32_ALPHA
 #define WS_F32_ALPHA 1
 #endif
@@ -172,6 +177,7 @@ struct __align__(16) Smem {
   int stop[kStages];
   int halt;  // WS_PAIRS: the consumers have stopped (no further round)
   uint4 lvl[kMaxLevels];
+  LevelTab lt;
   float4 samp[kStages][128];
   uint8_t na[kStages][128];                  // per row: active LOD levels (0 = no sample)
 #if !WS_ROWMAJOR
@@ -325,6 +331,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
     s.lvl[l] = make_uint4((uint32_t)res, dense ? 0u : p.grid.hash_mask[l], (uint32_t)base,
                           (uint32_t)(base >> 32));
   }
+  level_tab_init(s.lt, p.grid, tid, kCtaThreads);
   if (tid == 0) {
     s.halt = 0;
     ptx::mbar_init(&s.mbar, 1);
@@ -380,6 +387,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         for (int c = 0; c < kMaxLevels / 4; ++c) {  // A chunk c = levels 4c .. 4c + 3
           uint4 out = make_uint4(0u, 0u, 0u, 0u);
           const int nq = min(4, na_max - 4 * c);  // levels of the chunk active in some lane (uniform)
+#if WS_GATHER2
+          // a lane whose row has fewer levels than the warp's longest gathers the level anyway
+          // (a valid cell next to its neighbours') with weight 0
+          if (nq > 0) out = gather_chunk4(s.lt, 4 * c, nq, P.x, P.y, P.z, P.w);
+          (void)na;
+#else
           if (nq > 0) {
             const float fl0 = P.w - (float)(4 * c);
             GatherPrep gp[4];
@@ -412,6 +425,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
             for (int q = 0; q < 4; ++q) f[q] = h2u(gather_combine_h(e[q], gp[q].fu, gp[q].fv, gp[q].fs, wl[q]));
             out = make_uint4(f[0], f[1], f[2], f[3]);
           }
+#endif
           st16(s.A[b], a_off(ctid, c), out);
         }
       }
@@ -678,9 +692,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       if (have) {
         const float t = (float)__ldg(p.ts + cand);
         const float3 c = contract_f(make_float3(o.x + dx * t, o.y + dy * t, o.z + dz * t), p.contraction);
-        u = __saturatef((c.x + 2.f) * 0.25f);
-        v = __saturatef((c.y + 2.f) * 0.25f);
-        w = __saturatef((c.z + 2.f) * 0.25f);
+        u = unit_below1((c.x + 2.f) * 0.25f);  // [0, 1): the gather's cells need no clamp
+        v = unit_below1((c.y + 2.f) * 0.25f);
+        w = unit_below1((c.z + 2.f) * 0.25f);
         if (p.lod_enabled) {
           const float3 bq = contract_f(make_float3(o.x + nx * t, o.y + ny * t, o.z + nz * t), p.contraction);
           const float ex = c.x - bq.x, ey = c.y - bq.y, ez = c.z - bq.z;

@@ -17,7 +17,22 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// LUMI_MBAR_HINT: the try_wait carries a suspend-time hint, so a waiting warp sleeps until the
+// phase completes (or the hint expires) instead of re-issuing the test in a tight loop -- the
+// consumers' MMA waits would otherwise take issue slots from the producers' gather
+#ifndef LUMI_MBAR_HINT
+#define LUMI_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if LUMI_MBAR_HINT
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "LAB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra LAB_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity), "n"(LUMI_MBAR_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "LAB_WAIT_%=:\n\t"
@@ -25,6 +40,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra LAB_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // the arrival that also announces `bytes` of asynchronous (TMA) transactions on the barrier
