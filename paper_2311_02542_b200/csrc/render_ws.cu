@@ -107,6 +107,12 @@ constexpr int kConsLevels = WS_CONS_LEVELS;  // LOD levels gathered by the consu
 #ifndef WS_GATHER2
 #define WS_GATHER2 1
 #endif
+// WS_PROD_GEOM: the producers compute each row's sample geometry (position, contraction, LOD
+// footprint and weights) from the row's ray directions and candidate, which the consumers pass
+// through shared memory -- the consumers' fill phase loses its heaviest part
+#ifndef WS_PROD_GEOM
+#define WS_PROD_GEOM 1
+#endif
 #ifndef WS_F32_ALPHA
 #define WS_F32_ALPHA 1
 #endif
@@ -179,6 +185,10 @@ struct __align__(16) Smem {
   uint4 lvl[kMaxLevels];
   LevelTab lt;
   float4 samp[kStages][128];
+#if WS_PROD_GEOM
+  float4 rdir[kStages][128];   // per row: ray direction xyz + neighbour direction x
+  float2 rdir2[kStages][128];  // neighbour direction yz
+#endif
   uint8_t na[kStages][128];                  // per row: active LOD levels (0 = no sample)
 #if !WS_ROWMAJOR
   uint16_t pairs[kWarps * 32 * kMaxLevels];  // the round's gather list, warp lists concatenated
@@ -286,6 +296,35 @@ __device__ __forceinline__ void gather_done_arrive(int b) {
   else bar_arrive<kBarGather + 2, kCtaThreads>();
 }
 
+// One row's sample geometry (renderer.h:205-222 in fp32): position o + d t, contraction, the
+// grid coordinates (u, v, w) in [0, 1), the LOD footprint against the neighbour ray and the
+// weights as fl (w_l = saturate(fl - l)); returns the active level count (0: no sample).
+struct GeomConst {
+  float3 o;
+  float two_base, inv_log, bias;
+  int levels;
+};
+__device__ __forceinline__ int row_geometry(const RenderParams& p, const GeomConst& gc, float3 d, float3 nd,
+                                            int cand, float4& out) {
+  const float t = (float)__ldg(p.ts + cand);
+  const float3 c = contract_f(make_float3(gc.o.x + d.x * t, gc.o.y + d.y * t, gc.o.z + d.z * t), p.contraction);
+  const float u = unit_below1((c.x + 2.f) * 0.25f);  // [0, 1): the gather's cells need no clamp
+  const float v = unit_below1((c.y + 2.f) * 0.25f);
+  const float w = unit_below1((c.z + 2.f) * 0.25f);
+  LodW lw;
+  if (p.lod_enabled) {
+    const float3 bq = contract_f(make_float3(gc.o.x + nd.x * t, gc.o.y + nd.y * t, gc.o.z + nd.z * t), p.contraction);
+    const float ex = c.x - bq.x, ey = c.y - bq.y, ez = c.z - bq.z;
+    const float rc = fmaxf(0.5f * sqrtf(ex * ex + ey * ey + ez * ez), 1e-12f);
+    const float l = fminf(-__logf(gc.two_base * rc) * gc.inv_log, (float)(gc.levels - 1));
+    lw = lod_weights_f(l + gc.bias, gc.levels);
+  } else {
+    lw = LodW{gc.levels, 0.f, false};
+  }
+  out = make_float4(u, v, w, lw.floor_only ? 1e-4f : (float)lw.full + lw.frac);
+  return active_levels(lw, gc.levels);
+}
+
 __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
@@ -365,6 +404,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
 
   if (wg == 1) {
     // ================================ producers ==============================================
+#if WS_PROD_GEOM
+    const GeomConst gc{make_float3((float)p.cam.origin[0], (float)p.cam.origin[1], (float)p.cam.origin[2]),
+                       (float)p.grid.two_base, (float)(1.0 / p.grid.log_scale), (float)p.lod_bias,
+                       p.grid.levels};
+    unsigned pcnt_levels = 0;
+#endif
     int b = 0;  // j % kStages
 #pragma unroll 1
     for (int j = 0;; ++j, b = b + 1 == kStages ? 0 : b + 1) {
@@ -379,9 +424,23 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
 #endif
 #if WS_ROWMAJOR
       {
+#if WS_PROD_GEOM
+        // row ctid: its ray directions and candidate from the consumers -> grid coordinates,
+        // LOD (fl) and active level count
+        float4 P = make_float4(0.f, 0.f, 0.f, 0.f);
+        int na = 0;
+        if (s.na[b][ctid]) {
+          const float4 d4 = s.rdir[b][ctid];
+          const float2 d2 = s.rdir2[b][ctid];
+          na = row_geometry(p, gc, make_float3(d4.x, d4.y, d4.z), make_float3(d4.w, d2.x, d2.y),
+                            s.rowcand[b][warp][lane], P);
+          pcnt_levels += (unsigned)na;
+        }
+#else
         // row ctid: grid coordinates + LOD (fl) and its active level count, from the consumers
         const float4 P = s.samp[b][ctid];
         const int na = s.na[b][ctid];
+#endif
         const int na_max = __reduce_max_sync(FULL, (unsigned)na);
 #pragma unroll 1
         for (int c = 0; c < kMaxLevels / 4; ++c) {  // A chunk c = levels 4c .. 4c + 3
@@ -501,6 +560,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       WS_T(1);
 #endif
     }
+#if WS_PROD_GEOM
+    add_work_stats(p, 0, pcnt_levels, 0, 0);
+#endif
   } else {
     // ================================ consumers ==============================================
     if (tma_weights) ptx::mbar_wait(&s.wbar, 0);  // the weight tiles have landed
@@ -686,6 +748,16 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
                   dz = __shfl_sync(FULL, r.d.z, rl);
       const float nx = __shfl_sync(FULL, r.nd.x, rl), ny = __shfl_sync(FULL, r.nd.y, rl),
                   nz = __shfl_sync(FULL, r.nd.z, rl);
+#if WS_PROD_GEOM
+      // the producers derive the row's geometry: pass its ray directions (the candidate is in
+      // rowcand) and a has-sample flag
+      if (have) {
+        s.rdir[b][ctid] = make_float4(dx, dy, dz, nx);
+        s.rdir2[b][ctid] = make_float2(ny, nz);
+        ++cnt.evals;
+      }
+      s.na[b][ctid] = have ? 1 : 0;
+#else
       float u = 0.f, v = 0.f, w = 0.f;
       LodW lw{0, 0.f, false};
       int na = 0;
@@ -732,6 +804,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         if (lane == 0) s.cnt[b][warp] = wsum;
 #endif
       }
+#endif  // WS_PROD_GEOM
 #if !WS_ROWMAJOR
       ptx::fence_async_smem();  // A chunk 0 (the MMA's async proxy reads it)
 #endif
