@@ -184,7 +184,9 @@ struct __align__(16) Smem {
   int halt;  // WS_PAIRS: the consumers have stopped (no further round)
   uint4 lvl[kMaxLevels];
   LevelTab lt;
-  float4 samp[kStages][128];
+#if !WS_PROD_GEOM || !WS_ROWMAJOR
+  float4 samp[kStages][128];  // per row: grid coordinates + LOD (fl), from the consumers
+#endif
 #if WS_PROD_GEOM
   float4 rdir[kStages][128];   // per row: ray direction xyz + neighbour direction x
   float2 rdir2[kStages][128];  // neighbour direction yz
