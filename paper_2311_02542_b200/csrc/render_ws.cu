@@ -113,6 +113,11 @@ constexpr int kConsLevels = WS_CONS_LEVELS;  // LOD levels gathered by the consu
 #ifndef WS_PROD_GEOM
 #define WS_PROD_GEOM 1
 #endif
+// WS_FILL_TRANSPOSE: a new mask word's per-candidate ray sets by one 32x32 bit transpose across
+// the warp (5 shuffle stages) and a scan, instead of 32 ballots with a serial running count
+#ifndef WS_FILL_TRANSPOSE
+#define WS_FILL_TRANSPOSE 1
+#endif
 #ifndef WS_F32_ALPHA
 #define WS_F32_ALPHA 1
 #endif
@@ -718,6 +723,26 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
 #else
         const uint32_t bits = r.alive ? __ldg(p.kept_mask + (size_t)word * p.total_rays + r.id) : 0u;
 #endif
+#if WS_FILL_TRANSPOSE
+        // lane i: the rays keeping candidate word * 32 + i (a 32x32 bit transpose instead of 32
+        // ballots), then an exclusive scan of the per-candidate counts
+        {
+          const uint32_t col = warp_transpose32(bits);
+          const int cnt_c = __popc(col);
+          int incl = cnt_c;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, off);
+            if (lane >= off) incl += v;
+          }
+          s.ballot[warp][lane] = col;
+          s.prefix[warp][lane] = (uint16_t)(incl - cnt_c);
+          if (lane == 31) s.prefix[warp][32] = (uint16_t)incl;
+          __syncwarp();
+          g_next = 0;
+          word_total = __shfl_sync(FULL, incl, 31);
+        }
+#else
         int run = 0;
         for (int i = 0; i < 32; ++i) {
           const uint32_t bb = __ballot_sync(FULL, (bits >> i) & 1u);
@@ -731,6 +756,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         __syncwarp();
         g_next = 0;
         word_total = run;
+#endif
 #endif
       }
       WS_T(6);
