@@ -118,6 +118,18 @@ constexpr int kConsLevels = WS_CONS_LEVELS;  // LOD levels gathered by the consu
 #ifndef WS_FILL_TRANSPOSE
 #define WS_FILL_TRANSPOSE 1
 #endif
+// WS_PROD_DIRS: the producers also load each row's ray directions (march-pass SoA planes, by the
+// packet id and ray lane the consumers pass) and hand the direction back for the SH encoding;
+// the consumers keep no directions and a new packet costs them no loads but its first mask
+// word, which is prefetched one packet ahead
+#ifndef WS_PROD_DIRS
+#define WS_PROD_DIRS 0  // measured -6 %: the direction loads lengthen the producers' critical path
+#endif
+// WS_NEXT_FIRST: the next packet's first mask word is loaded one round after the next packet id
+// (so a new packet's first word switch does not wait on a load)
+#ifndef WS_NEXT_FIRST
+#define WS_NEXT_FIRST 1
+#endif
 #ifndef WS_F32_ALPHA
 #define WS_F32_ALPHA 1
 #endif
@@ -182,6 +194,7 @@ struct __align__(16) Smem {
   uint32_t own[kStages][kWarps][32];
   uint16_t rowcand[kStages][kWarps][32];
   uint8_t rowlane[kStages][128];
+  int rowpkt[kStages][kWarps];  // per warp: the packet of the round's rows
   uint64_t mbar;
   uint64_t wbar;  // the weight tiles' TMA bulk copy
   uint32_t tmem_base;
@@ -194,7 +207,9 @@ struct __align__(16) Smem {
 #endif
 #if WS_PROD_GEOM
   float4 rdir[kStages][128];   // per row: ray direction xyz + neighbour direction x
+#if !WS_PROD_DIRS
   float2 rdir2[kStages][128];  // neighbour direction yz
+#endif
 #endif
   uint8_t na[kStages][128];                  // per row: active LOD levels (0 = no sample)
 #if !WS_ROWMAJOR
@@ -437,10 +452,19 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         float4 P = make_float4(0.f, 0.f, 0.f, 0.f);
         int na = 0;
         if (s.na[b][ctid]) {
+#if WS_PROD_DIRS
+          const size_t T = (size_t)p.total_rays;
+          const float* rd = p.ray_dirs + ((size_t)s.rowpkt[b][warp] * 32 + s.rowlane[b][ctid]);
+          const float3 d = make_float3(__ldg(rd), __ldg(rd + T), __ldg(rd + 2 * T));
+          const float3 nd = make_float3(__ldg(rd + 3 * T), __ldg(rd + 4 * T), __ldg(rd + 5 * T));
+          s.rdir[b][ctid] = make_float4(d.x, d.y, d.z, 0.f);  // for the consumers' SH encoding
+          na = row_geometry(p, gc, d, nd, s.rowcand[b][warp][lane], P);
+#else
           const float4 d4 = s.rdir[b][ctid];
           const float2 d2 = s.rdir2[b][ctid];
           na = row_geometry(p, gc, make_float3(d4.x, d4.y, d4.z), make_float3(d4.w, d2.x, d2.y),
                             s.rowcand[b][warp][lane], P);
+#endif
           pcnt_levels += (unsigned)na;
         }
 #else
@@ -604,6 +628,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
     if (lane == 0) next_pkt = (long long)atomicAdd(p.work_counter, 1u);
     uint32_t next_bits = 0;
 #endif
+#if WS_NEXT_FIRST
+    // the next packet's first mask word, loaded once its id has arrived (the round after the
+    // atomic was issued)
+    uint32_t next_first = 0;
+    bool nf_ready = false;
+#endif
     uint32_t phase = 0;
     long long pkt_cycles = 0;  // this warp's cycles on its current packet (RowStats.ms diagnostic)
 
@@ -614,6 +644,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       if (stop_round < 0) {
       // ---- F(j): this warp's rows of round j from its packet stream -----------------------
       int take = 0, rl = lane, cand = 0;
+#if WS_NEXT_FIRST
+      if (!nf_ready) {
+        const long long np = __shfl_sync(FULL, next_pkt, 0);
+        next_first = np < total_packets ? __ldg(p.kept_mask + np * 32 + lane) : 0u;
+        nf_ready = true;
+      }
+#endif
       while (take < 32 && !no_more && !pending) {
         if (!packet_live) {
           long long pkt = 0;
@@ -639,7 +676,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           r.valid = px_ < p.cam.width && py_ < p.row_end;
           r.alive = r.valid;
           if (r.valid) {
-#if WS_MARCH_DIRS
+#if WS_PROD_DIRS
+#elif WS_MARCH_DIRS
             const size_t T = (size_t)p.total_rays;
             const float* rd = p.ray_dirs + rid;
             r.d = make_float3(__ldg(rd), __ldg(rd + T), __ldg(rd + 2 * T));
@@ -661,6 +699,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           g_next = word_total = 0;
 #if WS_TMASK
           next_bits = __ldg(p.kept_mask + r.id);  // lane = candidate of word 0: its rays
+#elif WS_NEXT_FIRST
+          next_bits = next_first;  // (bits of invalid rays are masked by r.alive)
+          nf_ready = false;
 #elif WS_PREFETCH
           next_bits = r.valid ? __ldg(p.kept_mask + r.id) : 0u;
 #endif
@@ -772,16 +813,22 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         s.rowlane[b][ctid] = (uint8_t)rl;
         __syncwarp();
       }
+#if WS_PROD_DIRS
+      if (lane == 0) s.rowpkt[b][warp] = r.id >> 5;
+#else
       const float dx = __shfl_sync(FULL, r.d.x, rl), dy = __shfl_sync(FULL, r.d.y, rl),
                   dz = __shfl_sync(FULL, r.d.z, rl);
       const float nx = __shfl_sync(FULL, r.nd.x, rl), ny = __shfl_sync(FULL, r.nd.y, rl),
                   nz = __shfl_sync(FULL, r.nd.z, rl);
+#endif
 #if WS_PROD_GEOM
       // the producers derive the row's geometry: pass its ray directions (the candidate is in
       // rowcand) and a has-sample flag
       if (have) {
+#if !WS_PROD_DIRS
         s.rdir[b][ctid] = make_float4(dx, dy, dz, nx);
         s.rdir2[b][ctid] = make_float2(ny, nz);
+#endif
         ++cnt.evals;
       }
       s.na[b][ctid] = have ? 1 : 0;
@@ -859,8 +906,14 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         gather_done_sync(bp);
         WS_T(3);
         const int rlp = s.rowlane[bp][ctid];
+#if WS_PROD_DIRS
+        const float4 pd4 = s.rdir[bp][ctid];  // written by the producers (rows without a sample: stale, unused)
+        const float pdx = pd4.x, pdy = pd4.y, pdz = pd4.z;
+        (void)rlp;
+#else
         const float pdx = __shfl_sync(FULL, r.d.x, rlp), pdy = __shfl_sync(FULL, r.d.y, rlp),
                     pdz = __shfl_sync(FULL, r.d.z, rlp);
+#endif
         float v32[32];
         if (issuer) {
           ptx::tc_fence_after();
