@@ -184,7 +184,7 @@ cudaError_t launch_mlp_batch(const MlpDev& mlp, const void* feat, const float* d
 // ---- the hash-grid gather in isolation: the attainable gather rate ----------------------
 // report the gather against a measured gather peak (the table of C1/C2 is
 // L2-resident, so HBM is the wrong denominator there).  Every thread evaluates all levels of
-// one point with the renderer's own gather_level (fp16 table, 8 corners, fp16 weights, FHFMA);
+// one point with the renderer's own gather_chunk4 (fp16 table, 8 corners, packed-fp16 lerps);
 // points are either uniform random (no reuse between neighbouring threads) or coherent (the
 // 32 lanes of a warp sample a small neighbourhood, like a packet of neighbouring rays).
 namespace lumi_dev {
@@ -201,14 +201,8 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 __device__ __forceinline__ float u01(uint32_t h) { return (h >> 8) * (1.f / 16777216.f); }
 
 __global__ void __launch_bounds__(256) k_gather_bench(GridDev g, int n, int coherent, float* out) {
-  __shared__ uint4 lvl[kMaxLevels];
-  for (int l = threadIdx.x; l < kMaxLevels; l += blockDim.x) {
-    const int res = l < g.levels ? g.res[l] : 1;
-    const unsigned long long base =
-        reinterpret_cast<unsigned long long>(g.table16 + (l < g.levels ? g.offset2[l] : 0));
-    lvl[l] = make_uint4((uint32_t)res, ((g.dense_mask >> l) & 1u) ? 0u : g.hash_mask[l],
-                        (uint32_t)base, (uint32_t)(base >> 32));
-  }
+  __shared__ pk::LevelTab lt;
+  pk::level_tab_init(lt, g, threadIdx.x, blockDim.x);
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -223,17 +217,19 @@ __global__ void __launch_bounds__(256) k_gather_bench(GridDev g, int n, int cohe
     v = u01(hash32(3u * i + 2u));
     w = u01(hash32(3u * i + 3u));
   }
+  // the renderer's producer gather: four levels (32 corner loads) in flight per chunk, every
+  // level at weight 1
+  const float fl = (float)g.levels;
   float acc = 0.f;
-  // four levels in flight per thread (32 independent corner loads), the most ILP the
-  // renderer's producers could hold in registers
 #pragma unroll 1
-  for (int l0 = 0; l0 < g.levels; l0 += 4) {
-    float2 f[4];
+  for (int c = 0; 4 * c < g.levels; ++c) {
+    const uint4 q = pk::gather_chunk4(lt, 4 * c, min(4, g.levels - 4 * c), u, v, w, fl);
+    const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      f[q] = l0 + q < g.levels ? pk::gather_level(lvl[l0 + q], u, v, w, 1.f) : make_float2(0.f, 0.f);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc += f[q].x + f[q].y;
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qs[k]));
+      acc += f.x + f.y;
+    }
   }
   out[i] = acc;
 }
@@ -241,7 +237,7 @@ __global__ void __launch_bounds__(256) k_gather_bench(GridDev g, int n, int cohe
 // The production encoding of n given samples (parity of the renderer's gather, grid.h:90-114):
 // contracted positions [n][3] -> u = saturate((c + 2) / 4) as the render kernel computes it,
 // LOD weights carried as fl (w_l = saturate(fl - l), the kernel's representation), every
-// active level through pk::gather_level -> features [n][2 * levels] fp32 (zeros for w_l = 0).
+// active level through pk::gather_chunk4 -> features [n][2 * levels] fp32 (zeros for w_l = 0).
 __global__ void __launch_bounds__(256) k_encode(GridDev g, int n, const float* __restrict__ pos,
                                                 const float* __restrict__ fl,
                                                 float* __restrict__ out) {

@@ -23,10 +23,6 @@ constexpr uint32_t kShCol = 112;
 constexpr uint32_t kOnesCol = 120;
 constexpr int kKb = 16;              // every layer's bias is one extra K = 16 step
 constexpr int kAch = (32 + kKb) / 8; // 8-element K chunks of the layer-1 A tile
-#ifndef LUMI_PK_PAIRS
-#define LUMI_PK_PAIRS 3
-#endif
-constexpr int kPairs = LUMI_PK_PAIRS;  // (sample, level) pairs per lane per gather step
 
 
 __device__ __forceinline__ uint32_t core_off(int row, int chunk, int kchunks) {
@@ -34,15 +30,9 @@ __device__ __forceinline__ uint32_t core_off(int row, int chunk, int kchunks) {
 }
 
 // The layer-1 A tile is chunk-major (all 128 rows of an 8-element K chunk contiguous; core
-// matrices LBO = 2048 B along K, SBO = 128 B along M), so row r, chunk c starts at c*2048 + r*16
-// and a (sample, level) feature pair lands at a byte offset that IS its gather-list code:
-// src*16 | (l & 3)*4 | (l >> 2)*2048 within the warp's 32 rows.
+// matrices LBO = 2048 B along K, SBO = 128 B along M), so row r, chunk c starts at c*2048 + r*16.
 constexpr uint32_t kALbo = 2048;
 __device__ __forceinline__ uint32_t a_off(int row, int chunk) { return (uint32_t)(chunk * kALbo + row * 16); }
-__device__ __forceinline__ uint32_t pair_code(int src, int l) {
-  return (uint32_t)((src << 4) | ((l & 3) << 2) | ((l >> 2) << 11));
-}
-__device__ __forceinline__ int pair_level(uint32_t code) { return (int)(((code >> 2) & 3u) | ((code >> 9) & 12u)); }
 
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
@@ -115,7 +105,26 @@ __device__ __forceinline__ uint32_t pack2_relu(float lo, float hi) {
 
 // hidden-layer epilogue into TMEM: D row (64 fp32, bias included), ReLU, fp16 pairs -> the A
 // columns of this thread's lane for the next layer
+#ifndef LUMI_EPI_PAIR
+#define LUMI_EPI_PAIR 0
+#endif
 __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane) {
+#if LUMI_EPI_PAIR
+  // two 16-column loads per wait (32 values live)
+#pragma unroll
+  for (int h = 0; h < 4; h += 2) {
+    float v[32];
+    ptx::tmem_ld16(t_lane + 16 * h, v);
+    ptx::tmem_ld16(t_lane + 16 * h + 16, v + 16);
+    ptx::tmem_ld_wait();
+    uint32_t w[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) w[j] = pack2_relu(v[2 * j], v[2 * j + 1]);
+    ptx::tmem_st16(a_lane + 8 * h, w);
+  }
+  ptx::tmem_st_wait();
+  return;
+#endif
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
     float v[16];
@@ -127,74 +136,6 @@ __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane)
     ptx::tmem_st8(a_lane + 8 * h, w);
   }
   ptx::tmem_st_wait();
-}
-
-// One hash-grid level of one sample from the fp16 table (grid.h:96-113, 144-167): fp32 grid
-// coordinates, 32-bit entry indices off the level's base address, fp16 trilinear weights
-// (HMUL2) accumulated in fp32 by FHFMA in two interleaved chains per feature.  Split in three
-// so a thread can put the corner loads of several pairs in flight before it consumes any:
-// gather_prep (cell, corner indices, fractions), the 8 loads, gather_combine.
-struct GatherPrep {
-  const __half2* base;  // the level's first entry
-  uint32_t idx[8];
-  float fu, fv, fs;
-};
-
-__device__ __forceinline__ void gather_prep(uint4 L, float u, float v, float s, GatherPrep& g) {
-  const int res = (int)L.x;
-  const float r = (float)res;
-  g.base = reinterpret_cast<const __half2*>(((unsigned long long)L.w << 32) | L.z);
-  const float pu = u * r, pv = v * r, ps = s * r;
-  const int iu = min((int)pu, res - 1), iv = min((int)pv, res - 1), is = min((int)ps, res - 1);
-  corner_indices(L.y == 0u, iu, iv, is, (uint32_t)res + 1u, L.y, g.idx);
-  g.fu = pu - (float)iu;
-  g.fv = pv - (float)iv;
-  g.fs = ps - (float)is;
-}
-
-#ifndef LUMI_GATHER_LERP
-#define LUMI_GATHER_LERP 1
-#endif
-// The trilinear combination of the 8 corner entries (corner k: bit 0 = x + 1, bit 1 = y + 1,
-// bit 2 = z + 1) times the level's LOD weight, both features at once in packed fp16 -- the
-// value the renderer stores into the layer-1 A tile.  LUMI_GATHER_LERP: seven packed lerps
-// a + (b - a) f (HADD2 + HFMA2 each) instead of eight corner weights and eight products.
-__device__ __forceinline__ __half2 gather_combine_h(const __half2* e, float fu, float fv, float fs, float wl) {
-#if LUMI_GATHER_LERP
-  const __half2 hu = __float2half2_rn(fu), hv = __float2half2_rn(fv), hs = __float2half2_rn(fs);
-  const __half2 x00 = __hfma2(__hsub2(e[1], e[0]), hu, e[0]), x10 = __hfma2(__hsub2(e[3], e[2]), hu, e[2]),
-                x01 = __hfma2(__hsub2(e[5], e[4]), hu, e[4]), x11 = __hfma2(__hsub2(e[7], e[6]), hu, e[6]);
-  const __half2 y0 = __hfma2(__hsub2(x10, x00), hv, x00), y1 = __hfma2(__hsub2(x11, x01), hv, x01);
-  return __hmul2(__hfma2(__hsub2(y1, y0), hs, y0), __float2half2_rn(wl));
-#else
-  const __half2 hu = __floats2half2_rn(1.f - fu, fu);
-  const __half2 w0 = __hmul2(hu, __float2half2_rn(1.f - fv));
-  const __half2 w1 = __hmul2(hu, __float2half2_rn(fv));
-  const __half2 gs2 = __float2half2_rn(1.f - fs), fs2 = __float2half2_rn(fs);
-  const __half2 t[4] = {__hmul2(w0, gs2), __hmul2(w1, gs2), __hmul2(w0, fs2), __hmul2(w1, fs2)};
-  // both features at once in packed fp16 (HFMA2), two chains, one widening add at the end
-  __half2 c[2];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const __half2 tri = (k & 1) ? __high2half2(t[k >> 1]) : __low2half2(t[k >> 1]);
-    c[k & 1] = k < 2 ? __hmul2(e[k], tri) : __hfma2(e[k], tri, c[k & 1]);
-  }
-  const float2 x = __half22float2(c[0]), y = __half22float2(c[1]);
-  return __floats2half2_rn((x.x + y.x) * wl, (x.y + y.y) * wl);
-#endif
-}
-
-__device__ __forceinline__ float2 gather_combine(const __half2* e, float fu, float fv, float fs, float wl) {
-  return __half22float2(gather_combine_h(e, fu, fv, fs, wl));
-}
-
-__device__ __forceinline__ float2 gather_level(uint4 L, float u, float v, float s, float wl) {
-  GatherPrep g;
-  gather_prep(L, u, v, s, g);
-  __half2 e[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) e[k] = __ldg(g.base + g.idx[k]);  // one IMAD.WIDE per corner
-  return gather_combine(e, g.fu, g.fv, g.fs, wl);
 }
 
 // ---- the production gather: four levels (one 16-byte A chunk) of one sample -----------------
@@ -372,14 +313,7 @@ __device__ __forceinline__ int nth_set_bit(uint32_t m, int k) {
   return pos;
 }
 
-#ifndef LUMI_FLOAT_ACCUM
-#define LUMI_FLOAT_ACCUM 1
-#endif
-#if LUMI_FLOAT_ACCUM
 using accum_t = float;
-#else
-using accum_t = double;
-#endif
 
 // The owner-lane state of one ray of the packet.
 struct Ray {
@@ -389,9 +323,8 @@ struct Ray {
   int kept_total, contributing;
   bool term;
   double trans;
-  // the running colour / depth / opacity sums: each step is evaluated in double and, with
-  // LUMI_FLOAT_ACCUM, rounded to fp32 (5 registers fewer in the row-owning warps); the
-  // transmittance, which decides the termination cut, stays double
+  // the running colour / depth / opacity sums in fp32 (5 registers fewer in the row-owning
+  // warps than double); the transmittance, which decides the termination cut, stays double
   accum_t px, py, pz, depth, opac;
 };
 

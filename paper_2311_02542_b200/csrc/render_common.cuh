@@ -47,10 +47,6 @@ struct RenderParams {
   // kept_mask[word * total_rays + id], kept_count[id]
   uint32_t* kept_mask;
   uint16_t* kept_count;
-  // 1: kept_mask is stored transposed per 32-ray packet (ray ids packet-major, 32 per packet):
-  // word w of id pkt * 32 + c is the bitmask of the packet's rays (bit = ray lane) that keep
-  // candidate w * 32 + c -- the candidate-major view the packet renderer streams
-  int mask_transposed;
   // optional, written by the march pass for the packet renderer: fp32 direction of each ray id
   // and of its right neighbour (x + 1.5), SoA [6][total_rays], so a warp starting a packet
   // loads its rays instead of running the double-precision ray generation on its critical path
