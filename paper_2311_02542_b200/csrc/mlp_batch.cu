@@ -184,7 +184,7 @@ cudaError_t launch_mlp_batch(const MlpDev& mlp, const void* feat, const float* d
 // ---- the hash-grid gather in isolation: the attainable gather rate ----------------------
 // report the gather against a measured gather peak (the table of C1/C2 is
 // L2-resident, so HBM is the wrong denominator there).  Every thread evaluates all levels of
-// one point with the renderer's own gather_chunk4 (fp16 table, 8 corners, packed-fp16 lerps);
+// one point with the renderer's own gather_row (fp16 table, 8 corners, packed-fp16 lerps);
 // points are either uniform random (no reuse between neighbouring threads) or coherent (the
 // 32 lanes of a warp sample a small neighbourhood, like a packet of neighbouring rays).
 namespace lumi_dev {
@@ -217,27 +217,23 @@ __global__ void __launch_bounds__(256) k_gather_bench(GridDev g, int n, int cohe
     v = u01(hash32(3u * i + 2u));
     w = u01(hash32(3u * i + 3u));
   }
-  // the renderer's producer gather: four levels (32 corner loads) in flight per chunk, every
-  // level at weight 1
-  const float fl = (float)g.levels;
+  // the renderer's producer gather (pk::gather_row), every level at weight 1
   float acc = 0.f;
-#pragma unroll 1
-  for (int c = 0; 4 * c < g.levels; ++c) {
-    const uint4 q = pk::gather_chunk4(lt, 4 * c, min(4, g.levels - 4 * c), u, v, w, fl);
+  pk::gather_row(lt, g.levels, u, v, w, (float)g.levels, [&](int, uint4 q) {
     const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qs[k]));
       acc += f.x + f.y;
     }
-  }
+  });
   out[i] = acc;
 }
 
 // The production encoding of n given samples (parity of the renderer's gather, grid.h:90-114):
 // contracted positions [n][3] -> u = saturate((c + 2) / 4) as the render kernel computes it,
 // LOD weights carried as fl (w_l = saturate(fl - l), the kernel's representation), every
-// active level through pk::gather_chunk4 -> features [n][2 * levels] fp32 (zeros for w_l = 0).
+// active level through pk::gather_row -> features [n][2 * levels] fp32 (zeros for w_l = 0).
 __global__ void __launch_bounds__(256) k_encode(GridDev g, int n, const float* __restrict__ pos,
                                                 const float* __restrict__ fl,
                                                 float* __restrict__ out) {
@@ -249,23 +245,23 @@ __global__ void __launch_bounds__(256) k_encode(GridDev g, int n, const float* _
   const float u = pk::unit_below1((pos[3 * i] + 2.f) * 0.25f), v = pk::unit_below1((pos[3 * i + 1] + 2.f) * 0.25f),
               w = pk::unit_below1((pos[3 * i + 2] + 2.f) * 0.25f);
   const float f = fl[i];
-  // the renderer's producer code: chunks of four levels, the levels past this sample's last
-  // active one not loaded (weight 0 either way)
+  // the renderer's producer code (pk::gather_row): the levels past this sample's last active
+  // one are not loaded (weight 0 either way) and come out zero
   int na = 0;
   for (int l = 0; l < g.levels; ++l)
     if (__saturatef(f - (float)l) > 0.f) na = l + 1;
-  for (int c = 0; c < kMaxLevels / 4; ++c) {
-    const int nq = min(4, na - 4 * c);
-    const uint4 q4 = nq > 0 ? pk::gather_chunk4(lt, 4 * c, nq, u, v, w, f) : make_uint4(0u, 0u, 0u, 0u);
+  float* o = out + (size_t)i * 2 * g.levels;
+  for (int l = 0; l < 2 * g.levels; ++l) o[l] = 0.f;
+  pk::gather_row(lt, na, u, v, w, f, [&](int c, uint4 q4) {
     const uint32_t qs[4] = {q4.x, q4.y, q4.z, q4.w};
     for (int q = 0; q < 4; ++q) {
       const int l = 4 * c + q;
       if (l >= g.levels) break;
       const float2 r = __half22float2(*reinterpret_cast<const __half2*>(&qs[q]));
-      out[(size_t)i * 2 * g.levels + 2 * l] = r.x;
-      out[(size_t)i * 2 * g.levels + 2 * l + 1] = r.y;
+      o[2 * l] = r.x;
+      o[2 * l + 1] = r.y;
     }
-  }
+  });
 }
 
 }  // namespace mb

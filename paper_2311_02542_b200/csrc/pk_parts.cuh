@@ -105,26 +105,7 @@ __device__ __forceinline__ uint32_t pack2_relu(float lo, float hi) {
 
 // hidden-layer epilogue into TMEM: D row (64 fp32, bias included), ReLU, fp16 pairs -> the A
 // columns of this thread's lane for the next layer
-#ifndef LUMI_EPI_PAIR
-#define LUMI_EPI_PAIR 0
-#endif
 __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane) {
-#if LUMI_EPI_PAIR
-  // two 16-column loads per wait (32 values live)
-#pragma unroll
-  for (int h = 0; h < 4; h += 2) {
-    float v[32];
-    ptx::tmem_ld16(t_lane + 16 * h, v);
-    ptx::tmem_ld16(t_lane + 16 * h + 16, v + 16);
-    ptx::tmem_ld_wait();
-    uint32_t w[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) w[j] = pack2_relu(v[2 * j], v[2 * j + 1]);
-    ptx::tmem_st16(a_lane + 8 * h, w);
-  }
-  ptx::tmem_st_wait();
-  return;
-#endif
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
     float v[16];
@@ -138,7 +119,7 @@ __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane)
   ptx::tmem_st_wait();
 }
 
-// ---- the production gather: four levels (one 16-byte A chunk) of one sample -----------------
+// ---- the production gather ------------------------------------------------------------------
 // MultiResHashGrid::corners + encode (grid.h:96-113, 144-167) restated for the fp16 table:
 //  * cell and fractions of TWO levels at once in packed f32x2: p = u r rounded down (u < 1, so
 //    p < r and no clamp to res - 1 is needed), b = p + 2^23 rounded down holds floor(p) in its
@@ -146,8 +127,9 @@ __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane)
 //  * corner indices straight off those biased bits: the bias is folded into per-level addends
 //    (dense: idx = x + y V + z V^2; hashed: (x ^ y P1 ^ z P2) & mask, where the mask < 2^24
 //    strips the bias bits of x), dense corners x+1 as a +4-byte load offset;
-//  * the trilinear value as seven packed-fp16 lerps with the (fu, fv) and (fs, w_l) pairs
-//    converted once each (operand swizzles select the halves).
+//  * the trilinear value as seven packed-fp16 lerps, the fractions of two levels packed per
+//    axis (operand swizzles select the halves);
+//  * software-pipelined over level pairs (gather_row, below).
 struct LevelTab {
   float res[kMaxLevels];       // resolution as float
   uint32_t mask[kMaxLevels];   // hashed: table entries - 1; dense: 0
@@ -156,6 +138,7 @@ struct LevelTab {
   uint32_t k1[kMaxLevels];     // y addend folding the bias (and, dense, x's bias)
   uint32_t k2[kMaxLevels];     // z addend folding the bias
   unsigned long long base[kMaxLevels];  // the level's first fp16 entry pair (byte address)
+  uint32_t dense_mask;         // bit l: level l is dense
 };
 
 constexpr uint32_t kFloorBias = 0x4B000000u;  // bits of 2^23
@@ -176,6 +159,7 @@ __device__ __forceinline__ void level_tab_init(LevelTab& t, const GridDev& g, in
     t.k2[l] = dense ? 0u - kFloorBias * (V * V) : 0u - kFloorBias * 805459861u;
     t.base[l] = reinterpret_cast<unsigned long long>(g.table16 + (live ? g.offset2[l] : 0));
   }
+  if (tid == 0) t.dense_mask = g.dense_mask & ((1u << g.levels) - 1u);
 }
 
 __device__ __forceinline__ uint64_t f2pk(float a, float b) {
@@ -203,13 +187,6 @@ __device__ __forceinline__ void cell2(float a, uint64_t r2, uint32_t& b0, uint32
   f1 = ff.y;
 }
 
-__device__ __forceinline__ __half2 lerp7(const __half2* e, __half2 huv, __half2 hsw) {
-  const __half2 hu = __low2half2(huv), hv = __high2half2(huv), hs = __low2half2(hsw);
-  const __half2 x00 = __hfma2(__hsub2(e[1], e[0]), hu, e[0]), x10 = __hfma2(__hsub2(e[3], e[2]), hu, e[2]),
-                x01 = __hfma2(__hsub2(e[5], e[4]), hu, e[4]), x11 = __hfma2(__hsub2(e[7], e[6]), hu, e[6]);
-  const __half2 y0 = __hfma2(__hsub2(x10, x00), hv, x00), y1 = __hfma2(__hsub2(x11, x01), hv, x01);
-  return __hmul2(__hfma2(__hsub2(y1, y0), hs, y0), __high2half2(hsw));
-}
 
 // (a ^ b) & c in one LOP3 (immediate 0x28: (0xF0 ^ 0xCC) & 0xAA)
 __device__ __forceinline__ uint32_t xor_and(uint32_t a, uint32_t b, uint32_t c) {
@@ -250,45 +227,104 @@ __device__ __forceinline__ void corners8(const LevelTab& t, int l, uint32_t xb, 
   }
 }
 
-// Levels l0 .. l0 + 3 of one sample: (u, v, w) in [0, 1) (the caller clamps below 1), fl the LOD
-// as w_l = saturate(fl - l); nq (warp-uniform) = how many of the four levels any lane needs --
-// the others are not loaded and come out zero.  Returns the four half2 features.
-__device__ __forceinline__ uint4 gather_chunk4(const LevelTab& t, int l0, int nq, float u, float v, float w,
-                                               float fl) {
-  uint32_t xb[4], yb[4], zb[4];
-  float fu[4], fv[4], fs[4];
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const uint64_t r2 = *reinterpret_cast<const uint64_t*>(&t.res[l0 + 2 * j]);
-    cell2(u, r2, xb[2 * j], xb[2 * j + 1], fu[2 * j], fu[2 * j + 1]);
-    cell2(v, r2, yb[2 * j], yb[2 * j + 1], fv[2 * j], fv[2 * j + 1]);
-    cell2(w, r2, zb[2 * j], zb[2 * j + 1], fs[2 * j], fs[2 * j + 1]);
-  }
-  __half2 e[4][8];
-  if (nq == 4) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) corners8(t, l0 + q, xb[q], yb[q], zb[q], e[q]);
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (q < nq) {
-        corners8(t, l0 + q, xb[q], yb[q], zb[q], e[q]);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) e[q][k] = __half2{};
-      }
-    }
-  }
-  uint32_t f[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float wl = __saturatef(fl - (float)(l0 + q));
-    f[q] = h2u(lerp7(e[q], __floats2half2_rn(fu[q], fv[q]), __floats2half2_rn(fs[q], wl)));
-  }
-  return make_uint4(f[0], f[1], f[2], f[3]);
+// a hashed level's corners with the multipliers and bias addends as immediates (only the mask
+// and the base come from the table)
+__device__ __forceinline__ void corners8_hashed(const LevelTab& t, int l, uint32_t xb, uint32_t yb, uint32_t zb,
+                                                __half2* e) {
+  constexpr uint32_t P1 = 2654435761u, P2 = 805459861u;
+  constexpr uint32_t K1 = 0u - kFloorBias * P1, K2 = 0u - kFloorBias * P2;
+  const uint32_t mask = t.mask[l];
+  const uint32_t hy0 = yb * P1 + K1, hy1 = hy0 + P1;
+  const uint32_t hz0 = zb * P2 + K2, hz1 = hz0 + P2;
+  const __half2* base = reinterpret_cast<const __half2*>(t.base[l]);
+  const uint32_t xb1 = xb + 1u;
+  const uint32_t yz00 = hy0 ^ hz0, yz10 = hy1 ^ hz0, yz01 = hy0 ^ hz1, yz11 = hy1 ^ hz1;
+  e[0] = __ldg(base + xor_and(xb, yz00, mask));
+  e[1] = __ldg(base + xor_and(xb1, yz00, mask));
+  e[2] = __ldg(base + xor_and(xb, yz10, mask));
+  e[3] = __ldg(base + xor_and(xb1, yz10, mask));
+  e[4] = __ldg(base + xor_and(xb, yz01, mask));
+  e[5] = __ldg(base + xor_and(xb1, yz01, mask));
+  e[6] = __ldg(base + xor_and(xb, yz11, mask));
+  e[7] = __ldg(base + xor_and(xb1, yz11, mask));
 }
 
-// the clamp every caller of gather_chunk4 applies: [0, 1] -> [0, 1 - 2^-24]
+// ---- the production gather, software-pipelined over level pairs ------------------------------
+// Every level of one sample, two levels (one cell2) at a time, with the corner loads of the next
+// two pairs in flight while a pair is combined: the loads of pair k + 2 are issued right after
+// pair k is combined, so ~100 instructions (the next pair's combine and the following pair's
+// cells, indices and loads) separate a load from its use instead of none (+1.2 % frame rate
+// over four levels at a time with one full load wait per four).
+struct LvlPair {
+  __half2 e[2][8];
+  __half2 hu, hv, hs;  // the fractions of the pair's two levels (low half: level l, high: l + 1)
+};
+
+// cells and corner loads of levels l (even) and l + 1 (the second only if `two`, warp-uniform)
+__device__ __forceinline__ void pair_issue(const LevelTab& t, int l, bool two, float u, float v, float w,
+                                           LvlPair& q) {
+  const uint64_t r2 = *reinterpret_cast<const uint64_t*>(&t.res[l]);
+  uint32_t xb0, xb1, yb0, yb1, zb0, zb1;
+  float f0, f1;
+  cell2(u, r2, xb0, xb1, f0, f1);
+  q.hu = __floats2half2_rn(f0, f1);
+  cell2(v, r2, yb0, yb1, f0, f1);
+  q.hv = __floats2half2_rn(f0, f1);
+  cell2(w, r2, zb0, zb1, f0, f1);
+  q.hs = __floats2half2_rn(f0, f1);
+  if (((t.dense_mask >> l) & 3u) == 0u) {
+    corners8_hashed(t, l, xb0, yb0, zb0, q.e[0]);
+    if (two) corners8_hashed(t, l + 1, xb1, yb1, zb1, q.e[1]);
+  } else {
+    corners8(t, l, xb0, yb0, zb0, q.e[0]);
+    if (two) corners8(t, l + 1, xb1, yb1, zb1, q.e[1]);
+  }
+  if (!two) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q.e[1][k] = __half2{};
+  }
+}
+
+// level l + i of the pair, weighted by w_l = saturate(flc) (flc = fl - (l + i)): seven packed
+// lerps a + (b - a) f (HADD2 + HFMA2 each, both features at once) with the pair's packed
+// fractions selected by half, times w_l
+__device__ __forceinline__ uint32_t pair_combine(const LvlPair& q, int i, float flc) {
+  const __half2 hu = i ? __high2half2(q.hu) : __low2half2(q.hu);
+  const __half2 hv = i ? __high2half2(q.hv) : __low2half2(q.hv);
+  const __half2 hs = i ? __high2half2(q.hs) : __low2half2(q.hs);
+  const __half2* e = q.e[i];
+  const __half2 x00 = __hfma2(__hsub2(e[1], e[0]), hu, e[0]), x10 = __hfma2(__hsub2(e[3], e[2]), hu, e[2]),
+                x01 = __hfma2(__hsub2(e[5], e[4]), hu, e[4]), x11 = __hfma2(__hsub2(e[7], e[6]), hu, e[6]);
+  const __half2 y0 = __hfma2(__hsub2(x10, x00), hv, x00), y1 = __hfma2(__hsub2(x11, x01), hv, x01);
+  return h2u(__hmul2(__hfma2(__hsub2(y1, y0), hs, y0), __float2half2_rn(__saturatef(flc))));
+}
+
+// Levels [0, na_max) of one sample (na_max warp-uniform: the longest level count of the warp's
+// rows; a lane with fewer levels gathers the others with weight 0) -> store(c, chunk) for every
+// A chunk c = levels 4c .. 4c + 3 that holds a level; chunks past them are not stored.
+template <class Store>
+__device__ __forceinline__ void gather_row(const LevelTab& t, int na_max, float u, float v, float w, float fl,
+                                           Store&& store) {
+  const int np = (na_max + 1) >> 1;  // level pairs
+  LvlPair qa, qb;
+  if (np > 0) pair_issue(t, 0, na_max > 1, u, v, w, qa);
+  if (np > 1) pair_issue(t, 2, na_max > 3, u, v, w, qb);
+#pragma unroll 1
+  for (int c = 0; 2 * c < np; ++c) {  // chunk c: pair 2c in qa, pair 2c + 1 in qb
+    const float flc = fl - (float)(4 * c);
+    const uint32_t o0 = pair_combine(qa, 0, flc), o1 = pair_combine(qa, 1, flc - 1.f);
+    if (2 * c + 2 < np) pair_issue(t, 4 * c + 4, na_max > 4 * c + 5, u, v, w, qa);
+    uint32_t o2 = 0u, o3 = 0u;
+    if (2 * c + 1 < np) {
+      o2 = pair_combine(qb, 0, flc - 2.f);
+      o3 = pair_combine(qb, 1, flc - 3.f);
+      if (2 * c + 3 < np) pair_issue(t, 4 * c + 6, na_max > 4 * c + 7, u, v, w, qb);
+    }
+    store(c, make_uint4(o0, o1, o2, o3));
+  }
+}
+
+// the clamp every caller of gather_row applies: [0, 1] -> [0, 1 - 2^-24]
 __device__ __forceinline__ float unit_below1(float x) { return fminf(__saturatef(x), 0.99999994f); }
 
 // trunc_exp / sigmoid (network.h:41-57) with the MUFU exp2 / reciprocal: ~2 ulp, far below the

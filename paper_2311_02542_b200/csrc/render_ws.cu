@@ -58,6 +58,8 @@ static_assert(128 * WS_CONS_REGS + kProdThreads * WS_PROD_REGS <=
 // named barriers: 0 = __syncthreads (setup / teardown), LIST_READY 1 + b, GATHER_DONE 3 + b,
 // 5 = consumer warpgroup only
 constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5;
+// Producer gather: pk::gather_row, the row's levels two at a time with the next two level pairs'
+// corner loads in flight while a pair is combined.
 
 #ifdef LUMI_PHASE_TIMING
 // warp-cycles: producers [wait list, gather], consumers [fill barrier, wait gather, MLP,
@@ -96,8 +98,10 @@ struct __align__(16) Smem {
   uint32_t tmem_base;
   int stop[kStages];
   alignas(16) LevelTab lt;
-  float4 rdir[kStages][128];   // per row: ray direction xyz + neighbour direction x
-  float2 rdir2[kStages][128];  // neighbour direction yz
+  // per consumer warp, two packet slots (current / next, prefetched by cp.async): the packet's
+  // ray and neighbour directions [component][ray lane], from the march pass
+  float pdir[2][kWarps][6][32];
+  uint8_t rowslot[kStages][kWarps];  // per round and consumer warp: the slot of its rows' packet
   uint8_t na[kStages][128];    // per row: 1 = the row holds a sample
 };
 
@@ -161,6 +165,13 @@ __device__ __forceinline__ bool bar_and(bool v) {
       : "memory");
   return r != 0;
 }
+
+// 4-byte cp.async (global -> shared, L1-allocating) and its group handling
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ptx::smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // stage-indexed barriers: b < kStages
 __device__ __forceinline__ void list_ready_sync(int b) {
@@ -285,21 +296,21 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       float4 P = make_float4(0.f, 0.f, 0.f, 0.f);
       int na = 0;
       if (s.na[b][ctid]) {
-        const float4 d4 = s.rdir[b][ctid];
-        const float2 d2 = s.rdir2[b][ctid];
-        na = row_geometry(p, gc, make_float3(d4.x, d4.y, d4.z), make_float3(d4.w, d2.x, d2.y),
-                          s.rowcand[b][warp][lane], P);
+        const float(*pd)[32] = s.pdir[s.rowslot[b][warp]][warp];
+        const int rl = s.rowlane[b][ctid];
+        na = row_geometry(p, gc, make_float3(pd[0][rl], pd[1][rl], pd[2][rl]),
+                          make_float3(pd[3][rl], pd[4][rl], pd[5][rl]), s.rowcand[b][warp][lane], P);
         pcnt_levels += (unsigned)na;
       }
       const int na_max = __reduce_max_sync(FULL, (unsigned)na);
-#pragma unroll 1
-      for (int c = 0; c < kMaxLevels / 4; ++c) {  // A chunk c = levels 4c .. 4c + 3
-        uint4 out = make_uint4(0u, 0u, 0u, 0u);
-        const int nq = min(4, na_max - 4 * c);  // levels of the chunk active in some lane (uniform)
-        // a lane whose row has fewer levels than the warp's longest gathers the level anyway
-        // (a valid cell next to its neighbours') with weight 0
-        if (nq > 0) out = gather_chunk4(s.lt, 4 * c, nq, P.x, P.y, P.z, P.w);
-        st16(s.A[b], a_off(ctid, c), out);
+      {
+        uint8_t* arow = s.A[b] + a_off(ctid, 0);
+        int nst = 0;
+        gather_row(s.lt, na_max, P.x, P.y, P.z, P.w, [&](int c, uint4 q) {
+          st16(arow, (uint32_t)c * kALbo, q);
+          nst = c + 1;
+        });
+        for (int c = nst; c < kMaxLevels / 4; ++c) st16(arow, (uint32_t)c * kALbo, make_uint4(0u, 0u, 0u, 0u));
       }
       ptx::fence_async_smem();
       gather_done_arrive(b);
@@ -339,6 +350,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
     // atomic was issued)
     uint32_t next_first = 0;
     bool nf_ready = false;
+    int slot = 1;  // the current packet's direction slot (the first packet flips it to 0)
     uint32_t phase = 0;
     long long pkt_cycles = 0;  // this warp's cycles on its current packet (RowStats.ms diagnostic)
 
@@ -352,6 +364,15 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         if (!nf_ready) {
           const long long np = __shfl_sync(FULL, next_pkt, 0);
           next_first = np < total_packets ? __ldg(p.kept_mask + np * 32 + lane) : 0u;
+          if (np < total_packets) {
+            // the next packet's directions into the other slot (free: the packet that used it
+            // had every round gathered before the current one could start)
+            const size_t T = (size_t)p.total_rays;
+            const float* rd = p.ray_dirs + np * 32 + lane;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) cp_async4(&s.pdir[slot ^ 1][warp][k][lane], rd + k * T);
+            cp_async_commit();
+          }
           nf_ready = true;
         }
         while (take < 32 && !no_more && !pending) {
@@ -374,13 +395,10 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
             r.id = (int)rid;
             r.valid = px_ < p.cam.width && py_ < p.row_end;
             r.alive = r.valid;
-            if (r.valid) {
-              const size_t T = (size_t)p.total_rays;
-              const float* rd = p.ray_dirs + rid;
-              r.d = make_float3(__ldg(rd), __ldg(rd + T), __ldg(rd + 2 * T));
-              r.nd = make_float3(__ldg(rd + 3 * T), __ldg(rd + 4 * T), __ldg(rd + 5 * T));
-              ++cnt.rays;
-            }
+            if (r.valid) ++cnt.rays;
+            cp_async_wait_all();  // its directions (prefetched a round or more ago)
+            __syncwarp();
+            slot ^= 1;
             r.contributing = 0;
             r.term = false;
             r.trans = 1.0;
@@ -447,18 +465,10 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           s.rowlane[b][ctid] = (uint8_t)rl;
           __syncwarp();
         }
-        // the producers derive the row's geometry: pass its ray directions (the candidate is
-        // in rowcand) and a has-sample flag
-        const float dx = __shfl_sync(FULL, r.d.x, rl), dy = __shfl_sync(FULL, r.d.y, rl),
-                    dz = __shfl_sync(FULL, r.d.z, rl);
-        const float nx = __shfl_sync(FULL, r.nd.x, rl), ny = __shfl_sync(FULL, r.nd.y, rl),
-                    nz = __shfl_sync(FULL, r.nd.z, rl);
-        if (have) {
-          s.rdir[b][ctid] = make_float4(dx, dy, dz, nx);
-          s.rdir2[b][ctid] = make_float2(ny, nz);
-          ++cnt.evals;
-        }
+        // the producers find the row's directions by its packet slot and ray lane
+        if (have) ++cnt.evals;
         s.na[b][ctid] = have ? 1 : 0;
+        if (lane == 0) s.rowslot[b][warp] = (uint8_t)slot;
         WS_T(7);
         // all consumer warps finished (every packet stored) -> the producers stop at round j
         const bool stop = bar_and<kBarCons, 128>(no_more && !packet_live);
@@ -476,8 +486,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         gather_done_sync(bp);
         WS_T(3);
         const int rlp = s.rowlane[bp][ctid];
-        const float pdx = __shfl_sync(FULL, r.d.x, rlp), pdy = __shfl_sync(FULL, r.d.y, rlp),
-                    pdz = __shfl_sync(FULL, r.d.z, rlp);
+        const float(*pdp)[32] = s.pdir[s.rowslot[bp][warp]][warp];
+        const float pdx = pdp[0][rlp], pdy = pdp[1][rlp], pdz = pdp[2][rlp];
         float v32[32];
         if (issuer) {
           ptx::tc_fence_after();

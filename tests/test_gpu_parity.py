@@ -673,7 +673,7 @@ def test_c5_full_model_dense_band_vs_oracle(lumi, torch_cuda, oracle, full_scene
 
 @pytest.mark.parametrize("which", ["small", "full"])
 def test_production_gather_vs_oracle_encode(lumi, torch_cuda, oracle, small, full_scene, which):
-    """The renderer's own gather (pk::gather_chunk4: fp16 table copy, seven packed-fp16 lerps,
+    """The renderer's own gather (pk::gather_row: fp16 table copy, seven packed-fp16 lerps,
     the weight applied in fp16) level by level against MultiResHashGrid::encode (grid.h:90-114) in
     the oracle, on uniform random and packet-coherent points with random / edge LOD weights.
     Bound per feature: 4e-3 x w_l (fp16 table rounding 2^-11 of |entry| <= 1 plus the fp16

@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """The renderer's hash-grid gather in isolation: every level of n points through
-gather_chunk4 (the production producer gather) on the fp16 table, for the L2-resident T=2^19 table (C1/C2) and the T=2^22 table
+gather_row (the production producer gather) on the fp16 table, for the L2-resident T=2^19 table (C1/C2) and the T=2^22 table
 (C3-C5, 260 MB > L2), with packet-coherent and uniform random points.  Reports level-samples/s
 and the algorithmic gather GB/s (32 B per level-sample: 8 corners x 2 fp16 features), i.e. the
 attainable gather rate the renderer's roofline can be read against.
@@ -48,7 +48,7 @@ def main():
                 "table_MB_fp16": round(field.grid_params.nbytes / 2e6, 1), "ms": round(ms, 3),
                 "Glevel_samples_s": round(ls / 1e9, 2), "gather_GBs": round(32 * ls / 1e9, 1)}
         del dm
-    print(json.dumps({"metric": "hash-grid gather in isolation (renderer gather_chunk4, all 16 levels "
+    print(json.dumps({"metric": "hash-grid gather in isolation (renderer gather_row, all 16 levels "
                                 "per point)", "points": a.n, "results": res}))
 
 

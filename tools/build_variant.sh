@@ -11,6 +11,6 @@ for f in *.cu; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $extra \
     -I../../include "$@" -Xptxas -v -c $f -o $d/${f%.cu}.o 2> $d/${f%.cu}.ptxas.txt || { cat $d/${f%.cu}.ptxas.txt; exit 1; }
 done
-for f in *.cpp; do g++ -std=c++17 -O2 -fPIC -I../../include -c $f -o $d/${f%.cpp}.o; done
+for f in *.cpp; do g++ -std=c++17 -O2 -fPIC -pthread -I../../include -I/usr/local/cuda/include -c $f -o $d/${f%.cpp}.o; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../lib/ab/$name.so $d/*.o -lcudart
 grep -h -A2 "k_render_ws\|k_march" $d/*.ptxas.txt | grep -E "registers|spill" | head -4
