@@ -58,6 +58,12 @@ static_assert(128 * WS_CONS_REGS + kProdThreads * WS_PROD_REGS <=
 // named barriers: 0 = __syncthreads (setup / teardown), LIST_READY 1 + b, GATHER_DONE 3 + b,
 // 5 = consumer warpgroup only
 constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5;
+// WS_NO_FILL_BAR: no consumer barrier after the fill -- each consumer warp posts a done flag and
+// arrives at LIST_READY on its own, so fast warps start waiting for the gather while a slow one
+// still fills; the producers decide the stop from the four flags and pass it back with GATHER_DONE
+#ifndef WS_NO_FILL_BAR
+#define WS_NO_FILL_BAR 1
+#endif
 // Producer gather: pk::gather_row, the row's levels two at a time with the next two level pairs'
 // corner loads in flight while a pair is combined.
 
@@ -97,6 +103,9 @@ struct __align__(16) Smem {
   uint64_t wbar;  // the weight tiles' TMA bulk copy
   uint32_t tmem_base;
   int stop[kStages];
+#if WS_NO_FILL_BAR
+  uint8_t wdone[kStages][kWarps];  // per round: consumer warp w has stored its last packet
+#endif
   alignas(16) LevelTab lt;
   // per consumer warp, two packet slots (current / next, prefetched by cp.async): the packet's
   // ray and neighbour directions [component][ray lane], from the march pass
@@ -287,7 +296,18 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
     for (int j = 0;; ++j, b ^= 1) {
       list_ready_sync(b);
       WS_T(0);
+#if WS_NO_FILL_BAR
+      {
+        const bool stop = s.wdone[b][0] & s.wdone[b][1] & s.wdone[b][2] & s.wdone[b][3];
+        if (ctid == 0) s.stop[b] = stop ? 1 : 0;
+        if (stop) {  // round j holds no rows: tell the consumers through its GATHER_DONE
+          gather_done_arrive(b);
+          break;
+        }
+      }
+#else
       if (s.stop[b]) break;
+#endif
       // row ctid: its ray directions and candidate from the consumers -> grid coordinates, LOD
       // (fl) and active level count.  The 32 rows of a warp are neighbouring rays of one packet
       // at nearly the same distance, so their LOD (hence their level count) is nearly uniform
@@ -470,11 +490,16 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         s.na[b][ctid] = have ? 1 : 0;
         if (lane == 0) s.rowslot[b][warp] = (uint8_t)slot;
         WS_T(7);
+#if WS_NO_FILL_BAR
+        if (lane == 0) s.wdone[b][warp] = (no_more && !packet_live) ? 1 : 0;
+        list_ready_arrive(b);
+#else
         // all consumer warps finished (every packet stored) -> the producers stop at round j
         const bool stop = bar_and<kBarCons, 128>(no_more && !packet_live);
         if (ctid == 0) s.stop[b] = stop ? 1 : 0;
         list_ready_arrive(b);
         if (stop) stop_round = j;
+#endif
         WS_T(2);
       }
 
@@ -484,6 +509,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         // ---- M(jm): the tcgen05 MLP over round jm's 128 rows (field.h:106-137) -------------
         const int bp = b ^ 1;  // jm % kStages
         gather_done_sync(bp);
+#if WS_NO_FILL_BAR
+        if (s.stop[bp]) break;  // round jm is the first with no rows anywhere: every packet stored
+#endif
         WS_T(3);
         const int rlp = s.rowlane[bp][ctid];
         const float(*pdp)[32] = s.pdir[s.rowslot[bp][warp]][warp];
