@@ -186,10 +186,14 @@ def gather_isolated(achieved, table_log2: int):
             "note": "comparison with the isolated gather benchmark, not a hardware ceiling"}
 
 
-def ncu_kernel(kernel: str):
-    """The render kernel's entry of the committed ncu --set full summary (profiles/), if any."""
+def ncu_kernel(kernel: str, config: str = "C3"):
+    """The render kernel's entry of the committed ncu --set full summary (profiles/), if any --
+    only for the workload the capture was taken on (one C3 eye: per-launch figures do not carry
+    over to another eye size or scene)."""
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        if prof.get("workload", "C3") != config:
+            return {}
         k = dict(prof["kernels"].get(kernel) or {})
         k["_source"] = f"profiles/{prof.get('source', 'ncu_summary.json')}"
         return k
@@ -197,16 +201,16 @@ def ncu_kernel(kernel: str):
         return {}
 
 
-def ncu_traffic(kernel: str):
+def ncu_traffic(kernel: str, config: str):
     """dram bytes per launch from the committed ncu --set full capture, if any."""
-    return ncu_kernel(kernel).get("dram_bytes_per_launch")
+    return ncu_kernel(kernel, config).get("dram_bytes_per_launch")
 
 
-def issue_roofline(kernel: str, ms_per_launch: float, sm_mhz):
+def issue_roofline(kernel: str, config: str, ms_per_launch: float, sm_mhz):
     """The binding limit of the render kernel: warp-instruction issue.  ncu's executed warp
     instructions per launch of the same kernel and workload (one C3 eye) over the live
     per-launch time, against 4 issue slots per SM per clock x 148 SMs."""
-    k = ncu_kernel(kernel)
+    k = ncu_kernel(kernel, config)
     wi = k.get("warp_instructions")
     if not wi or not ms_per_launch or not sm_mhz:
         return None
@@ -500,7 +504,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": None if achieved is None else round(achieved, 1),
                      "peak": hbm, "unit": "GB/s",
                      "frac": None if achieved is None else round(achieved / hbm, 4),
-                     "traffic": ncu_traffic(kname),
+                     "traffic": ncu_traffic(kname, args.config),
                      "algorithmic": f"{bytes_per_ls} B per active (w_l>0) level-sample: 8 corners "
                                     f"x 2 features x {bytes_per_ls // 16} B "
                                     f"({'fp32 table' if dm.kernel == 'simt' else 'fp16 table copy'}); "
@@ -514,7 +518,7 @@ def run_ours(args):
                          "algorithmic": "18,944 FLOP per evaluated sample (fp16 operands; "
                                         "peak = MEASURED_PEAKS bf16 sustained, the kernel runs "
                                         "inside a long step)"},
-        "roofline_issue": issue_roofline(kname, render_ms / max(render_launches, 1),
+        "roofline_issue": issue_roofline(kname, args.config, render_ms / max(render_launches, 1),
                                          clocks.get("sm_mhz") or peaks.get("sm_max_mhz")),
         "clocks": clocks,
         "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,

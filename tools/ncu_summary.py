@@ -91,7 +91,8 @@ def main():
     total = sum(v[1] for v in share.values()) or 1
     launch_table = {k: {"launches": v[0], "ms": round(v[1], 3), "share_pct": round(v[1] / total * 100, 2)}
                     for k, v in sorted(share.items(), key=lambda t: -t[1][1])}
-    out = {"tag": tag, "source": os.path.basename(rep), "kernels": kernels,
+    out = {"tag": tag, "source": os.path.basename(rep), "workload": os.environ.get("NCU_WORKLOAD", "C3"),
+           "kernels": kernels,
            "launch_list": {"source": os.path.basename(launches), "kernels": launch_table}}
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:

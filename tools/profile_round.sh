@@ -16,7 +16,7 @@ timeout 600 python bench.py > $d/bench.json 2> $d/bench.err
 timeout 900 python bench.py --impl reference > $d/bench_ref.json 2> $d/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $d/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1 > $d/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_render_ws -c 1 -o $d/ws python tools/profile_frame.py C3 1 > $d/ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_march_mask_fast -c 1 -o $d/march python tools/profile_frame.py C3 1 > $d/ncu_march.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_march_seg -c 1 -o $d/march python tools/profile_frame.py C3 1 > $d/ncu_march.log 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:k_mlp_batch -c 1 -o $d/mlp python tools/bench_mlp.py --steps 1 > $d/ncu_mlp.log 2>&1
 timeout 900 python bench.py --config C5 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $d/c5.json 2> $d/c5.err
 LUMI_BENCH_SHARED_GPU=1 timeout 900 python bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 2 > $d/n2.json 2> $d/n2.err
