@@ -58,14 +58,12 @@ static_assert(128 * WS_CONS_REGS + kProdThreads * WS_PROD_REGS <=
 // named barriers: 0 = __syncthreads (setup / teardown), LIST_READY 1 + b, GATHER_DONE 3 + b,
 // 5 = consumer warpgroup only
 constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5;
-// WS_NO_FILL_BAR: no consumer barrier after the fill -- each consumer warp posts a done flag and
-// arrives at LIST_READY on its own, so fast warps start waiting for the gather while a slow one
-// still fills; the producers decide the stop from the four flags and pass it back with GATHER_DONE
-#ifndef WS_NO_FILL_BAR
-#define WS_NO_FILL_BAR 1
-#endif
+// No consumer barrier after the fill: each consumer warp posts a done flag and arrives at
+// LIST_READY on its own, so fast warps start waiting for the gather while a slow one still
+// fills; the producers decide the stop from the four flags and pass it back with GATHER_DONE.
 // Producer gather: pk::gather_row, the row's levels two at a time with the next two level pairs'
 // corner loads in flight while a pair is combined.
+
 
 #ifdef LUMI_PHASE_TIMING
 // warp-cycles: producers [wait list, gather], consumers [fill barrier, wait gather, MLP,
@@ -103,13 +101,14 @@ struct __align__(16) Smem {
   uint64_t wbar;  // the weight tiles' TMA bulk copy
   uint32_t tmem_base;
   int stop[kStages];
-#if WS_NO_FILL_BAR
   uint8_t wdone[kStages][kWarps];  // per round: consumer warp w has stored its last packet
-#endif
   alignas(16) LevelTab lt;
   // per consumer warp, two packet slots (current / next, prefetched by cp.async): the packet's
   // ray and neighbour directions [component][ray lane], from the march pass
   float pdir[2][kWarps][6][32];
+  // per packet slot: each ray's SH encoding (network.h:17-37) in fp16, computed when the packet
+  // starts; a row's SH block is a copy into TMEM
+  uint4 psh[2][kWarps][32][2];
   uint8_t rowslot[kStages][kWarps];  // per round and consumer warp: the slot of its rows' packet
   uint8_t na[kStages][128];    // per row: 1 = the row holds a sample
 };
@@ -139,18 +138,40 @@ __global__ void k_pack_weight_tiles(MlpDev mlp, uint8_t* img) {
   load_weight_tile(C3, c3, 3, 16, 64);
 }
 
-// layer 1 with the bias step's A from the shared ones block (LBO 128 B between its two core
-// matrices, SBO 0: every 8-row group reads the same [1 0 ... 0] rows)
-__device__ __forceinline__ void issue_layer1_shared_ones(const uint8_t* A, const uint8_t* ones,
-                                                         const uint8_t* B, uint32_t d_tmem) {
+// The shared-memory matrix descriptors of the weight tiles, the A stages and the ones block,
+// built from the CTA's layout; a K step only adds its offset to the start-address field
+struct MmaDescs {
+  uint64_t w1, f, c2, c3, ones, a[kStages];
+};
+__device__ __forceinline__ MmaDescs make_descs(const Smem& s) {
+  MmaDescs d;
+  d.w1 = ptx::make_smem_desc(ptx::smem_addr(s.W1), 128, ((32 + kKb) / 8) * 128);
+  d.f = ptx::make_smem_desc(ptx::smem_addr(s.F), 128, ((80 + kKb) / 8) * 128);
+  d.c2 = ptx::make_smem_desc(ptx::smem_addr(s.C2), 128, ((64 + kKb) / 8) * 128);
+  d.c3 = ptx::make_smem_desc(ptx::smem_addr(s.C3), 128, ((64 + kKb) / 8) * 128);
+  d.ones = ptx::make_smem_desc(ptx::smem_addr(s.ones), 128, 0);
+  for (int b = 0; b < kStages; ++b) d.a[b] = ptx::make_smem_desc(ptx::smem_addr(s.A[b]), kALbo, 128);
+  return d;
+}
+// the start-address field counts 16-byte units
+__device__ __forceinline__ uint64_t desc_at(uint64_t d, uint32_t bytes) {
+  // a 32-bit add on the low word: the 14-bit address field cannot carry out (smem < 256 KB)
+  return ((d >> 32) << 32) | (uint32_t)((uint32_t)d + (bytes >> 4));
+}
+__device__ __forceinline__ void issue_l1_pre(uint64_t a, uint64_t ones, uint64_t w1, uint32_t d_tmem) {
   constexpr uint32_t idesc = ptx::idesc_f16_f32<128, 64>();
-  constexpr uint32_t sbo = ((32 + kKb) / 8) * 128;
-  const uint32_t a = ptx::smem_addr(A), o = ptx::smem_addr(ones), b = ptx::smem_addr(B);
 #pragma unroll
   for (int kk = 0; kk < 2; ++kk)
-    ptx::mma_f16(d_tmem, ptx::make_smem_desc(a + kk * 2 * kALbo, kALbo, 128),
-                 ptx::make_smem_desc(b + kk * 256, 128, sbo), idesc, kk > 0 ? 1u : 0u);
-  ptx::mma_f16(d_tmem, ptx::make_smem_desc(o, 128, 0), ptx::make_smem_desc(b + 2 * 256, 128, sbo), idesc, 1u);
+    ptx::mma_f16(d_tmem, desc_at(a, kk * 2 * kALbo), desc_at(w1, kk * 256), idesc, kk > 0 ? 1u : 0u);
+  ptx::mma_f16(d_tmem, ones, desc_at(w1, 2 * 256), idesc, 1u);
+}
+template <int N, int K>
+__device__ __forceinline__ void issue_ts_pre(uint32_t a_tmem, uint32_t ones_tmem, uint64_t b, uint32_t d_tmem) {
+  constexpr uint32_t idesc = ptx::idesc_f16_f32<128, N>();
+#pragma unroll
+  for (int kk = 0; kk < K / 16; ++kk)
+    ptx::mma_f16_ts(d_tmem, a_tmem + kk * 8, desc_at(b, kk * 256), idesc, kk > 0 ? 1u : 0u);
+  ptx::mma_f16_ts(d_tmem, ones_tmem, desc_at(b, (K / 16) * 256), idesc, 1u);
 }
 
 // named barriers with immediate ids, so ptxas reserves only the barriers used (a register id
@@ -162,17 +183,6 @@ __device__ __forceinline__ void bar_sync() {
 template <int ID, int N>
 __device__ __forceinline__ void bar_arrive() {
   asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(N) : "memory");
-}
-template <int ID, int N>
-__device__ __forceinline__ bool bar_and(bool v) {
-  uint32_t r;
-  asm volatile(
-      "{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n bar.red.and.pred q, %2, %3, p;\n"
-      " selp.u32 %0, 1, 0, q;\n}"
-      : "=r"(r)
-      : "r"((uint32_t)v), "n"(ID), "n"(N)
-      : "memory");
-  return r != 0;
 }
 
 // 4-byte cp.async (global -> shared, L1-allocating) and its group handling
@@ -296,7 +306,6 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
     for (int j = 0;; ++j, b ^= 1) {
       list_ready_sync(b);
       WS_T(0);
-#if WS_NO_FILL_BAR
       {
         const bool stop = s.wdone[b][0] & s.wdone[b][1] & s.wdone[b][2] & s.wdone[b][3];
         if (ctid == 0) s.stop[b] = stop ? 1 : 0;
@@ -305,9 +314,6 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           break;
         }
       }
-#else
-      if (s.stop[b]) break;
-#endif
       // row ctid: its ray directions and candidate from the consumers -> grid coordinates, LOD
       // (fl) and active level count.  The 32 rows of a warp are neighbouring rays of one packet
       // at nearly the same distance, so their LOD (hence their level count) is nearly uniform
@@ -374,11 +380,11 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
     uint32_t phase = 0;
     long long pkt_cycles = 0;  // this warp's cycles on its current packet (RowStats.ms diagnostic)
 
-    int b = 0, stop_round = -1;  // b = j % kStages; stop_round: the first round with no rows
+    int b = 0;  // j % kStages
 #pragma unroll 1
     for (int j = 0;; ++j, b ^= 1) {
       const long long t_iter = clock64();
-      if (stop_round < 0) {
+      {
         // ---- F(j): this warp's rows of round j from its packet stream ---------------------
         int take = 0, rl = lane, cand = 0;
         if (!nf_ready) {
@@ -419,6 +425,15 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
             cp_async_wait_all();  // its directions (prefetched a round or more ago)
             __syncwarp();
             slot ^= 1;
+            {
+              float sh[16];
+              sh_encode(d3{(double)s.pdir[slot][warp][0][lane], (double)s.pdir[slot][warp][1][lane],
+                           (double)s.pdir[slot][warp][2][lane]}, sh);
+              s.psh[slot][warp][lane][0] = make_uint4(pack2(sh[0], sh[1]), pack2(sh[2], sh[3]),
+                                                      pack2(sh[4], sh[5]), pack2(sh[6], sh[7]));
+              s.psh[slot][warp][lane][1] = make_uint4(pack2(sh[8], sh[9]), pack2(sh[10], sh[11]),
+                                                      pack2(sh[12], sh[13]), pack2(sh[14], sh[15]));
+            }
             r.contributing = 0;
             r.term = false;
             r.trans = 1.0;
@@ -490,36 +505,28 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         s.na[b][ctid] = have ? 1 : 0;
         if (lane == 0) s.rowslot[b][warp] = (uint8_t)slot;
         WS_T(7);
-#if WS_NO_FILL_BAR
         if (lane == 0) s.wdone[b][warp] = (no_more && !packet_live) ? 1 : 0;
         list_ready_arrive(b);
-#else
-        // all consumer warps finished (every packet stored) -> the producers stop at round j
-        const bool stop = bar_and<kBarCons, 128>(no_more && !packet_live);
-        if (ctid == 0) s.stop[b] = stop ? 1 : 0;
-        list_ready_arrive(b);
-        if (stop) stop_round = j;
-#endif
         WS_T(2);
       }
 
       // the round whose MLP and compositing run now: one round behind the fill
       const int jm = j - 1;
-      if (jm >= 0 && (stop_round < 0 || jm < stop_round)) {
+      if (jm >= 0) {
         // ---- M(jm): the tcgen05 MLP over round jm's 128 rows (field.h:106-137) -------------
         const int bp = b ^ 1;  // jm % kStages
         gather_done_sync(bp);
-#if WS_NO_FILL_BAR
         if (s.stop[bp]) break;  // round jm is the first with no rows anywhere: every packet stored
-#endif
         WS_T(3);
         const int rlp = s.rowlane[bp][ctid];
-        const float(*pdp)[32] = s.pdir[s.rowslot[bp][warp]][warp];
-        const float pdx = pdp[0][rlp], pdy = pdp[1][rlp], pdz = pdp[2][rlp];
+        const uint4* shp = s.psh[s.rowslot[bp][warp]][warp][rlp];
         float v32[32];
         if (issuer) {
           ptx::tc_fence_after();
-          issue_layer1_shared_ones(s.A[bp], s.ones, s.W1, tmem);
+          {
+            const MmaDescs dd = make_descs(s);
+            issue_l1_pre(bp ? dd.a[1] : dd.a[0], dd.ones, dd.w1, tmem);
+          }
           ptx::mma_commit(&s.mbar);
         }
         ptx::mbar_wait(&s.mbar, phase);
@@ -527,11 +534,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         ptx::tc_fence_after();
         relu64_to_tmem(t_lane, a_lane);
         {
-          float sh[16];
-          sh_encode(d3{(double)pdx, (double)pdy, (double)pdz}, sh);
-          uint32_t wv[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) wv[q] = pack2(sh[2 * q], sh[2 * q + 1]);
+          const uint4 h0 = shp[0], h1 = shp[1];
+          const uint32_t wv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
           ptx::tmem_st8(t_lane + kShCol, wv);
           ptx::tmem_st_wait();
         }
@@ -539,7 +543,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         bar_sync<kBarCons, 128>();
         if (issuer) {
           ptx::tc_fence_after();
-          issue_layer_ts<80, 80>(a_tmem, ones_tmem, s.F, tmem);
+          issue_ts_pre<80, 80>(a_tmem, ones_tmem, make_descs(s).f, tmem);
           ptx::mma_commit(&s.mbar);
         }
         ptx::mbar_wait(&s.mbar, phase);
@@ -553,7 +557,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         bar_sync<kBarCons, 128>();
         if (issuer) {
           ptx::tc_fence_after();
-          issue_layer_ts<64, 64>(a_tmem, ones_tmem, s.C2, tmem);
+          issue_ts_pre<64, 64>(a_tmem, ones_tmem, make_descs(s).c2, tmem);
           ptx::mma_commit(&s.mbar);
         }
         ptx::mbar_wait(&s.mbar, phase);
@@ -564,7 +568,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         bar_sync<kBarCons, 128>();
         if (issuer) {
           ptx::tc_fence_after();
-          issue_layer_ts<16, 64>(a_tmem, ones_tmem, s.C3, tmem);
+          issue_ts_pre<16, 64>(a_tmem, ones_tmem, make_descs(s).c3, tmem);
           ptx::mma_commit(&s.mbar);
         }
         ptx::mbar_wait(&s.mbar, phase);
@@ -632,7 +636,6 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         pending = false;
         packet_live = false;
       }
-      if (stop_round >= 0 && jm + 1 >= stop_round) break;  // every round with rows composited
     }
     ptx::tc_fence_before();
     bar_sync<kBarCons, 128>();
