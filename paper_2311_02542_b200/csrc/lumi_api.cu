@@ -223,9 +223,18 @@ int get_ts(LumiModel* m, double tn, double tf, int n, const double** d_ts, doubl
     ts[0] = tn;
     ts[n - 1] = tf;
     const double r = std::pow(tf / tn, 1.0 / (n - 1));
+    // followed by the packet kernel's compositing inputs per candidate, {(float)t_i,
+    // (float)delta_i}, delta as march_ray forms it (renderer.h:209: next t minus t, the last
+    // one t (ratio - 1)) in IEEE double like the device's dsub / dmul
+    std::vector<float2> tdf(n);
+    for (int i = 0; i < n; ++i) {
+      const double dl = i + 1 < n ? ts[i + 1] - ts[i] : ts[i] * (r - 1.0);
+      tdf[i] = make_float2(static_cast<float>(ts[i]), static_cast<float>(dl));
+    }
     double* d = nullptr;
-    LUMI_CUDA_TRY(cudaMalloc(&d, sizeof(double) * n));
+    LUMI_CUDA_TRY(cudaMalloc(&d, (sizeof(double) + sizeof(float2)) * n));
     LUMI_CUDA_TRY(cudaMemcpy(d, ts.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    LUMI_CUDA_TRY(cudaMemcpy(d + n, tdf.data(), sizeof(float2) * n, cudaMemcpyHostToDevice));
     it = m->ts_cache.emplace(key, std::make_pair(d, r)).first;
   }
   *d_ts = it->second.first;
@@ -276,6 +285,7 @@ int make_params(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions
   p->occ_res = m->occ_res;
   p->occ_bias = march_occ_bias(m->occ_res);
   if ((rc = get_ts(m, cam->t_near, cam->t_far, o->samples_per_ray, &p->ts, &p->ratio))) return rc;
+  p->tdf = reinterpret_cast<const float2*>(p->ts + o->samples_per_ray);
   p->n = o->samples_per_ray;
   p->lod_enabled = o->lod_enabled ? 1 : 0;
   p->lod_bias = o->lod_bias;

@@ -20,6 +20,7 @@ struct RenderParams {
                        // copies of uniform 64-bit bases in registers)
   const double* ts;    // host-computed exponential distances (renderer.h:135-141)
   double ratio;        // host-computed pow(t_far/t_near, 1/(n-1)) (renderer.h:142)
+  const float2* tdf;   // [n] host-computed {(float)t_i, (float)delta_i} (packet kernel compositing)
   int n;               // samples_per_ray
   int lod_enabled;
   double lod_bias;

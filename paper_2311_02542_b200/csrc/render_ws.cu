@@ -220,7 +220,7 @@ struct GeomConst {
 };
 __device__ __forceinline__ int row_geometry(const RenderParams& p, const GeomConst& gc, float3 d, float3 nd,
                                             int cand, float4& out) {
-  const float t = (float)__ldg(p.ts + cand);
+  const float t = __ldg(p.tdf + cand).x;
   const float3 c = contract_f(make_float3(gc.o.x + d.x * t, gc.o.y + d.y * t, gc.o.z + d.z * t), p.contraction);
   const float u = unit_below1((c.x + 2.f) * 0.25f);  // [0, 1): the gather's cells need no clamp
   const float v = unit_below1((c.y + 2.f) * 0.25f);
@@ -520,7 +520,6 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         WS_T(3);
         const int rlp = s.rowlane[bp][ctid];
         const uint4* shp = s.psh[s.rowslot[bp][warp]][warp][rlp];
-        float v32[32];
         if (issuer) {
           ptx::tc_fence_after();
           {
@@ -549,9 +548,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         ptx::mbar_wait(&s.mbar, phase);
         phase ^= 1;
         ptx::tc_fence_after();
-        ptx::tmem_ld16(t_lane + 64, v32);
+        const float sigma_raw = ptx::tmem_ld1(t_lane + 64);
         ptx::tmem_ld_wait();
-        const float sigma = trunc_exp_fast(v32[0]);
+        const float sigma = trunc_exp_fast(sigma_raw);
         relu64_to_tmem(t_lane, a_lane);
         ptx::tc_fence_before();
         bar_sync<kBarCons, 128>();
@@ -574,14 +573,15 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         ptx::mbar_wait(&s.mbar, phase);
         phase ^= 1;
         ptx::tc_fence_after();
-        ptx::tmem_ld16(t_lane, v32);
+        float v4[4];
+        ptx::tmem_ld4(t_lane, v4);
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         {
           float rgb[3];
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
-            const float raw = v32[k];
+            const float raw = v4[k];
             rgb[k] = p.mlp.color_space == 0 ? sigmoid_fast(raw) : trunc_exp_fast(raw);
           }
           s.res[ctid] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
@@ -595,16 +595,15 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           mine &= mine - 1;
           const float4 e = s.res[warp * 32 + jj];
           const int cnd = s.rowcand[bp][warp][jj];
-          const double t = __ldg(p.ts + cnd);
-          const double delta = (cnd + 1 < p.n) ? dsub(__ldg(p.ts + cnd + 1), t) : dmul(t, dsub(p.ratio, 1.0));
+          const float2 td = __ldg(p.tdf + cnd);  // (float)t, (float)delta (host, renderer.h:209)
           // alpha and the sample's weight in fp32 (the MUFU exp: ~2 ulp, far below the fp16
           // sigma's error); the transmittance that decides the cut accumulates in double
-          const float ef = __expf(-e.x * (float)delta);
+          const float ef = __expf(-e.x * td.y);
           const float wgt = (float)r.trans * (1.f - ef);
           r.px += wgt * e.y;
           r.py += wgt * e.z;
           r.pz += wgt * e.w;
-          r.depth += wgt * (float)t;
+          r.depth += wgt * td.x;
           r.opac += wgt;
           r.trans = dmul(r.trans, (double)ef);
           ++r.contributing;
