@@ -72,19 +72,31 @@ __global__ void __launch_bounds__(128, 4) k_mlp_batch(MlpDev mlp, const __half* 
   const uint32_t a_tmem = tmem + kAcol, ones_tmem = tmem + kOnesCol, a_lane = t_lane + kAcol;
   uint32_t phase = 0;
   const int tiles = (n + 127) / 128;
+  // a tile's 32 fp16 features per row (four 16-byte vectors) and its view direction, loaded one
+  // tile ahead: the next tile's loads are in flight while this one runs through the layers
+  uint4 nf[4];
+  float ndx = 0.f, ndy = 0.f, ndz = 1.f;
+  auto load_tile = [&](int tile) {
+    const int row = tile * 128 + tid;
+    const bool have = tile < tiles && row < n;
+    const uint4* src = reinterpret_cast<const uint4*>(feat + (size_t)row * 32);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) nf[q] = have ? __ldg(src + q) : make_uint4(0, 0, 0, 0);
+    ndx = 0.f, ndy = 0.f, ndz = 1.f;
+    if (have) {
+      ndx = __ldg(dirs + 3 * (size_t)row);
+      ndy = __ldg(dirs + 3 * (size_t)row + 1);
+      ndz = __ldg(dirs + 3 * (size_t)row + 2);
+    }
+  };
+  load_tile(blockIdx.x);
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int row = tile * 128 + tid;
     const bool have = row < n;
-    // this row's 32 fp16 features -> A chunks 0..3 (four 16-byte vectors)
-    const uint4* src = reinterpret_cast<const uint4*>(feat + (size_t)row * 32);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) st16(s.A, a_off(tid, q), have ? __ldg(src + q) : make_uint4(0, 0, 0, 0));
-    float dx = 0.f, dy = 0.f, dz = 1.f;
-    if (have) {
-      dx = __ldg(dirs + 3 * (size_t)row);
-      dy = __ldg(dirs + 3 * (size_t)row + 1);
-      dz = __ldg(dirs + 3 * (size_t)row + 2);
-    }
+    for (int q = 0; q < 4; ++q) st16(s.A, a_off(tid, q), nf[q]);
+    const float dx = ndx, dy = ndy, dz = ndz;
+    load_tile(tile + gridDim.x);
     ptx::fence_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
