@@ -528,16 +528,17 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
           }
           ptx::mma_commit(&s.mbar);
         }
-        ptx::mbar_wait(&s.mbar, phase);
-        phase ^= 1;
-        ptx::tc_fence_after();
-        relu64_to_tmem(t_lane, a_lane);
         {
+          // the row's SH block into its TMEM columns while layer 1 runs (the MMA writes columns
+          // [0, 64); the previous round's fused layer, the last reader, has completed)
           const uint4 h0 = shp[0], h1 = shp[1];
           const uint32_t wv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
           ptx::tmem_st8(t_lane + kShCol, wv);
-          ptx::tmem_st_wait();
         }
+        ptx::mbar_wait(&s.mbar, phase);
+        phase ^= 1;
+        ptx::tc_fence_after();
+        relu64_to_tmem(t_lane, a_lane);  // (its store wait covers the SH block)
         ptx::tc_fence_before();
         bar_sync<kBarCons, 128>();
         if (issuer) {
@@ -548,10 +549,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         ptx::mbar_wait(&s.mbar, phase);
         phase ^= 1;
         ptx::tc_fence_after();
-        const float sigma_raw = ptx::tmem_ld1(t_lane + 64);
-        ptx::tmem_ld_wait();
-        const float sigma = trunc_exp_fast(sigma_raw);
+        const float sigma_raw = ptx::tmem_ld1(t_lane + 64);  // (the epilogue's first load wait covers it)
         relu64_to_tmem(t_lane, a_lane);
+        const float sigma = trunc_exp_fast(sigma_raw);
         ptx::tc_fence_before();
         bar_sync<kBarCons, 128>();
         if (issuer) {
