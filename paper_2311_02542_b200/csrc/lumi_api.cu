@@ -452,7 +452,8 @@ int lumi_model_create(int device, const LumiFieldDesc* desc, const float* table,
                       cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess ||
       (e = keep_pool_memory(device)) != cudaSuccess ||
-      (e = cudaMalloc(&m->d_table16, lay.total_floats * 2)) != cudaSuccess ||
+      // (+256 B: a dense level's top cell may address one corner past the level, pk::cell2)
+      (e = cudaMalloc(&m->d_table16, lay.total_floats * 2 + 256)) != cudaSuccess ||
       (e = launch_to_half(m->d_table, m->d_table16, lay.total_floats, nullptr)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess)
     return cleanup(fail(LUMI_ERR_CUDA, std::string("model upload: ") + cudaGetErrorString(e)));

@@ -121,9 +121,13 @@ __device__ __forceinline__ void relu64_to_tmem(uint32_t t_lane, uint32_t a_lane)
 
 // ---- the production gather ------------------------------------------------------------------
 // MultiResHashGrid::corners + encode (grid.h:96-113, 144-167) restated for the fp16 table:
-//  * cell and fractions of TWO levels at once in packed f32x2: p = u r rounded down (u < 1, so
-//    p < r and no clamp to res - 1 is needed), b = p + 2^23 rounded down holds floor(p) in its
-//    low mantissa bits (b = 0x4B000000 + floor(p) as an integer), f = p - (b - 2^23);
+//  * cell and fractions of TWO levels at once in packed f32x2: p = u r rounded to nearest (half
+//    the fraction error of rounding down), b = p + 2^23 rounded down holds floor(p) in its low
+//    mantissa bits (b = 0x4B000000 + floor(p) as an integer), f = p - (b - 2^23).  No clamp to
+//    res - 1: when p rounds up onto an integer k (at most r, as u < 1), the cell is k with
+//    fraction 0, which interpolates to the value of cell k - 1 at fraction 1 (the shared face's
+//    corners are the same entries; the k + 1 corners get weight exactly 0 -- hashed indices are
+//    masked into the level, a dense one at most one entry past it, inside the padded table);
 //  * corner indices straight off those biased bits: the bias is folded into per-level addends
 //    (dense: idx = x + y V + z V^2; hashed: (x ^ y P1 ^ z P2) & mask, where the mask < 2^24
 //    strips the bias bits of x), dense corners x+1 as a +4-byte load offset;
@@ -176,7 +180,7 @@ __device__ __forceinline__ float2 f2upk(uint64_t r) {
 // floor bits and fractions of coordinate a at the two resolutions r2 (levels l, l + 1)
 __device__ __forceinline__ void cell2(float a, uint64_t r2, uint32_t& b0, uint32_t& b1, float& f0, float& f1) {
   uint64_t p, b, fl, f;
-  asm("mul.rm.f32x2 %0, %1, %2;" : "=l"(p) : "l"(f2pk(a, a)), "l"(r2));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(f2pk(a, a)), "l"(r2));
   asm("add.rm.f32x2 %0, %1, %2;" : "=l"(b) : "l"(p), "l"(f2pk(8388608.f, 8388608.f)));
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(fl) : "l"(b), "l"(f2pk(-8388608.f, -8388608.f)));
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f) : "l"(p), "l"(fl));
