@@ -676,8 +676,12 @@ def test_production_gather_vs_oracle_encode(lumi, torch_cuda, oracle, small, ful
     """The renderer's own gather (pk::gather_row: fp16 table copy, seven packed-fp16 lerps,
     the weight applied in fp16) level by level against MultiResHashGrid::encode (grid.h:90-114) in
     the oracle, on uniform random and packet-coherent points with random / edge LOD weights.
-    Bound per feature: 4e-3 x w_l (fp16 table rounding 2^-11 of |entry| <= 1 plus the fp16
-    weights and sums), rms 5e-4; masked levels (w_l = 0) exactly zero, as in the reference."""
+    Bound per feature, from the error model of the fp16 arithmetic (entries |e| <= 1): the
+    table's rounding (2^-12 |e|), the cell fraction from the rounded fp32 product u r (half an
+    ulp of r, <= 2.4e-4 x |e1 - e0|), and three lerp stages of HADD2 + HFMA2 plus the weight's
+    HMUL2, each rounding to 2^-11 of values <= 2 -> <= 6e-3 x w_l worst case (measured: ~2.6e-3
+    on random points, ~4.1e-3 on the cell-face / domain-edge points below); rms 5e-4; masked
+    levels (w_l = 0) exactly zero, as in the reference."""
     torch = torch_cuda
     if which == "small":
         dm, om, levels = small["dm"], small["model"], 16
@@ -692,6 +696,14 @@ def test_production_gather_vs_oracle_encode(lumi, torch_cuda, oracle, small, ful
     coh = np.repeat(centers, 32, axis=0)
     coh[:, :2] += np.tile(off, (n_coh // 32, 1))
     pos[n_rand:] = coh
+    # edges: the domain's faces (u = 0 and u -> 1, where the kernel's nearest-rounded cell
+    # coordinate may land on res itself) and exact cell faces of every level on one axis
+    res = [int(np.floor(128 * 1.4 ** l)) for l in range(levels)]
+    faces = [4.0 * k / r - 2.0 for r in res for k in (1, r // 3, r // 2, r - 1)]
+    edge = np.array([[c, e, f] for c in (-2.0, 2.0, 1.99999, -1.99999) for e in (-2.0, 0.3, 2.0)
+                     for f in (-2.0, 2.0)] + [[x, 0.1, -0.7] for x in faces] + [[0.2, x, 1.3] for x in faces],
+                    np.float32)
+    pos = np.concatenate([pos, edge])
     fl = rng.uniform(0.0, 16.0, len(pos)).astype(np.float32)
     fl[::17] = 16.0   # every level fully active
     fl[5::17] = 1e-4  # the reference's L_eff < 0 case: only w_0 = 1e-4
@@ -711,7 +723,7 @@ def test_production_gather_vs_oracle_encode(lumi, torch_cuda, oracle, small, ful
     err = np.abs(got - want)
     assert (got[w2 == 0] == 0).all() and (want[w2 == 0] == 0).all()
     act = w2 > 0
-    bound = 4e-3 * w2
+    bound = 6e-3 * w2
     worst = float((err / np.maximum(w2, 1e-30))[act].max())
     rms = float(np.sqrt(np.mean(err[act] ** 2)))
     per_level = [float(err[:, 2 * l:2 * l + 2][act[:, 2 * l:2 * l + 2]].max(initial=0.0)) for l in range(levels)]
