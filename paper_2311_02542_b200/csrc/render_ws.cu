@@ -378,12 +378,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
     bool nf_ready = false;
     int slot = 1;  // the current packet's direction slot (the first packet flips it to 0)
     uint32_t phase = 0;
-    long long pkt_cycles = 0;  // this warp's cycles on its current packet (RowStats.ms diagnostic)
+    // the SM clock (low 32 bits) when the current packet started: its cycles at the store are the
+    // RowStats.ms diagnostic (a packet lasts far less than 2^32 cycles)
+    uint32_t pkt_t0 = 0;
 
     int b = 0;  // j % kStages
 #pragma unroll 1
     for (int j = 0;; ++j, b ^= 1) {
-      const long long t_iter = clock64();
       {
         // ---- F(j): this warp's rows of round j from its packet stream ---------------------
         int take = 0, rl = lane, cand = 0;
@@ -439,6 +440,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
             r.trans = 1.0;
             r.px = r.py = r.pz = r.depth = r.opac = 0.0;
             packet_live = true;
+            pkt_t0 = (uint32_t)clock();
             word = -1;
             g_next = word_total = 0;
             next_bits = next_first;  // (bits of invalid rays are masked by r.alive)
@@ -615,14 +617,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
       }
       WS_T(5);
       // a finished packet is stored once its last round is composited (renderer.h:233-236)
-      if (packet_live) pkt_cycles += clock64() - t_iter;
       if (pending && jm >= last_round) {
         if (p.row_cycles && (lane & (kPW - 1)) == 0) {  // one lane per packet row
           const long long pk_ = r.id >> 5;
           const int py_ = p.row_begin + (int)(pk_ / packets_x) * kPH + lane / kPW;
+          const uint32_t pkt_cycles = (uint32_t)clock() - pkt_t0;
           if (py_ < p.row_end) atomicAdd((unsigned long long*)&p.row_cycles[py_], (unsigned long long)(pkt_cycles / kPH));
         }
-        pkt_cycles = 0;
         if (r.valid) {
           const long long pk_ = r.id >> 5;
           const int px_ = (int)(pk_ % packets_x) * kPW + (lane % kPW);
