@@ -370,11 +370,15 @@ def run_ours(args):
         t_start.record()
         frames = []
         for k in range(args.steps):
-            st = drv.frame(args.warmup + k)
-            frames.append(st)
-            kernel_ms += st.worker_ms[rank]
+            # one GPU: frames are enqueued back to back (the single worker's assignment never
+            # changes); N GPUs: each frame's band times drive the next assignment
+            st = drv.frame(args.warmup + k, sync=world > 1)
+            if st is not None:
+                frames.append(st)
         t_end.record()
         torch.cuda.synchronize()
+        frames += drv.collect()
+        kernel_ms = sum(st.worker_ms[rank] for st in frames)
         if world > 1:
             dist.barrier()
     dm.set_timing(False)

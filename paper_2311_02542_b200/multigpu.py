@@ -70,9 +70,16 @@ def exchange_ms(torch, dist, ms_local: float, world: int, device) -> List[float]
     if world == 1:
         return [ms_local]
     t = torch.tensor([ms_local], dtype=torch.float64, device=device)
-    out = [torch.zeros_like(t) for _ in range(world)]
-    dist.all_gather(out, t)
-    return [float(x.item()) for x in out]
+    out = torch.empty(world, dtype=torch.float64, device=device)
+    try:
+        # one collective into one tensor, one device-to-host read: the exchange sits between
+        # two frames on every rank, so its latency is paid once per frame at any N
+        dist.all_gather_into_tensor(out, t)
+    except (RuntimeError, NotImplementedError):  # backends without the tensor form
+        parts = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        out = torch.cat(parts)
+    return out.cpu().tolist()
 
 
 def rebalance(assign: WorkerAssignment, ms: List[float], width: int,
@@ -115,6 +122,7 @@ class StereoFrameDriver:
         self.stats = torch.zeros(4, dtype=torch.int64, device=dev) if counters else None
         self.ev0 = torch.cuda.Event(enable_timing=True)
         self.ev1 = torch.cuda.Event(enable_timing=True)
+        self._pending = []  # world 1, frame(sync=False): (ev0, ev1) of frames not yet collected
         self.launches = 0
         self.history: List[FrameStats] = []
 
@@ -166,6 +174,9 @@ class StereoFrameDriver:
 
     def render_local(self, frame: int) -> None:
         """Enqueues this rank's band on the current stream (no host sync)."""
+        if self._pending:  # this frame gets its own events; the pending ones keep theirs
+            self.ev0 = self.torch.cuda.Event(enable_timing=True)
+            self.ev1 = self.torch.cuda.Event(enable_timing=True)
         stream = self.torch.cuda.current_stream().cuda_stream
         band = self.assign.ranges[self.rank]
         cams = self.cameras(frame)
@@ -191,10 +202,33 @@ class StereoFrameDriver:
         self.history.append(st)
         return st
 
-    def frame(self, frame: int) -> FrameStats:
+    def frame(self, frame: int, sync: bool = True) -> Optional[FrameStats]:
+        """One frame: render this rank's band, gather, rebalance from the band times (the
+        reference's run_frame + next_assignment, scheduler.cpp:114-162).  With one GPU the
+        assignment never changes (next_assignment of a single worker is the identity), so
+        `sync=False` only enqueues the frame -- frames run back to back on the device and
+        `collect()` returns their FrameStats once."""
+        if not sync and self.world == 1:
+            self.render_local(frame)
+            self._pending.append((self.ev0, self.ev1))
+            return None
         self.render_local(frame)
         self.gather_bands()
         return self.rebalance()
+
+    def collect(self) -> List[FrameStats]:
+        """FrameStats of the frames enqueued with frame(sync=False), in order (one host sync)."""
+        if not self._pending:
+            return []
+        self._pending[-1][1].synchronize()
+        out = []
+        for e0, e1 in self._pending:
+            ms = float(e0.elapsed_time(e1))
+            st, self.assign = rebalance(self.assign, [ms], self.W, self.damp)
+            self.history.append(st)
+            out.append(st)
+        self._pending = []
+        return out
 
     def counters(self) -> Optional[np.ndarray]:
         return None if self.stats is None else self.stats.cpu().numpy()
