@@ -112,90 +112,6 @@ __device__ __forceinline__ float fma_f32_f16(__half a, __half b, float c) {
   return d;
 }
 
-// One level from a half2 copy of the table (exact fp16 -> fp32 widening, then the same
-// float accumulation as the reference).  Used by the tensor-core renderer, whose fp16 MLP
-// operands dominate the error budget anyway (oracle: 1.59e-4 vs 1.57e-4 max |dPQ| at C1).
-__device__ __forceinline__ float2 encode_level_h(const GridDev& g, const __half2* __restrict__ t16,
-                                                 int l, double u, double v, double s, float wl) {
-  const int res = g.res[l];
-  const double r = (double)res;
-  // u, v, s arrive clamped to [0, 1] (hoisted out of the level loop by the caller)
-  const double pu = dmul(u, r), pv = dmul(v, r), ps = dmul(s, r);
-  const int iu = min(__double2int_rz(pu), res - 1), iv = min(__double2int_rz(pv), res - 1),
-            is = min(__double2int_rz(ps), res - 1);
-  uint32_t idx[8];
-  corner_indices((g.dense_mask >> l) & 1u, iu, iv, is, (uint32_t)res + 1u, g.hash_mask[l], idx);
-  const __half2* base = t16 + g.offset2[l];
-  __half2 e[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) e[k] = __ldg(base + idx[k]);
-  // Fractions exact in double; the eight trilinear weights as four packed-fp16 products
-  // (HMUL2), accumulated into fp32 with the sm_100 mixed fma.rn.f32.f16 (f16 x f16 + f32,
-  // product exact).  Oracle-measured: C1 max |dPQ| 1.60e-4 vs 1.59e-4 with fp32 weights,
-  // i.e. below the fp16 rounding of the MLP operands that follows.
-  const float fu = __double2float_rn(dsub(pu, (double)iu)),
-              fv = __double2float_rn(dsub(pv, (double)iv)),
-              fs = __double2float_rn(dsub(ps, (double)is));
-#ifdef LUMI_GATHER_FP32
-  const float gu = 1.f - fu, gv = 1.f - fv, gs = 1.f - fs;
-  const float wuv[4] = {gu * gv, fu * gv, gu * fv, fu * fv};
-  float b0 = 0.f, b1 = 0.f;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const float tri = wuv[k & 3] * ((k >> 2) ? fs : gs);
-    const float2 ef = __half22float2(e[k]);
-    b0 = fmaf(tri, ef.x, b0);
-    b1 = fmaf(tri, ef.y, b1);
-  }
-  return make_float2(b0 * wl, b1 * wl);
-#endif
-  const __half2 hu = __floats2half2_rn(1.f - fu, fu);  // (g_u, f_u)
-  const __half2 w0 = __hmul2(hu, __float2half2_rn(1.f - fv));  // k = 0,1 (y = 0)
-  const __half2 w1 = __hmul2(hu, __float2half2_rn(fv));        // k = 2,3 (y = 1)
-  const __half2 gs2 = __float2half2_rn(1.f - fs), fs2 = __float2half2_rn(fs);
-  const __half2 t[4] = {__hmul2(w0, gs2), __hmul2(w1, gs2), __hmul2(w0, fs2), __hmul2(w1, fs2)};
-  float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const __half tri = (k & 1) ? __high2half(t[k >> 1]) : __low2half(t[k >> 1]);
-    a0 = fma_f32_f16(tri, __low2half(e[k]), a0);
-    a1 = fma_f32_f16(tri, __high2half(e[k]), a1);
-  }
-  return make_float2(a0 * wl, a1 * wl);
-}
-
-// encode_level_h with fp32 grid coordinates (u, v, s in [0, 1]): cell index and fractions from
-// one FMUL per axis (the fraction pu - floor(pu) is exact in fp32).  Interpolation is
-// continuous across cells, so a boundary flip from the 2^-24 coordinate rounding moves the
-// feature by O(2^-24 * res) -- far below the fp16 weights that follow.
-__device__ __forceinline__ float2 encode_level_hf(const GridDev& g, const __half2* __restrict__ t16,
-                                                  int l, float u, float v, float s, float wl) {
-  const int res = g.res[l];
-  const float r = (float)res;
-  const float pu = u * r, pv = v * r, ps = s * r;
-  const int iu = min((int)pu, res - 1), iv = min((int)pv, res - 1), is = min((int)ps, res - 1);
-  uint32_t idx[8];
-  corner_indices((g.dense_mask >> l) & 1u, iu, iv, is, (uint32_t)res + 1u, g.hash_mask[l], idx);
-  const __half2* base = t16 + g.offset2[l];
-  __half2 e[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) e[k] = __ldg(base + idx[k]);
-  const float fu = pu - (float)iu, fv = pv - (float)iv, fs = ps - (float)is;
-  const __half2 hu = __floats2half2_rn(1.f - fu, fu);
-  const __half2 w0 = __hmul2(hu, __float2half2_rn(1.f - fv));
-  const __half2 w1 = __hmul2(hu, __float2half2_rn(fv));
-  const __half2 gs2 = __float2half2_rn(1.f - fs), fs2 = __float2half2_rn(fs);
-  const __half2 t[4] = {__hmul2(w0, gs2), __hmul2(w1, gs2), __hmul2(w0, fs2), __hmul2(w1, fs2)};
-  float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const __half tri = (k & 1) ? __high2half(t[k >> 1]) : __low2half(t[k >> 1]);
-    a0 = fma_f32_f16(tri, __low2half(e[k]), a0);
-    a1 = fma_f32_f16(tri, __high2half(e[k]), a1);
-  }
-  return make_float2(a0 * wl, a1 * wl);
-}
-
 // Full encode of one contracted point into 2*levels features (zero for masked levels,
 // which touch no memory -- grid.h:98-101).
 __device__ __forceinline__ void encode(const GridDev& g, d3 c, const LodW& lw, float* feat) {

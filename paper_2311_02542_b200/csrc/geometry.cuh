@@ -96,26 +96,7 @@ __device__ __forceinline__ double contracted_footprint(d3 o, d3 d, d3 nd, double
   return dmul(0.5, dnorm(d3{dsub(a.x, b.x), dsub(a.y, b.y), dsub(a.z, b.z)}));
 }
 
-// ---- fast variants for the tensor-core renderer ----------------------------------------
-// Contraction with one reciprocal instead of four divisions (within 1 ulp of contract()).
-__device__ __forceinline__ d3 contract_fast(d3 x, int mode) {
-  if (mode == 0) return x;
-  const double m = dlinf(x);
-  if (!(m <= 1.0)) {
-    const double inv = 1.0 / m;
-    d3 out{x.x * inv, x.y * inv, x.z * inv};
-    const double mapped = 2.0 - inv;
-    if (fabs(x.x) == m)
-      out.x = copysign(mapped, x.x);
-    else if (fabs(x.y) == m)
-      out.y = copysign(mapped, x.y);
-    else
-      out.z = copysign(mapped, x.z);
-    return out;
-  }
-  return x;
-}
-
+// contract (camera.cpp:34-49) in fp32 with one reciprocal: the producers' sample geometry
 __device__ __forceinline__ float3 contract_f(float3 x, int mode) {
   if (mode == 0) return x;
   const float m = fmaxf(fabsf(x.x), fmaxf(fabsf(x.y), fabsf(x.z)));
@@ -132,22 +113,6 @@ __device__ __forceinline__ float3 contract_f(float3 x, int mode) {
     return out;
   }
   return x;
-}
-
-// Effective LOD level L* + bias (grid.cpp:8-13, camera.cpp:68-73) from an fp32 footprint:
-// the weights are continuous in L*, and the ~1e-4 relative error of the fp32 footprint
-// moves them by less than the fp16 rounding of the features they scale.
-__device__ __forceinline__ float lod_eff_fast(d3 o, d3 d, d3 nd, double t, int mode,
-                                              float two_base, float inv_log_scale, int levels,
-                                              float bias) {
-  const float3 a = contract_f(make_float3((float)(o.x + d.x * t), (float)(o.y + d.y * t),
-                                          (float)(o.z + d.z * t)), mode);
-  const float3 b = contract_f(make_float3((float)(o.x + nd.x * t), (float)(o.y + nd.y * t),
-                                          (float)(o.z + nd.z * t)), mode);
-  const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
-  const float rc = fmaxf(0.5f * sqrtf(dx * dx + dy * dy + dz * dz), 1e-12f);
-  const float l = fminf(-__logf(two_base * rc) * inv_log_scale, (float)(levels - 1));
-  return l + bias;
 }
 
 // lod_level (grid.cpp:8-13); log_scale = std::log(per_level_scale) precomputed on the host

@@ -155,12 +155,6 @@ __device__ __forceinline__ void add_work_stats(const RenderParams& p, unsigned l
   }
 }
 
-// OccupancyGrid::is_occupied of a contracted point (occupancy.h:50-53), exact double.
-__device__ __forceinline__ bool occupied_exact(const RenderParams& p, d3 c) {
-  const int64_t vi = voxel_index(c, p.occ_res);
-  return vi >= 0 && __ldg(p.occ + vi) != 0;
-}
-
 // The occupancy test of one candidate decided in fp32 with a certified error bound:
 //
 // x = o + d t in fp32 differs from the exact value by at most ex = 8 * 2^-24 * (|o| + t)
