@@ -16,7 +16,7 @@ constexpr int kFeat = 2 * kMaxLevels;
 // MultiResHashGrid layout (grid.h:58-74) as seen by the kernels.
 struct GridDev {
   const float2* table;     // float pairs; level l starts at pair offset2[l]
-  const __half2* table16;  // the same table in fp16 pairs (tensor-core renderer)
+  const __half2* table16;  // the same table in fp16 pairs (the production gather, render_ws.cu)
   int levels;
   int res[kMaxLevels];
   uint32_t hash_mask[kMaxLevels];  // entries-1 for hashed levels

@@ -171,7 +171,7 @@ struct LumiModel {
   LumiFieldDesc desc{};
   LumiGridLayout layout{};
   float* d_table = nullptr;   // reference fp32 layout (SIMT cross-check kernel)
-  void* d_table16 = nullptr;  // half2 copy (tensor-core renderer)
+  void* d_table16 = nullptr;  // half2 copy (the production gather; padded, pk::cell2)
   float* d_dparams = nullptr;
   float* d_cparams = nullptr;
   float* d_fused = nullptr;  // density L2 folded into colour L1 (packet kernel), see fuse_l2_c1

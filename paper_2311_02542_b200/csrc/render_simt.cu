@@ -1,7 +1,7 @@
 // render_simt.cu -- reference-structured kernels: thread-per-ray fused march with the MLP
 // on CUDA cores (fp32 FFMA), and the occupancy-kept bitmask kernel.
 //
-// The SIMT renderer is the numerical baseline the tensor-core path (render_tc.cu) is
+// The SIMT renderer is the numerical baseline the tensor-core path (render_ws.cu) is
 // checked against on the GPU; the march-kept kernel produces the bit-exact, MLP-independent
 // sample index set of renderer.h:205-208.
 #include <cuda_runtime.h>
