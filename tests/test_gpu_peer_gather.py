@@ -90,3 +90,29 @@ def test_ipc_rejects_unknown_pointer():
     from paper_2311_02542_b200 import _abi
     with pytest.raises(L.Error):
         _abi.check(_abi.lib().lumi_ipc_close(0, 12345))
+
+
+def test_single_gpu_frames_back_to_back_equal_synchronous():
+    """One GPU: frames enqueued back to back (frame(sync=False) + collect(), the bench's timed
+    loop) render the same pixels as frames each followed by the band-time exchange, give one
+    FrameStats per frame in order, and keep the single worker's assignment."""
+    import torch
+    from paper_2311_02542_b200.multigpu import StereoFrameDriver
+    L, dm = _model()
+    sync = StereoFrameDriver(torch, dm, S, L.RenderOptions())
+    want = []
+    for f in range(3):
+        sync.frame(f)
+        want.append(sync.frame_buffer(f).cpu().numpy().copy())
+    drv = StereoFrameDriver(torch, dm, S, L.RenderOptions())
+    for f in range(3):  # back to back: the one frame buffer ends with the last frame
+        assert drv.frame(f, sync=False) is None
+    stats = drv.collect()
+    assert len(stats) == 3 and all(s.wall_ms > 0 for s in stats)
+    assert np.array_equal(drv.frame_buffer(2).cpu().numpy(), want[2])
+    assert [(r.begin, r.end) for r in drv.assign.ranges] == [(0, 2 * S)]
+    for f in range(3):  # and each enqueued frame alone
+        drv.frame(f, sync=False)
+        torch.cuda.synchronize()
+        assert np.array_equal(drv.frame_buffer(f).cpu().numpy(), want[f])
+    assert len(drv.collect()) == 3 and drv.collect() == []
