@@ -8,11 +8,12 @@
 // apart through double-buffered A tiles and row inputs, synchronised with named barriers (one
 // pair per buffer):
 //
-//   consumers, iteration j:  fill round j into buffer j&1 (per row: ray lane, candidate, ray
-//                            directions) -> arrive LIST_READY[j&1]
+//   consumers, iteration j:  fill round j into buffer j&1 (per row: ray lane, candidate; the
+//                            packet's directions and SH sit in a shared-memory packet slot)
+//                            -> post done flag, arrive LIST_READY[j&1] (no consumer barrier)
 //                            -> wait GATHER_DONE[(j-1)&1] -> MLP + composite of round j-1
 //   producers, iteration j:  wait LIST_READY[j&1] -> geometry + gather of round j's rows
-//                            -> arrive GATHER_DONE[j&1]
+//                            (software-pipelined over level pairs) -> arrive GATHER_DONE[j&1]
 //
 // Because round j is filled before round j-1 is composited, a packet whose stream ends is
 // stored only after the last round holding its rows is composited (one idle round per packet
@@ -20,8 +21,10 @@
 // j (they are skipped by the compositing, so the result is the reference's).
 //
 // Variants measured and rejected (DESIGN.md §4 and git history): a shared (row, level) gather
-// list, consumers gathering the coarse levels, per-warp-pair handoff, a third stage, transposed
-// mask words, producers loading the ray directions, 8 producer warps.
+// list, consumers gathering the coarse levels or a row's last level pair, per-warp-pair or
+// per-producer-warp list handoff, a third stage, transposed mask words or an expanded per-word
+// sample list, producers loading the ray directions or encoding the SH, balanced gather units,
+// two producer threads per row, the geometry on the consumers, other packet claim orders.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
