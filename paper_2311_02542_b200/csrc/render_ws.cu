@@ -109,9 +109,10 @@ struct __align__(16) Smem {
   // per consumer warp, two packet slots (current / next, prefetched by cp.async): the packet's
   // ray and neighbour directions [component][ray lane], from the march pass
   float pdir[2][kWarps][6][32];
-  // per packet slot: each ray's SH encoding (network.h:17-37) in fp16, computed when the packet
-  // starts; a row's SH block is a copy into TMEM
-  uint4 psh[2][kWarps][32][2];
+  // per consumer warp: its current packet's rays' SH encodings (network.h:17-37) in fp16,
+  // computed when the packet starts (the previous packet's rows are all composited by then); a
+  // row's SH block is a copy into TMEM
+  uint4 psh[kWarps][32][2];
   uint8_t rowslot[kStages][kWarps];  // per round and consumer warp: the slot of its rows' packet
   uint8_t na[kStages][128];    // per row: 1 = the row holds a sample
 };
@@ -433,9 +434,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
               float sh[16];
               sh_encode(d3{(double)s.pdir[slot][warp][0][lane], (double)s.pdir[slot][warp][1][lane],
                            (double)s.pdir[slot][warp][2][lane]}, sh);
-              s.psh[slot][warp][lane][0] = make_uint4(pack2(sh[0], sh[1]), pack2(sh[2], sh[3]),
+              s.psh[warp][lane][0] = make_uint4(pack2(sh[0], sh[1]), pack2(sh[2], sh[3]),
                                                       pack2(sh[4], sh[5]), pack2(sh[6], sh[7]));
-              s.psh[slot][warp][lane][1] = make_uint4(pack2(sh[8], sh[9]), pack2(sh[10], sh[11]),
+              s.psh[warp][lane][1] = make_uint4(pack2(sh[8], sh[9]), pack2(sh[10], sh[11]),
                                                       pack2(sh[12], sh[13]), pack2(sh[14], sh[15]));
             }
             r.contributing = 0;
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         if (s.stop[bp]) break;  // round jm is the first with no rows anywhere: every packet stored
         WS_T(3);
         const int rlp = s.rowlane[bp][ctid];
-        const uint4* shp = s.psh[s.rowslot[bp][warp]][warp][rlp];
+        const uint4* shp = s.psh[warp][rlp];
         if (issuer) {
           ptx::tc_fence_after();
           {
