@@ -94,7 +94,6 @@ struct __align__(16) Smem {
   uint8_t F[80 * (80 + kKb) * 2];
   uint8_t C2[64 * (64 + kKb) * 2];
   uint8_t C3[16 * (64 + kKb) * 2];
-  float4 res[128];                    // per row: sigma, rgb of the round being composited
   uint32_t ballot[kWarps][32];        // per warp: the current mask word, candidate-major
   uint16_t prefix[kWarps][33];        //   and its exclusive per-candidate sample counts
   uint32_t own[kStages][kWarps][32];  // per ray lane: the rows of the round it owns
@@ -590,7 +589,10 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
             const float raw = v4[k];
             rgb[k] = p.mlp.color_space == 0 ? sigmoid_fast(raw) : trunc_exp_fast(raw);
           }
-          s.res[ctid] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
+          // per row (sigma, rgb) for the compositing, in the first 2 KB of the round's A tile:
+          // its last reader (layer 1) has completed, and the producers refill it only after
+          // the next list handoff
+          reinterpret_cast<float4*>(s.A[bp])[ctid] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
         }
         __syncwarp();
         WS_T(4);
@@ -599,7 +601,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         while (mine && r.alive) {
           const int jj = __ffs(mine) - 1;
           mine &= mine - 1;
-          const float4 e = s.res[warp * 32 + jj];
+          const float4 e = reinterpret_cast<const float4*>(s.A[bp])[warp * 32 + jj];
           const int cnd = s.rowcand[bp][warp][jj];
           const float2 td = __ldg(p.tdf + cnd);  // (float)t, (float)delta (host, renderer.h:209)
           // alpha and the sample's weight in fp32 (the MUFU exp: ~2 ulp, far below the fp16
