@@ -91,9 +91,12 @@ def main():
     total = sum(v[1] for v in share.values()) or 1
     launch_table = {k: {"launches": v[0], "ms": round(v[1], 3), "share_pct": round(v[1] / total * 100, 2)}
                     for k, v in sorted(share.items(), key=lambda t: -t[1][1])}
-    out = {"tag": tag, "source": os.path.basename(rep), "workload": os.environ.get("NCU_WORKLOAD", "C3"),
+    # NCU_SOURCE / NCU_LAUNCHES_SOURCE: the names the capture and launch list are committed under
+    out = {"tag": tag, "source": os.environ.get("NCU_SOURCE", os.path.basename(rep)),
+           "workload": os.environ.get("NCU_WORKLOAD", "C3"),
            "kernels": kernels,
-           "launch_list": {"source": os.path.basename(launches), "kernels": launch_table}}
+           "launch_list": {"source": os.environ.get("NCU_LAUNCHES_SOURCE", os.path.basename(launches)),
+                           "kernels": launch_table}}
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
         json.dump(out, f, indent=1)
