@@ -264,7 +264,9 @@ struct LvlPair {
   __half2 hu, hv, hs;  // the fractions of the pair's two levels (low half: level l, high: l + 1)
 };
 
-// cells and corner loads of levels l (even) and l + 1 (the second only if `two`, warp-uniform)
+// cells and corner loads of levels l (even) and l + 1 (the second only if `two`, warp-uniform;
+// otherwise q.e[1] keeps what it holds -- zeros or an earlier pair's finite entries -- and the
+// level's weight 0 makes its feature 0)
 __device__ __forceinline__ void pair_issue(const LevelTab& t, int l, bool two, float u, float v, float w,
                                            LvlPair& q) {
   const uint64_t r2 = *reinterpret_cast<const uint64_t*>(&t.res[l]);
@@ -282,10 +284,6 @@ __device__ __forceinline__ void pair_issue(const LevelTab& t, int l, bool two, f
   } else {
     corners8(t, l, xb0, yb0, zb0, q.e[0]);
     if (two) corners8(t, l + 1, xb1, yb1, zb1, q.e[1]);
-  }
-  if (!two) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) q.e[1][k] = __half2{};
   }
 }
 
@@ -311,6 +309,8 @@ __device__ __forceinline__ void gather_row(const LevelTab& t, int na_max, float 
                                            Store&& store) {
   const int np = (na_max + 1) >> 1;  // level pairs
   LvlPair qa, qb;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) qa.e[1][k] = qb.e[1][k] = __half2{};  // never NaN (see pair_issue)
   if (np > 0) pair_issue(t, 0, na_max > 1, u, v, w, qa);
   if (np > 1) pair_issue(t, 2, na_max > 3, u, v, w, qb);
 #pragma unroll 1
