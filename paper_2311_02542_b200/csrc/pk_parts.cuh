@@ -267,8 +267,8 @@ struct LvlPair {
 // cells and corner loads of levels l (even) and l + 1 (the second only if `two`, warp-uniform;
 // otherwise q.e[1] keeps what it holds -- zeros or an earlier pair's finite entries -- and the
 // level's weight 0 makes its feature 0)
-__device__ __forceinline__ void pair_issue(const LevelTab& t, int l, bool two, float u, float v, float w,
-                                           LvlPair& q) {
+__device__ __forceinline__ void pair_issue(const LevelTab& t, uint32_t dense_mask, int l, bool two, float u,
+                                           float v, float w, LvlPair& q) {
   const uint64_t r2 = *reinterpret_cast<const uint64_t*>(&t.res[l]);
   uint32_t xb0, xb1, yb0, yb1, zb0, zb1;
   float f0, f1;
@@ -278,7 +278,7 @@ __device__ __forceinline__ void pair_issue(const LevelTab& t, int l, bool two, f
   q.hv = __floats2half2_rn(f0, f1);
   cell2(w, r2, zb0, zb1, f0, f1);
   q.hs = __floats2half2_rn(f0, f1);
-  if (((t.dense_mask >> l) & 3u) == 0u) {
+  if (((dense_mask >> l) & 3u) == 0u) {
     corners8_hashed(t, l, xb0, yb0, zb0, q.e[0]);
     if (two) corners8_hashed(t, l + 1, xb1, yb1, zb1, q.e[1]);
   } else {
@@ -308,21 +308,22 @@ template <class Store>
 __device__ __forceinline__ void gather_row(const LevelTab& t, int na_max, float u, float v, float w, float fl,
                                            Store&& store) {
   const int np = (na_max + 1) >> 1;  // level pairs
+  const uint32_t dm = t.dense_mask;  // read once per row (the pair issues test it per pair)
   LvlPair qa, qb;
 #pragma unroll
   for (int k = 0; k < 8; ++k) qa.e[1][k] = qb.e[1][k] = __half2{};  // never NaN (see pair_issue)
-  if (np > 0) pair_issue(t, 0, na_max > 1, u, v, w, qa);
-  if (np > 1) pair_issue(t, 2, na_max > 3, u, v, w, qb);
+  if (np > 0) pair_issue(t, dm, 0, na_max > 1, u, v, w, qa);
+  if (np > 1) pair_issue(t, dm, 2, na_max > 3, u, v, w, qb);
 #pragma unroll 1
   for (int c = 0; 2 * c < np; ++c) {  // chunk c: pair 2c in qa, pair 2c + 1 in qb
     const float flc = fl - (float)(4 * c);
     const uint32_t o0 = pair_combine(qa, 0, flc), o1 = pair_combine(qa, 1, flc - 1.f);
-    if (2 * c + 2 < np) pair_issue(t, 4 * c + 4, na_max > 4 * c + 5, u, v, w, qa);
+    if (2 * c + 2 < np) pair_issue(t, dm, 4 * c + 4, na_max > 4 * c + 5, u, v, w, qa);
     uint32_t o2 = 0u, o3 = 0u;
     if (2 * c + 1 < np) {
       o2 = pair_combine(qb, 0, flc - 2.f);
       o3 = pair_combine(qb, 1, flc - 3.f);
-      if (2 * c + 3 < np) pair_issue(t, 4 * c + 6, na_max > 4 * c + 7, u, v, w, qb);
+      if (2 * c + 3 < np) pair_issue(t, dm, 4 * c + 6, na_max > 4 * c + 7, u, v, w, qb);
     }
     store(c, make_uint4(o0, o1, o2, o3));
   }
