@@ -177,6 +177,7 @@ struct LumiModel {
   float* d_fused = nullptr;  // density L2 folded into colour L1 (packet kernel), see fuse_l2_c1
   void* d_wtiles = nullptr;  // the packet kernel's fp16 weight-tile image (TMA-staged per CTA)
   uint8_t* d_occ = nullptr;
+  uint32_t* d_occ_bits = nullptr;  // the same grid, 1 bit per voxel (the march pass)
   int occ_res = 0;
   int kernel = LUMI_KERNEL_WS;
   int num_sms = 148;
@@ -282,6 +283,7 @@ int make_params(LumiModel* m, const LumiCameraDesc* cam, const LumiRenderOptions
   p->mlp.wtiles = tma ? m->d_wtiles : nullptr;
   p->mlp.color_space = m->desc.color_space;
   p->occ = m->d_occ;
+  p->occ_bits = m->d_occ_bits;
   p->occ_res = m->occ_res;
   p->occ_bias = march_occ_bias(m->occ_res);
   if ((rc = get_ts(m, cam->t_near, cam->t_far, o->samples_per_ray, &p->ts, &p->ratio))) return rc;
@@ -487,10 +489,16 @@ int lumi_model_set_occupancy(LumiModel* m, const uint8_t* occ, int res) {
   std::vector<uint8_t> bits(n, 1);  // default all occupied (occupancy.cpp:15)
   if (occ)
     for (size_t i = 0; i < n; ++i) bits[i] = occ[i] ? 1 : 0;
+  std::vector<uint32_t> words((n + 31) / 32, 0u);
+  for (size_t i = 0; i < n; ++i) words[i >> 5] |= (uint32_t)bits[i] << (i & 31);
   if (m->d_occ) cudaFree(m->d_occ);
+  if (m->d_occ_bits) cudaFree(m->d_occ_bits);
   m->d_occ = nullptr;
+  m->d_occ_bits = nullptr;
   LUMI_CUDA_TRY(cudaMalloc(&m->d_occ, n));
   LUMI_CUDA_TRY(cudaMemcpy(m->d_occ, bits.data(), n, cudaMemcpyHostToDevice));
+  LUMI_CUDA_TRY(cudaMalloc(&m->d_occ_bits, words.size() * 4));
+  LUMI_CUDA_TRY(cudaMemcpy(m->d_occ_bits, words.data(), words.size() * 4, cudaMemcpyHostToDevice));
   m->occ_res = res;
   return LUMI_OK;
 }
@@ -505,6 +513,7 @@ int lumi_model_destroy(LumiModel* m) {
   cudaFree(m->d_fused);
   cudaFree(m->d_wtiles);
   cudaFree(m->d_occ);
+  cudaFree(m->d_occ_bits);
   for (auto& kv : m->ts_cache) cudaFree(kv.second.first);
   for (auto& a : m->ev_pool)
     for (auto x : a) cudaEventDestroy(x);

@@ -313,8 +313,15 @@ __device__ __forceinline__ void seg_word(const SegC& c, const float* __restrict_
           ok1 = ok1 && (rg & (2u << k));
         }
         uint32_t o0 = 256u, o1 = 256u;
+#ifdef LUMI_MARCH_BITS
+        // occ_adj addresses the bitfield's words: word vb >> 5, bit vb & 31 (the bias is a
+        // multiple of 2^22, so the low bits are the voxel's own)
+        if (ok0) o0 = (__ldg(reinterpret_cast<const uint32_t*>(occ_at(occ_adj, (vb0 >> 5) * 4u))) >> (vb0 & 31u)) & 1u;
+        if (ok1) o1 = (__ldg(reinterpret_cast<const uint32_t*>(occ_at(occ_adj, (vb1 >> 5) * 4u))) >> (vb1 & 31u)) & 1u;
+#else
         if (ok0) o0 = __ldg(occ_at(occ_adj, vb0));
         if (ok1) o1 = __ldg(occ_at(occ_adj, vb1));
+#endif
         ob = mad_u32(o0, 1u << k, ob);
         ob = mad_u32(o1, 2u << k, ob);
       }
@@ -434,8 +441,13 @@ __global__ void __launch_bounds__(128, LUMI_MARCH_SEG_CTAS) k_march_seg(RenderPa
   // the occupancy bytes off the biased index (p.occ_bias = kRintBits (r^2 + r + 1) mod 2^32)
   // (held in a per-thread register pair -- the lane term is zero -- so every candidate's
   // address is one IMAD.WIDE.U32 instead of a uniform-operand IADD3 pair)
+#ifdef LUMI_MARCH_BITS
+  const uint64_t occ_adj = reinterpret_cast<uint64_t>(p.occ_bits) - (uint64_t)(p.occ_bias >> 5) * 4u +
+                           (uint64_t)(p.zero & (uint32_t)lane);
+#else
   const uint64_t occ_adj = reinterpret_cast<uint64_t>(p.occ) - (uint64_t)p.occ_bias +
                            (uint64_t)(p.zero & (uint32_t)lane);
+#endif
   int count = 0;
   for (int w0 = 0; w0 < p.mask_words; ++w0) {
     const int base = w0 * 32, hi = min(32, p.n - base);

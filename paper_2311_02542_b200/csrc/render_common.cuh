@@ -14,6 +14,7 @@ struct RenderParams {
   GridDev grid;
   MlpDev mlp;
   const uint8_t* occ;  // occ_res^3 bytes
+  const uint32_t* occ_bits;  // the same grid as a bitfield: voxel i is bit i & 31 of word i >> 5
   int occ_res;
   uint32_t occ_bias;   // march_occ_bias(occ_res): the segment march pass's biased voxel index
   uint32_t zero;       // always 0 (a value the compiler cannot prove uniform: keeps per-thread
