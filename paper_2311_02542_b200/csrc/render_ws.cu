@@ -73,6 +73,8 @@ constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5;
 // warp-cycles: producers [wait list, gather], consumers [fill barrier, wait gather, MLP,
 // composite, stream fill, row handoff]
 __device__ unsigned long long g_ws_cycles[8];
+// [rounds with rows (per CTA), rows holding a sample, warp-rounds with no row, packets stored]
+__device__ unsigned long long g_ws_rows[4];
 #define WS_T(k)                                                    \
   do {                                                             \
     const long long _t = clock64();                                \
@@ -510,6 +512,16 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         }
         // the producers find the row's directions by its packet slot and ray lane
         if (have) ++cnt.evals;
+#ifdef LUMI_PHASE_TIMING
+        {
+          const unsigned nh = __popc(__ballot_sync(FULL, have));
+          if (lane == 0) {
+            atomicAdd(&g_ws_rows[1], (unsigned long long)nh);
+            if (nh == 0) atomicAdd(&g_ws_rows[2], 1ull);
+            if (warp == 0) atomicAdd(&g_ws_rows[0], 1ull);
+          }
+        }
+#endif
         s.na[b][ctid] = have ? 1 : 0;
         if (lane == 0) s.rowslot[b][warp] = (uint8_t)slot;
         WS_T(7);
@@ -644,6 +656,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
         }
         pending = false;
         packet_live = false;
+#ifdef LUMI_PHASE_TIMING
+        if (lane == 0) atomicAdd(&g_ws_rows[3], 1ull);
+#endif
       }
     }
     ptx::tc_fence_before();
@@ -734,6 +749,7 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
 #ifdef LUMI_PHASE_TIMING
   unsigned long long z6[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpyToSymbolAsync(ws::g_ws_cycles, z6, sizeof(z6), 0, cudaMemcpyHostToDevice, s);
+  cudaMemcpyToSymbolAsync(ws::g_ws_rows, z6, sizeof(ws::g_ws_rows), 0, cudaMemcpyHostToDevice, s);
 #endif
   ws::k_render_ws<<<(unsigned)grid, ws::kCtaThreads, smem, s>>>(p);
 #ifdef LUMI_PHASE_TIMING
@@ -746,6 +762,11 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
                  "row handoff %.1f%% fill barrier %.1f%% wait gather %.1f%% mlp %.1f%% composite %.1f%%\n",
                  100 * c[0] / tp, 100 * c[1] / tp, 100 * c[6] / tc, 100 * c[7] / tc, 100 * c[2] / tc,
                  100 * c[3] / tc, 100 * c[4] / tc, 100 * c[5] / tc);
+    unsigned long long rw[4];
+    cudaMemcpyFromSymbol(rw, ws::g_ws_rows, sizeof(rw));
+    std::fprintf(stderr, "[lumi] ws rounds %llu, rows with a sample %llu (%.1f%% of 128 per round), "
+                 "warp-rounds with no row %llu (%.1f%%), packets %llu\n", rw[0], rw[1],
+                 100.0 * rw[1] / (128.0 * rw[0]), rw[2], 100.0 * rw[2] / (4.0 * rw[0]), rw[3]);
   }
 #endif
   if (ev) cudaEventRecord(ev[2], s);
