@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <vector>
 
 #include "kernels.h"
 #include "pk_parts.cuh"
@@ -75,6 +76,8 @@ constexpr int kBarList = 1, kBarGather = 3, kBarCons = 5;
 __device__ unsigned long long g_ws_cycles[8];
 // [rounds with rows (per CTA), rows holding a sample, warp-rounds with no row, packets stored]
 __device__ unsigned long long g_ws_rows[4];
+// per consumer warp: globaltimer at its start and when it leaves the round loop
+__device__ unsigned long long g_ws_t[2][4096];
 #define WS_T(k)                                                    \
   do {                                                             \
     const long long _t = clock64();                                \
@@ -354,6 +357,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
   } else {
     // ================================ consumers ==============================================
     if (tma_weights) ptx::mbar_wait(&s.wbar, 0);  // the weight tiles have landed
+#ifdef LUMI_PHASE_TIMING
+    if (lane == 0 && blockIdx.x * 4 + warp < 4096) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_ws_t[0][blockIdx.x * 4 + warp] = t;
+    }
+#endif
     const uint32_t t_lane = tmem + ((uint32_t)(warp * 32) << 16);
     {
       const uint32_t ones[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -661,6 +671,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm) k_render_ws(RenderPar
 #endif
       }
     }
+#ifdef LUMI_PHASE_TIMING
+    if (lane == 0 && blockIdx.x * 4 + warp < 4096) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_ws_t[1][blockIdx.x * 4 + warp] = t;
+    }
+#endif
     ptx::tc_fence_before();
     bar_sync<kBarCons, 128>();
     ptx::tc_fence_after();
@@ -767,6 +784,19 @@ cudaError_t launch_render_ws(RenderParams p, cudaStream_t s, int num_sms, cudaEv
     std::fprintf(stderr, "[lumi] ws rounds %llu, rows with a sample %llu (%.1f%% of 128 per round), "
                  "warp-rounds with no row %llu (%.1f%%), packets %llu\n", rw[0], rw[1],
                  100.0 * rw[1] / (128.0 * rw[0]), rw[2], 100.0 * rw[2] / (4.0 * rw[0]), rw[3]);
+    // the launch's tail: consumer warps that ran out of packets before the last one finished
+    static unsigned long long tt[2][4096];
+    cudaMemcpyFromSymbol(tt, ws::g_ws_t, sizeof(tt));
+    const int nw = (int)std::min<long long>(4 * grid, 4096);
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (int i = 0; i < nw; ++i) { t0 = std::min(t0, tt[0][i]); t1 = std::max(t1, tt[1][i]); }
+    double idle = 0.0;
+    std::vector<double> ends(nw);
+    for (int i = 0; i < nw; ++i) { idle += (double)(t1 - tt[1][i]); ends[i] = (double)(tt[1][i] - t0) * 1e-3; }
+    std::sort(ends.begin(), ends.end());
+    std::fprintf(stderr, "[lumi] ws tail: span %.1f us, warps done at p1 %.1f / p50 %.1f / max %.1f us, "
+                 "idle warp-time after their last packet %.2f%%\n", (t1 - t0) * 1e-3, ends[nw / 100],
+                 ends[nw / 2], ends[nw - 1], 100.0 * idle / ((double)nw * (double)(t1 - t0)));
   }
 #endif
   if (ev) cudaEventRecord(ev[2], s);
