@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="target CPU time of the reference baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="frames of the end-to-end leg (default: --steps, the timed frames)")
     ap.add_argument("--no-checkpoint", action="store_true",
                     help="build the scene in memory instead of through a LUMICKPT round trip")
     return ap.parse_args()
@@ -402,7 +403,9 @@ def run_ours(args):
     fps = args.steps / sec
 
     # ---- end to end through the public API with host buffers -------------------------
-    e2e_steps = max(1, args.e2e_steps)
+    # the end-to-end leg renders the same head-path frames as the timed region (frame cost
+    # varies along the path), so the two numbers differ only by what e2e adds
+    e2e_steps = max(1, args.e2e_steps if args.e2e_steps is not None else args.steps)
     d2h = 3 * rays_frame * 4
     h2d = 2 * (C.sizeof(_abi.CameraDesc) + C.sizeof(_abi.RenderOptionsDesc))
     if world == 1:
